@@ -1,0 +1,186 @@
+/* exsum_b200.h — C ABI of the B200-native exact float64 summation library.
+ *
+ * Drop-in boundary for the reference's summation path.  The
+ * reference exposes a C++ class API only (no C ABI, no FFI); every entry point
+ * below names the reference symbol it replaces.  Paths are relative to
+ * /root/reference/proj.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ *   - Every function that can fail returns an int status (EXSUM_OK == 0) and
+ *     never throws; the reference throws std::invalid_argument instead
+ *     (small_accumulator.cpp:351-353, vector_ops.cpp:150-160).
+ *   - Accumulators are caller-owned values (exsum_small) or opaque handles
+ *     (exsum_large, exsum_context).  No global mutable state; functions are
+ *     reentrant for distinct accumulators / workspaces / streams.
+ *   - Device entry points (exsum_cuda_*) are stream-ordered and asynchronous:
+ *     pointers prefixed d_ are device pointers, `stream` is a cudaStream_t
+ *     passed as void* (0 = legacy default stream).
+ */
+#ifndef EXSUM_B200_H_
+#define EXSUM_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ----------------------------------------------------------------- status */
+#define EXSUM_OK 0
+#define EXSUM_EINVAL 1 /* bad argument (mean with n == 0, null pointer, length mismatch) */
+#define EXSUM_ECUDA 2  /* a CUDA runtime call failed (no device, launch failure, ...) */
+#define EXSUM_ENOMEM 3 /* allocation failed / workspace too small */
+
+/* -------------------------------------------------------------- geometry */
+/* small_accumulator.hpp:27-35 and large_accumulator.hpp:27-29 */
+#define EXSUM_SMALL_CHUNKS 67      /* kSmallChunks: chunk i weighs 2^(32 i - 1075) */
+#define EXSUM_SMALL_CARRY_TERMS 2047 /* kSmallCarryTerms: adds between propagations */
+#define EXSUM_LARGE_CHUNKS 4096    /* kLargeChunks: one per sign+exponent */
+#define EXSUM_NO_INDEX UINT64_MAX  /* "no such special value" in exsum_partial */
+
+/* The small superaccumulator as a plain value.  Byte-for-byte the layout of
+ * exsum::SmallAccumulator (small_accumulator.hpp:99-102: chunks_, inf_bits_,
+ * nan_bits_, adds_until_propagate_), standard-layout, 560 bytes. */
+typedef struct exsum_small {
+  int64_t chunk[EXSUM_SMALL_CHUNKS];
+  uint64_t inf_bits;            /* bit pattern of an absorbed infinity, 0 if none */
+  uint64_t nan_bits;            /* bit pattern of the first absorbed NaN, 0 if none */
+  int32_t adds_until_propagate; /* in [0, 2047] */
+  int32_t reserved_;            /* padding, keep 0 */
+} exsum_small;
+
+/* A shard's exact sum as it leaves a device: the canonical (carry-propagated)
+ * small accumulator plus the index-ordered special-value record that makes the
+ * Inf/NaN outcome independent of how the array was sharded.
+ * Indices are GLOBAL positions in the logical array (base_index + local). */
+typedef struct exsum_partial {
+  exsum_small acc;        /* canonical chunks; inf/nan bits as serial add order gives */
+  uint64_t first_pos_inf; /* global index of the first +Inf, EXSUM_NO_INDEX if none */
+  uint64_t first_neg_inf; /* global index of the first -Inf */
+  uint64_t first_nan;     /* global index of the first NaN */
+  uint64_t nan_payload;   /* bit pattern of the NaN at first_nan (0 if none) */
+} exsum_partial;
+
+/* ---------------------------------------------- host small superaccumulator */
+/* SmallAccumulator() — small_accumulator.hpp:49,99-102; SPEC small_new */
+int exsum_small_init(exsum_small *acc);
+/* SmallAccumulator::add(double) — small_accumulator.cpp:165-172; SPEC small_add */
+int exsum_small_add(exsum_small *acc, double v);
+/* SmallAccumulator::add(span) — small_accumulator.cpp:174-189; SPEC small_add_array */
+int exsum_small_add_array(exsum_small *acc, const double *x, size_t n);
+/* SmallAccumulator::add_inf_nan — small_accumulator.cpp:230-242; SPEC small_add_inf_nan */
+int exsum_small_add_inf_nan(exsum_small *acc, uint64_t bits);
+/* SmallAccumulator::carry_propagate — small_accumulator.cpp:244-303.  Returns the
+ * index of the top nonzero chunk, -1 for an exact zero (or for acc == NULL). */
+int exsum_small_carry_propagate(exsum_small *acc);
+/* SmallAccumulator::merge — small_accumulator.cpp:305-328; SPEC small_merge */
+int exsum_small_merge(exsum_small *dst, const exsum_small *src);
+/* SmallAccumulator::round — small_accumulator.cpp:330-348; SPEC small_round */
+int exsum_small_round(exsum_small *acc, double *out);
+/* SmallAccumulator::mean — small_accumulator.cpp:350-421; EXSUM_EINVAL for n == 0 */
+int exsum_small_mean(exsum_small *acc, uint64_t n, double *out);
+
+/* ---------------------------------------------- host large superaccumulator */
+typedef struct exsum_large exsum_large; /* opaque; ~42 KB, see large_accumulator.hpp:99-103 */
+/* LargeAccumulator() — large_accumulator.cpp:22-26; SPEC large_new */
+exsum_large *exsum_large_new(void);
+void exsum_large_free(exsum_large *acc);
+/* LargeAccumulator::add(double) — large_accumulator.hpp:47-59; SPEC large_add */
+int exsum_large_add(exsum_large *acc, double v);
+/* LargeAccumulator::add(span) — large_accumulator.cpp:28-32; SPEC large_add_array */
+int exsum_large_add_array(exsum_large *acc, const double *x, size_t n);
+/* LargeAccumulator::drain — large_accumulator.cpp:113-131; SPEC large_drain */
+int exsum_large_drain(exsum_large *acc);
+/* LargeAccumulator::round — large_accumulator.cpp:133-136; SPEC large_round */
+int exsum_large_round(exsum_large *acc, double *out);
+/* LargeAccumulator::mean — large_accumulator.cpp:138-141 */
+int exsum_large_mean(exsum_large *acc, uint64_t n, double *out);
+/* LargeAccumulator::small() — large_accumulator.hpp:75-76 (copy out) */
+int exsum_large_small(const exsum_large *acc, exsum_small *out);
+/* LargeAccumulator::chunks_in_use — large_accumulator.cpp:143-149 */
+int exsum_large_chunks_in_use(const exsum_large *acc);
+
+/* ---------------------------------------------------- partial records (host) */
+/* Exact sum of x[0..n) into a partial record (host code; the record format the
+ * device path and the multi-GPU exchange use).  base_index is the global index
+ * of x[0]. */
+int exsum_partial_from_array(const double *x, size_t n, uint64_t base_index,
+                             exsum_partial *out);
+/* Merge of k partial records: the combine step of parallel_exact_sum
+ * (vector_ops.cpp:64-70) with index-ordered special values.  Writes the merged
+ * canonical record (may alias parts[0]) and/or the rounded result. */
+int exsum_partial_merge(const exsum_partial *parts, size_t k, exsum_partial *out,
+                        double *result);
+/* Rounded value of a partial record (SmallAccumulator::round on its acc). */
+int exsum_partial_round(const exsum_partial *p, double *out);
+
+/* ----------------------------------------------------------- device path */
+/* Device workspace: accumulation state that persists across the stream-ordered
+ * launches of one sum (67 chunk sums, special-value indices, counters).  Zero it
+ * once with exsum_cuda_workspace_init; every finalizing call leaves it zeroed. */
+size_t exsum_cuda_workspace_bytes(void);
+int exsum_cuda_workspace_init(void *d_ws, size_t ws_bytes, void *stream);
+
+/* exact_sum(values, ExactMethod::large) — vector_ops.cpp:121-130, with
+ * LargeAccumulator() + add(span) + drain + SmallAccumulator::round
+ * (large_accumulator.cpp:22-136, small_accumulator.cpp:244-348) as ONE launch:
+ * K1 streaming accumulate, K2 per-CTA flush, K3 grid combine + round.
+ * d_x: n doubles (any 8-byte alignment).  base_index: global index of d_x[0]
+ * (0 for a whole array; the shard offset in a multi-GPU sum).  Outputs (either
+ * may be NULL): d_result (1 double), d_partial (1 exsum_partial). */
+int exsum_cuda_sum(const double *d_x, size_t n, uint64_t base_index, double *d_result,
+                   exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream);
+
+/* Incremental form (LargeAccumulator::add(span) across calls, large_accumulator.hpp:61):
+ * accumulate d_x into the workspace without rounding; then finalize. */
+int exsum_cuda_accumulate(const double *d_x, size_t n, uint64_t base_index, void *d_ws,
+                          size_t ws_bytes, void *stream);
+int exsum_cuda_finalize(double *d_result, exsum_partial *d_partial, void *d_ws,
+                        size_t ws_bytes, void *stream);
+
+/* One exact_sum per segment: segment i is d_x[d_offsets[i] .. d_offsets[i+1]).
+ * d_offsets has nseg + 1 nondecreasing entries.  No reference batch API exists;
+ * semantics = exact_sum(segment_i) for every i.
+ * d_partials may be NULL; otherwise nseg records, indices local to the segment. */
+int exsum_cuda_sum_segmented(const double *d_x, const uint64_t *d_offsets, size_t nseg,
+                             double *d_out, exsum_partial *d_partials, void *d_ws,
+                             size_t ws_bytes, void *stream);
+
+/* Merge k partial records resident on the device (after an all-gather of the
+ * shards' records): parallel_exact_sum's merge phase, vector_ops.cpp:64-70. */
+int exsum_cuda_merge(const exsum_partial *d_parts, size_t k, double *d_result,
+                     exsum_partial *d_out, void *stream);
+
+/* ------------------------------------------------ host-buffer convenience */
+/* A device context: workspace, pinned-free staging ring, copy + compute streams.
+ * exsum_context_sum is exact_sum(values) for a HOST array: host->device copies
+ * pipelined against the device accumulate, result copied back.  Blocking. */
+typedef struct exsum_context exsum_context;
+exsum_context *exsum_context_create(int device, size_t staging_bytes);
+void exsum_context_free(exsum_context *ctx);
+int exsum_context_sum(exsum_context *ctx, const double *h_x, size_t n, double *h_result,
+                      exsum_partial *h_partial);
+
+/* --------------------------------------------------- synthetic data (bench) */
+/* Seeded counter-based generators for the BASELINE.json configs (SURVEY.md
+ * §8(d)); the value at index i depends only on (config, seed, i, n), so shards
+ * generate independently.  config: 1..4 (config 5 values: exsum_cuda_gen_segmented). */
+int exsum_cuda_gen(int config, uint64_t seed, uint64_t n_total, uint64_t first,
+                   size_t count, double *d_out, void *stream);
+int exsum_host_gen(int config, uint64_t seed, uint64_t n_total, uint64_t first,
+                   size_t count, double *out);
+/* Config 5: nseg segment lengths log-uniform in [lo, hi]; offsets (nseg+1). */
+int exsum_host_gen_offsets(uint64_t seed, size_t nseg, uint64_t lo, uint64_t hi,
+                           uint64_t *offsets);
+int exsum_cuda_gen_segmented(uint64_t seed, uint64_t n_total, double *d_out, void *stream);
+
+/* Library build/version info: "exsum_b200 <version> sm_100a". */
+const char *exsum_version(void);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* EXSUM_B200_H_ */

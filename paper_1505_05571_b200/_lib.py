@@ -1,0 +1,116 @@
+"""ctypes binding of ``lib/libexsum_b200.so`` (declared in include/exsum_b200.h).
+
+The library is the product; this module only declares its C ABI.  Importing it
+raises if the shared library is missing, so no caller can silently fall back to
+a Python or CPU implementation of the device path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "lib" / "libexsum_b200.so"
+
+EXSUM_OK, EXSUM_EINVAL, EXSUM_ECUDA, EXSUM_ENOMEM = 0, 1, 2, 3
+SMALL_CHUNKS = 67
+NO_INDEX = (1 << 64) - 1
+
+_STATUS_NAMES = {EXSUM_EINVAL: "EXSUM_EINVAL", EXSUM_ECUDA: "EXSUM_ECUDA",
+                 EXSUM_ENOMEM: "EXSUM_ENOMEM"}
+
+
+class ExsumSmall(C.Structure):
+    """``exsum_small``: layout of exsum::SmallAccumulator (small_accumulator.hpp:99-102)."""
+
+    _fields_ = [("chunk", C.c_int64 * SMALL_CHUNKS), ("inf_bits", C.c_uint64),
+                ("nan_bits", C.c_uint64), ("adds_until_propagate", C.c_int32),
+                ("reserved_", C.c_int32)]
+
+
+class ExsumPartial(C.Structure):
+    """``exsum_partial``: canonical accumulator + index-ordered Inf/NaN record."""
+
+    _fields_ = [("acc", ExsumSmall), ("first_pos_inf", C.c_uint64),
+                ("first_neg_inf", C.c_uint64), ("first_nan", C.c_uint64),
+                ("nan_payload", C.c_uint64)]
+
+
+assert C.sizeof(ExsumSmall) == 560
+assert C.sizeof(ExsumPartial) == 592
+
+
+class ExsumError(RuntimeError):
+    def __init__(self, fn: str, status: int):
+        super().__init__(f"{fn} failed: {_STATUS_NAMES.get(status, status)}")
+        self.status = status
+
+
+def _load() -> C.CDLL:
+    if not LIB_PATH.exists():
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_1505_05571_b200.build` "
+            "(the exact-sum path has no CPU fallback)")
+    return C.CDLL(str(LIB_PATH))
+
+
+lib = _load()
+
+_vp, _sz, _u64, _i32 = C.c_void_p, C.c_size_t, C.c_uint64, C.c_int
+_dp = C.POINTER(C.c_double)
+_sp = C.POINTER(ExsumSmall)
+_pp = C.POINTER(ExsumPartial)
+
+# name: (restype, argtypes)
+_SIGNATURES = {
+    "exsum_small_init": (_i32, [_sp]),
+    "exsum_small_add": (_i32, [_sp, C.c_double]),
+    "exsum_small_add_array": (_i32, [_sp, _vp, _sz]),
+    "exsum_small_add_inf_nan": (_i32, [_sp, _u64]),
+    "exsum_small_carry_propagate": (_i32, [_sp]),
+    "exsum_small_merge": (_i32, [_sp, _sp]),
+    "exsum_small_round": (_i32, [_sp, _dp]),
+    "exsum_small_mean": (_i32, [_sp, _u64, _dp]),
+    "exsum_large_new": (_vp, []),
+    "exsum_large_free": (None, [_vp]),
+    "exsum_large_add": (_i32, [_vp, C.c_double]),
+    "exsum_large_add_array": (_i32, [_vp, _vp, _sz]),
+    "exsum_large_drain": (_i32, [_vp]),
+    "exsum_large_round": (_i32, [_vp, _dp]),
+    "exsum_large_mean": (_i32, [_vp, _u64, _dp]),
+    "exsum_large_small": (_i32, [_vp, _sp]),
+    "exsum_large_chunks_in_use": (_i32, [_vp]),
+    "exsum_partial_from_array": (_i32, [_vp, _sz, _u64, _pp]),
+    "exsum_partial_merge": (_i32, [_pp, _sz, _pp, _dp]),
+    "exsum_partial_round": (_i32, [_pp, _dp]),
+    "exsum_cuda_workspace_bytes": (_sz, []),
+    "exsum_cuda_workspace_init": (_i32, [_vp, _sz, _vp]),
+    "exsum_cuda_sum": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "exsum_cuda_accumulate": (_i32, [_vp, _sz, _u64, _vp, _sz, _vp]),
+    "exsum_cuda_finalize": (_i32, [_vp, _vp, _vp, _sz, _vp]),
+    "exsum_cuda_sum_segmented": (_i32, [_vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp]),
+    "exsum_cuda_merge": (_i32, [_vp, _sz, _vp, _vp, _vp]),
+    "exsum_context_create": (_vp, [_i32, _sz]),
+    "exsum_context_free": (None, [_vp]),
+    "exsum_context_sum": (_i32, [_vp, _vp, _sz, _dp, _pp]),
+    "exsum_cuda_gen": (_i32, [_i32, _u64, _u64, _u64, _sz, _vp, _vp]),
+    "exsum_host_gen": (_i32, [_i32, _u64, _u64, _u64, _sz, _vp]),
+    "exsum_host_gen_offsets": (_i32, [_u64, _sz, _u64, _u64, _vp]),
+    "exsum_cuda_gen_segmented": (_i32, [_u64, _u64, _vp, _vp]),
+    "exsum_version": (C.c_char_p, []),
+}
+
+for _name, (_res, _args) in _SIGNATURES.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+EXPORTED = tuple(_SIGNATURES)
+
+
+def check(fn: str, status: int) -> None:
+    if status != EXSUM_OK:
+        raise ExsumError(fn, status)
+
+
+def call(fn: str, *args) -> None:
+    check(fn, getattr(lib, fn)(*args))

@@ -1,0 +1,70 @@
+"""In-tree build of the native library ``lib/libexsum_b200.so`` (sm_100a).
+
+Compiles the CUDA sources with ``nvcc -gencode arch=compute_100a,code=sm_100a
+-lineinfo -O3`` and the host C++ with g++, links one shared library with a
+static CUDA runtime (so it does not depend on the toolkit's libcudart at run
+time), and leaves it next to this file so it travels with the repo snapshot.
+nvcc cross-compiles: no GPU is needed to build.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+INCLUDE = ROOT / "include"
+BUILD = PKG / "_build"
+LIB = PKG / "lib" / "libexsum_b200.so"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = "/usr/bin/g++"
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CU_SOURCES = ["sum_kernels.cu", "synth.cu", "context.cu"]
+CXX_SOURCES = ["host_accumulators.cpp"]
+HEADERS = [CSRC / "exsum_core.h", INCLUDE / "exsum_b200.h"]
+
+
+def _stale(target: Path, deps: list[Path]) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def _run(cmd: list[str], verbose: bool) -> None:
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+
+
+def build(verbose: bool = False, force: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    LIB.parent.mkdir(exist_ok=True)
+    objs: list[Path] = []
+    common_inc = [f"-I{INCLUDE}", f"-I{CSRC}"]
+    for src in CU_SOURCES:
+        obj = BUILD / (src + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [CSRC / src, *HEADERS]):
+            _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xptxas", "-v" if verbose else "-O3",
+                  "-Xcompiler", "-fPIC,-ffp-contract=off,-fopenmp", *common_inc,
+                  "-c", str(CSRC / src), "-o", str(obj)], verbose)
+    for src in CXX_SOURCES:
+        obj = BUILD / (src + ".o")
+        objs.append(obj)
+        if force or _stale(obj, [CSRC / src, *HEADERS]):
+            _run([CXX, "-std=c++17", "-O2", "-fPIC", "-Wall", "-Wextra", *common_inc,
+                  "-c", str(CSRC / src), "-o", str(obj)], verbose)
+    if force or _stale(LIB, objs):
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs),
+              "-Xcompiler", "-fopenmp", "-lgomp"], verbose)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(verbose="-v" in sys.argv, force="-f" in sys.argv)
+    print(LIB)

@@ -1,0 +1,444 @@
+// host_accumulators.cpp — host side of the C ABI: the small and large
+// superaccumulator objects and the partial-record helpers.
+//
+// These are the reference's caller-owned accumulator objects re-expressed in
+// C++ behind the C ABI.  They run on the CPU by design, as
+// their reference counterparts do (small_accumulator.cpp, large_accumulator.cpp);
+// the data-parallel hot path (exact sum of a whole array) is the device path in
+// sum_kernels.cu and never falls back to this file.
+//
+// Arithmetic follows the paper (Neal 2015, Fig. 3 and Fig. 4):
+//   small add      — two signed 64-bit chunk updates per term, carry budget 2047
+//   large add      — raw-bits accumulation per sign+exponent index with a 4096
+//                    countdown, transfer as three 32-bit pieces into the small one
+// Canonicalisation, rounding and the mean share exsum_core.h with the kernels.
+
+#include <cstdint>
+#include <cstring>
+#include <new>
+
+#include "exsum_b200.h"
+#include "exsum_core.h"
+
+using namespace exsum_b200;
+
+namespace {
+
+inline uint64_t bits_of(double v) {
+  uint64_t b;
+  std::memcpy(&b, &v, sizeof b);
+  return b;
+}
+
+inline double double_of(uint64_t b) {
+  double v;
+  std::memcpy(&v, &b, sizeof v);
+  return v;
+}
+
+// ------------------------------------------------------------ small accumulator
+
+// add_inf_nan semantics (small_accumulator.cpp:230-242): the first NaN keeps its
+// payload; a second, different infinity turns the result into the canonical NaN.
+inline void small_special(exsum_small *a, uint64_t bits) {
+  if ((bits & kMantMask) == 0) {
+    if (a->inf_bits == 0) {
+      a->inf_bits = bits;
+    } else if (a->inf_bits != bits && a->nan_bits == 0) {
+      a->nan_bits = kCanonicalQnan;
+    }
+  } else if (a->nan_bits == 0) {
+    a->nan_bits = bits;
+  }
+}
+
+// Fig. 3: split the 53-bit significand, positioned by the low five exponent
+// bits, into a low 32-bit piece for chunk e>>5 and the rest for the next chunk.
+// Returns false for terms that leave the chunks untouched (+-0, Inf, NaN).
+inline bool small_add_term(exsum_small *a, uint64_t bits) {
+  const uint32_t e = static_cast<uint32_t>(bits >> kMantBits) & 0x7FFu;
+  uint64_t m = bits & kMantMask;
+  uint32_t ee = e;
+  if (e == 0x7FFu) {
+    small_special(a, bits);
+    return false;
+  }
+  if (e == 0) {
+    if (m == 0) return false;
+    ee = 1;  // denormal: exponent 1 without the implicit bit
+  } else {
+    m |= uint64_t{1} << kMantBits;
+  }
+  const uint32_t sh = ee & 31u;
+  const uint32_t ix = ee >> 5;
+  const int64_t low = static_cast<int64_t>((m << sh) & 0xFFFFFFFFull);
+  const int64_t high = static_cast<int64_t>(m >> (32u - sh));
+  if (bits >> 63) {
+    a->chunk[ix] -= low;
+    a->chunk[ix + 1] -= high;
+  } else {
+    a->chunk[ix] += low;
+    a->chunk[ix + 1] += high;
+  }
+  return true;
+}
+
+inline int small_propagate(exsum_small *a) {
+  a->adds_until_propagate = kCarryTerms;
+  return exsum_canonicalize(a->chunk);
+}
+
+void small_zero(exsum_small *a) {
+  std::memset(a, 0, sizeof *a);
+  a->adds_until_propagate = kCarryTerms;
+}
+
+// Magnitude, sign and top of an accumulator after propagation.
+struct Mag {
+  uint32_t d[kDigits + 4];
+  int nd;
+  bool neg;
+};
+
+// Correctly rounded (value / n), value = A * 2^-1075.  The quotient is formed
+// with enough extra low bits that the rounding position is at least two bits
+// above the division's truncation point, the remainder feeding the sticky bit.
+uint64_t mean_bits(const int64_t *c, int top, uint64_t n) {
+  uint32_t d[kDigits];
+  const bool neg = exsum_magnitude(c, top, d);
+  int h = kDigits - 1;
+  while (h > 0 && d[h] == 0) --h;
+  const int alen = 32 * h + 32 - exsum_clz32(d[h]);
+  int nlen = 64;
+  while (nlen > 1 && !((n >> (nlen - 1)) & 1u)) --nlen;
+  int t = 55 + nlen - alen + 1;
+  if (t < 2) t = 2;
+  // num = A << t, as digits (t < 32 * 8 always: alen >= 2, nlen <= 64)
+  constexpr int kMax = kDigits + 8;
+  uint32_t num[kMax] = {};
+  const int ws = t >> 5, bs = t & 31;
+  for (int i = 0; i < kDigits; ++i) {
+    const uint64_t v = static_cast<uint64_t>(d[i]) << bs;
+    num[i + ws] |= static_cast<uint32_t>(v);
+    if (i + ws + 1 < kMax) num[i + ws + 1] |= static_cast<uint32_t>(v >> 32);
+  }
+  // Long division by n (remainder < n < 2^64, so rem:digit fits in 96 bits).
+  unsigned __int128 rem = 0;
+  for (int i = kMax - 1; i >= 0; --i) {
+    const unsigned __int128 cur = (rem << 32) | num[i];
+    num[i] = static_cast<uint32_t>(cur / n);
+    rem = cur % n;
+  }
+  return exsum_round_digits(num, kMax, neg, -1075 - t, rem != 0);
+}
+
+// ------------------------------------------------------------ large accumulator
+
+constexpr int kBins = 4096;
+constexpr int kBinAdds = 4096;  // kLargeChunkAdds: 12 spare bits above the mantissa
+
+}  // namespace
+
+struct exsum_large {
+  uint64_t word[kBins];    // wrapped sum of raw bit patterns, valid while in use
+  int16_t left[kBins];     // adds remaining before a transfer; -1 = not in use
+  uint64_t used[kBins / 64];
+  uint64_t used_words;
+  exsum_small small;
+};
+
+namespace {
+
+// Transfer of one bin into the small accumulator (paper §large; reference
+// large_accumulator.cpp:59-111).  The bin holds sum of (4096 - left) raw
+// patterns; adding index*left at bit 52 completes the index bits to a multiple
+// of 2^64, leaving the mantissa-field sum; the implicit ones (one per add) are
+// re-inserted above it; the 96-bit window is applied as three 32-bit pieces.
+void large_transfer(exsum_large *L, uint32_t ix) {
+  exsum_small *s = &L->small;
+  if (s->adds_until_propagate < 3) small_propagate(s);
+  const int64_t left = L->left[ix];
+  uint64_t w = L->word[ix];
+  if (left > 0) w += (static_cast<uint64_t>(left) * ix) << kMantBits;
+  const uint32_t e = ix & 0x7FFu;
+  const uint32_t sh = e ? (e & 31u) : 1u;
+  const uint32_t base = e ? (e >> 5) : 0u;
+  const uint64_t p0 = (w << sh) & 0xFFFFFFFFull;
+  uint64_t mid = w >> (32u - sh);
+  if (e) mid += static_cast<uint64_t>(kBinAdds - left) << (kMantBits - 32 + sh);
+  const uint64_t p2 = mid >> 32;
+  const uint64_t p1 = mid & 0xFFFFFFFFull;
+  const int64_t sgn = (ix >> 11) ? -1 : 1;
+  s->chunk[base] += sgn * static_cast<int64_t>(p0);
+  s->chunk[base + 1] += sgn * static_cast<int64_t>(p1);
+  s->chunk[base + 2] += sgn * static_cast<int64_t>(p2);
+  s->adds_until_propagate -= 3;
+}
+
+// The rare branch of an add (decremented count negative): Inf/NaN, first use
+// of a bin, or a bin that has absorbed its 4096 adds.
+void large_slow(exsum_large *L, uint32_t ix, uint64_t bits) {
+  if ((ix & 0x7FFu) == 0x7FFu) {  // Inf/NaN: bin stays unused
+    small_special(&L->small, bits);
+    return;
+  }
+  if (L->left[ix] >= 0) large_transfer(L, ix);  // full bin (left == 0)
+  L->word[ix] = bits;
+  L->left[ix] = kBinAdds - 1;
+  L->used[ix >> 6] |= uint64_t{1} << (ix & 63u);
+  L->used_words |= uint64_t{1} << (ix >> 6);
+}
+
+inline void large_add_bits(exsum_large *L, uint64_t bits) {
+  const uint32_t ix = static_cast<uint32_t>(bits >> kMantBits);
+  const int left = L->left[ix] - 1;
+  if (left < 0) {
+    large_slow(L, ix, bits);
+  } else {
+    L->left[ix] = static_cast<int16_t>(left);
+    L->word[ix] += bits;
+  }
+}
+
+void large_reset(exsum_large *L) {
+  for (int i = 0; i < kBins; ++i) L->left[i] = -1;
+  std::memset(L->used, 0, sizeof L->used);
+  L->used_words = 0;
+  small_zero(&L->small);
+}
+
+void large_drain(exsum_large *L) {
+  uint64_t words = L->used_words;
+  while (words) {
+    const int w = __builtin_ctzll(words);
+    uint64_t flags = L->used[w];
+    while (flags) {
+      const uint32_t ix = static_cast<uint32_t>(w * 64 + __builtin_ctzll(flags));
+      if (L->left[ix] >= 0 && L->left[ix] < kBinAdds) large_transfer(L, ix);
+      L->left[ix] = -1;
+      flags &= flags - 1;
+    }
+    L->used[w] = 0;
+    words &= words - 1;
+  }
+  L->used_words = 0;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+
+extern "C" {
+
+int exsum_small_init(exsum_small *acc) {
+  if (!acc) return EXSUM_EINVAL;
+  small_zero(acc);
+  return EXSUM_OK;
+}
+
+int exsum_small_add(exsum_small *acc, double v) {
+  if (!acc) return EXSUM_EINVAL;
+  if (acc->adds_until_propagate <= 0) small_propagate(acc);
+  if (small_add_term(acc, bits_of(v))) --acc->adds_until_propagate;
+  return EXSUM_OK;
+}
+
+int exsum_small_add_array(exsum_small *acc, const double *x, size_t n) {
+  if (!acc || (n && !x)) return EXSUM_EINVAL;
+  size_t i = 0;
+  while (i < n) {
+    if (acc->adds_until_propagate <= 0) small_propagate(acc);
+    size_t run = static_cast<size_t>(acc->adds_until_propagate);
+    if (run > n - i) run = n - i;
+    for (size_t j = 0; j < run; ++j) small_add_term(acc, bits_of(x[i + j]));
+    acc->adds_until_propagate -= static_cast<int32_t>(run);  // budget per element
+    i += run;
+  }
+  return EXSUM_OK;
+}
+
+int exsum_small_add_inf_nan(exsum_small *acc, uint64_t bits) {
+  if (!acc || ((bits >> kMantBits) & 0x7FFu) != 0x7FFu) return EXSUM_EINVAL;
+  small_special(acc, bits);
+  return EXSUM_OK;
+}
+
+int exsum_small_carry_propagate(exsum_small *acc) {
+  if (!acc) return -1;
+  return small_propagate(acc);
+}
+
+int exsum_small_merge(exsum_small *dst, const exsum_small *src) {
+  if (!dst || !src) return EXSUM_EINVAL;
+  exsum_small s = *src;
+  small_propagate(&s);
+  if (s.nan_bits && !dst->nan_bits) dst->nan_bits = s.nan_bits;
+  if (s.inf_bits) {
+    if (!dst->inf_bits) {
+      dst->inf_bits = s.inf_bits;
+    } else if (dst->inf_bits != s.inf_bits && !dst->nan_bits) {
+      dst->nan_bits = kCanonicalQnan;
+    }
+  }
+  for (int i = 0; i < kChunks; ++i) dst->chunk[i] += s.chunk[i];
+  small_propagate(dst);
+  return EXSUM_OK;
+}
+
+int exsum_small_round(exsum_small *acc, double *out) {
+  if (!acc || !out) return EXSUM_EINVAL;
+  if (acc->nan_bits) {
+    *out = double_of(acc->nan_bits);
+  } else if (acc->inf_bits) {
+    *out = double_of(acc->inf_bits);
+  } else {
+    const int top = small_propagate(acc);
+    *out = double_of(exsum_round_canonical(acc->chunk, top));
+  }
+  return EXSUM_OK;
+}
+
+int exsum_small_mean(exsum_small *acc, uint64_t n, double *out) {
+  if (!acc || !out || n == 0) return EXSUM_EINVAL;
+  if (acc->nan_bits) {
+    *out = double_of(acc->nan_bits);
+  } else if (acc->inf_bits) {
+    *out = double_of(acc->inf_bits);
+  } else {
+    const int top = small_propagate(acc);
+    *out = top < 0 ? 0.0 : double_of(mean_bits(acc->chunk, top, n));
+  }
+  return EXSUM_OK;
+}
+
+exsum_large *exsum_large_new(void) {
+  exsum_large *L = new (std::nothrow) exsum_large;
+  if (L) large_reset(L);
+  return L;
+}
+
+void exsum_large_free(exsum_large *acc) { delete acc; }
+
+int exsum_large_add(exsum_large *acc, double v) {
+  if (!acc) return EXSUM_EINVAL;
+  large_add_bits(acc, bits_of(v));
+  return EXSUM_OK;
+}
+
+int exsum_large_add_array(exsum_large *acc, const double *x, size_t n) {
+  if (!acc || (n && !x)) return EXSUM_EINVAL;
+  for (size_t i = 0; i < n; ++i) large_add_bits(acc, bits_of(x[i]));
+  return EXSUM_OK;
+}
+
+int exsum_large_drain(exsum_large *acc) {
+  if (!acc) return EXSUM_EINVAL;
+  large_drain(acc);
+  return EXSUM_OK;
+}
+
+int exsum_large_round(exsum_large *acc, double *out) {
+  if (!acc || !out) return EXSUM_EINVAL;
+  large_drain(acc);
+  return exsum_small_round(&acc->small, out);
+}
+
+int exsum_large_mean(exsum_large *acc, uint64_t n, double *out) {
+  if (!acc || !out || n == 0) return EXSUM_EINVAL;
+  large_drain(acc);
+  return exsum_small_mean(&acc->small, n, out);
+}
+
+int exsum_large_small(const exsum_large *acc, exsum_small *out) {
+  if (!acc || !out) return EXSUM_EINVAL;
+  *out = acc->small;
+  return EXSUM_OK;
+}
+
+int exsum_large_chunks_in_use(const exsum_large *acc) {
+  if (!acc) return 0;
+  int used = 0;
+  for (int i = 0; i < kBins; ++i) used += acc->left[i] >= 0;
+  return used;
+}
+
+// ------------------------------------------------------------ partial records
+
+int exsum_partial_from_array(const double *x, size_t n, uint64_t base_index,
+                             exsum_partial *out) {
+  if (!out || (n && !x)) return EXSUM_EINVAL;
+  exsum_large *L = exsum_large_new();
+  if (!L) return EXSUM_ENOMEM;
+  uint64_t P = kNoIndex, M = kNoIndex, N = kNoIndex, payload = 0;
+  for (size_t i = 0; i < n; ++i) {
+    const uint64_t b = bits_of(x[i]);
+    if (((b >> kMantBits) & 0x7FFu) == 0x7FFu) {
+      const uint64_t gi = base_index + i;
+      if (b & kMantMask) {
+        if (N == kNoIndex) {
+          N = gi;
+          payload = b;
+        }
+      } else if (b >> 63) {
+        if (M == kNoIndex) M = gi;
+      } else if (P == kNoIndex) {
+        P = gi;
+      }
+      continue;
+    }
+    large_add_bits(L, b);
+  }
+  large_drain(L);
+  out->acc = L->small;
+  exsum_large_free(L);
+  small_propagate(&out->acc);
+  exsum_resolve_specials(P, M, N, payload, &out->acc.inf_bits, &out->acc.nan_bits);
+  out->acc.reserved_ = 0;
+  out->first_pos_inf = P;
+  out->first_neg_inf = M;
+  out->first_nan = N;
+  out->nan_payload = payload;
+  return EXSUM_OK;
+}
+
+int exsum_partial_merge(const exsum_partial *parts, size_t k, exsum_partial *out,
+                        double *result) {
+  if (!parts && k) return EXSUM_EINVAL;
+  int64_t c[kChunks] = {};
+  uint64_t P = kNoIndex, M = kNoIndex, N = kNoIndex, payload = 0;
+  for (size_t j = 0; j < k; ++j) {
+    exsum_small s = parts[j].acc;
+    exsum_canonicalize(s.chunk);  // each addend within 2^33: no overflow for k < 2^29
+    for (int i = 0; i < kChunks; ++i) c[i] += s.chunk[i];
+    if (parts[j].first_pos_inf < P) P = parts[j].first_pos_inf;
+    if (parts[j].first_neg_inf < M) M = parts[j].first_neg_inf;
+    if (parts[j].first_nan < N) {
+      N = parts[j].first_nan;
+      payload = parts[j].nan_payload;
+    }
+  }
+  const int top = exsum_canonicalize(c);
+  uint64_t ib, nb;
+  exsum_resolve_specials(P, M, N, payload, &ib, &nb);
+  if (result) *result = double_of(exsum_result_bits(ib, nb, c, top));
+  if (out) {
+    std::memcpy(out->acc.chunk, c, sizeof c);
+    out->acc.inf_bits = ib;
+    out->acc.nan_bits = nb;
+    out->acc.adds_until_propagate = kCarryTerms;
+    out->acc.reserved_ = 0;
+    out->first_pos_inf = P;
+    out->first_neg_inf = M;
+    out->first_nan = N;
+    out->nan_payload = payload;
+  }
+  return EXSUM_OK;
+}
+
+int exsum_partial_round(const exsum_partial *p, double *out) {
+  if (!p || !out) return EXSUM_EINVAL;
+  exsum_small s = p->acc;
+  return exsum_small_round(&s, out);
+}
+
+}  // extern "C"

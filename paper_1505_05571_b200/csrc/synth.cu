@@ -1,0 +1,251 @@
+// synth.cu — seeded synthetic inputs for the BASELINE.json configs.
+//
+// The reference's benchmarks run on generated data only (generator.cpp:23-45,
+// PAPER.md:817-826); the configs here are BASELINE.json's.  Each value is a pure
+// function of (config, seed, global index, n_total): shards of a multi-GPU run
+// generate their own slices and the host can regenerate any slice bit-for-bit.
+// Configs 1-4 use only integer arithmetic and correctly rounded IEEE +,*
+// (no FMA contraction), so host and device produce identical bits.  Config 5
+// (normal * 10^k with specials) is generated on the device only.
+//
+//   1: U[-1,1)                    2: U[0,1)
+//   3: random sign/mantissa, exponent uniform 1..2046 (p=0.99) or 0 (denormal
+//      or +-0, p=0.01); no Inf/NaN
+//   4: floor(0.45 n) pairs (x,-x), x = +-10^u, u ~ U[-20,20], then the rest
+//      U[-1e-10,1e-10]; physical order = keyed Feistel bijection of the index
+//   5: N(0,1) * 10^k, k uniform in [-300,300]; P=1e-4 special, split evenly
+//      between +Inf, -Inf and the canonical quiet NaN
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include "exsum_b200.h"
+
+#if defined(__CUDA_ARCH__)
+#define SYN_ADD(a, b) __dadd_rn((a), (b))
+#define SYN_MUL(a, b) __dmul_rn((a), (b))
+#else
+#define SYN_ADD(a, b) ((a) + (b))
+#define SYN_MUL(a, b) ((a) * (b))
+#endif
+
+namespace {
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+// Independent 64-bit draw `stream` for index i.
+__host__ __device__ __forceinline__ uint64_t draw(uint64_t seed, uint64_t stream, uint64_t i) {
+  return mix64(mix64(seed * 0x9E3779B97F4A7C15ull + stream * 0xD1B54A32D192ED03ull) ^
+               (i * 0xA24BAED4963EE407ull + 0x632BE59BD9B4E019ull));
+}
+
+__host__ __device__ __forceinline__ double bits_to_double(uint64_t b) {
+#if defined(__CUDA_ARCH__)
+  return __longlong_as_double(static_cast<long long>(b));
+#else
+  double d;
+  __builtin_memcpy(&d, &b, 8);
+  return d;
+#endif
+}
+
+__host__ __device__ __forceinline__ uint64_t double_to_bits(double d) {
+#if defined(__CUDA_ARCH__)
+  return static_cast<uint64_t>(__double_as_longlong(d));
+#else
+  uint64_t b;
+  __builtin_memcpy(&b, &d, 8);
+  return b;
+#endif
+}
+
+// Uniform on [0,1) with 53 random bits (exact).
+__host__ __device__ __forceinline__ double unit(uint64_t h) {
+  return static_cast<double>(h >> 11) * 0x1.0p-53;
+}
+
+// 2^f for f in [0,1): fixed Horner sequence of exp(f ln 2), round-to-nearest
+// adds and multiplies only, so host and device agree bit for bit.
+__host__ __device__ __forceinline__ double exp2_frac(double f) {
+  const double y = SYN_MUL(f, 0.6931471805599453);
+  double p = 1.0 / 87178291200.0;  // 1/14!
+  const double inv[14] = {1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0,
+                          1.0 / 3628800.0,    1.0 / 362880.0,    1.0 / 40320.0,
+                          1.0 / 5040.0,       1.0 / 720.0,       1.0 / 120.0,
+                          1.0 / 24.0,         1.0 / 6.0,         0.5,
+                          1.0,                1.0};
+  for (int i = 0; i < 14; ++i) p = SYN_ADD(SYN_MUL(p, y), inv[i]);
+  return p;
+}
+
+// Keyed bijection on [0, 2^bits) (bits even): 4-round Feistel.
+__host__ __device__ __forceinline__ uint64_t feistel(uint64_t v, int bits, uint64_t key) {
+  const int hb = bits / 2;
+  const uint64_t mask = (uint64_t{1} << hb) - 1;
+  uint64_t l = v >> hb, r = v & mask;
+  for (int round = 0; round < 4; ++round) {
+    const uint64_t f = mix64(r ^ (key + 0x9E3779B97F4A7C15ull * (round + 1))) & mask;
+    const uint64_t nl = r;
+    r = l ^ f;
+    l = nl;
+  }
+  return (l << hb) | r;
+}
+
+__host__ __device__ __forceinline__ int perm_bits(uint64_t n) {
+  int b = 2;
+  while (b < 64 && (uint64_t{1} << b) < n) b += 2;
+  return b;
+}
+
+__host__ __device__ __forceinline__ double config4_logical(uint64_t seed, uint64_t n, uint64_t j) {
+  const uint64_t pairs = (n / 100) * 45 + ((n % 100) * 45) / 100;  // floor(0.45 n)
+  if (j < 2 * pairs) {
+    const uint64_t p = j >> 1;
+    const uint64_t h = draw(seed, 41, p);
+    // u ~ U[-20,20]; 10^u = 2^(u log2 10) = 2^y
+    const double y = SYN_ADD(SYN_MUL(unit(h), 132.8771237954945), -66.43856189774725);
+    const double fl = floor(y);
+    const double frac = SYN_ADD(y, -fl);
+    const double m = exp2_frac(frac);  // in [1, 2]
+    const int64_t ex = static_cast<int64_t>(fl);
+    uint64_t b = double_to_bits(m);
+    b += static_cast<uint64_t>(ex) << 52;  // exact scaling, stays normal
+    const uint64_t sign = (draw(seed, 42, p) & 1u) ^ (j & 1u);
+    return bits_to_double(b | (sign << 63));
+  }
+  const double u = unit(draw(seed, 43, j));
+  return SYN_MUL(SYN_ADD(SYN_MUL(u, 2.0), -1.0), 1e-10);
+}
+
+__host__ __device__ __forceinline__ double gen_value(int config, uint64_t seed, uint64_t n,
+                                                     uint64_t i) {
+  switch (config) {
+    case 1:
+      return SYN_ADD(SYN_MUL(unit(draw(seed, 11, i)), 2.0), -1.0);
+    case 2:
+      return unit(draw(seed, 21, i));
+    case 3: {
+      const uint64_t h = draw(seed, 31, i);
+      const uint64_t g = draw(seed, 32, i);
+      uint64_t e = 0;
+      if ((g >> 32) >= 42949673ull) e = 1 + (g & 0xFFFFFFFFull) % 2046;  // P(denormal)=0.01
+      return bits_to_double((h & 0x800FFFFFFFFFFFFFull) | (e << 52));
+    }
+    case 4: {
+      const int bits = perm_bits(n);
+      uint64_t j = i;
+      const uint64_t key = mix64(seed ^ 0x5DEECE66Dull);
+      do {
+        j = feistel(j, bits, key);
+      } while (j >= n);  // cycle walking keeps the bijection on [0, n)
+      return config4_logical(seed, n, j);
+    }
+    default:
+      return 0.0;
+  }
+}
+
+__global__ void gen_kernel(int config, uint64_t seed, uint64_t n_total, uint64_t first,
+                           uint64_t count, double *out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < count;
+       t += stride)
+    out[t] = gen_value(config, seed, n_total, first + t);
+}
+
+__constant__ double c_pow10[601];
+bool g_pow10_ready = false;
+
+__global__ void gen5_kernel(uint64_t seed, uint64_t count, double *out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += stride) {
+    const uint64_t h = draw(seed, 51, i);
+    double v;
+    if ((h >> 11) < 900719925474ull) {  // 1e-4 * 2^53
+      const uint64_t kind = draw(seed, 52, i) % 3;
+      v = bits_to_double(kind == 0 ? 0x7FF0000000000000ull
+                                   : kind == 1 ? 0xFFF0000000000000ull : 0x7FF8000000000000ull);
+    } else {
+      const double u1 = (static_cast<double>(draw(seed, 53, i) >> 11) + 1.0) * 0x1.0p-53;
+      const double u2 = unit(draw(seed, 54, i));
+      const double z = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+      const int k = static_cast<int>(draw(seed, 55, i) % 601);
+      v = z * c_pow10[k];
+    }
+    out[i] = v;
+  }
+}
+
+unsigned gen_grid(uint64_t count) {
+  uint64_t g = (count + 255) / 256;
+  if (g > 148ull * 16) g = 148ull * 16;
+  if (g < 1) g = 1;
+  return static_cast<unsigned>(g);
+}
+
+}  // namespace
+
+extern "C" {
+
+int exsum_cuda_gen(int config, uint64_t seed, uint64_t n_total, uint64_t first, size_t count,
+                   double *d_out, void *stream) {
+  if (config < 1 || config > 4 || (count && !d_out) || first + count > n_total)
+    return EXSUM_EINVAL;
+  if (count == 0) return EXSUM_OK;
+  gen_kernel<<<gen_grid(count), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      config, seed, n_total, first, count, d_out);
+  return cudaGetLastError() == cudaSuccess ? EXSUM_OK : EXSUM_ECUDA;
+}
+
+int exsum_host_gen(int config, uint64_t seed, uint64_t n_total, uint64_t first, size_t count,
+                   double *out) {
+  if (config < 1 || config > 4 || (count && !out) || first + count > n_total)
+    return EXSUM_EINVAL;
+#pragma omp parallel for schedule(static)
+  for (long long t = 0; t < static_cast<long long>(count); ++t)
+    out[t] = gen_value(config, seed, n_total, first + static_cast<uint64_t>(t));
+  return EXSUM_OK;
+}
+
+int exsum_host_gen_offsets(uint64_t seed, size_t nseg, uint64_t lo, uint64_t hi,
+                           uint64_t *offsets) {
+  if (!offsets || lo == 0 || hi < lo) return EXSUM_EINVAL;
+  const double a = log(static_cast<double>(lo)), b = log(static_cast<double>(hi));
+  offsets[0] = 0;
+  for (size_t s = 0; s < nseg; ++s) {
+    uint64_t len = static_cast<uint64_t>(floor(exp(a + unit(draw(seed, 56, s)) * (b - a))));
+    if (len < lo) len = lo;
+    if (len > hi) len = hi;
+    offsets[s + 1] = offsets[s] + len;
+  }
+  return EXSUM_OK;
+}
+
+int exsum_cuda_gen_segmented(uint64_t seed, uint64_t n_total, double *d_out, void *stream) {
+  if (n_total && !d_out) return EXSUM_EINVAL;
+  if (!g_pow10_ready) {
+    double p[601];
+    char buf[16];
+    for (int k = -300; k <= 300; ++k) {
+      snprintf(buf, sizeof buf, "1e%d", k);
+      p[k + 300] = strtod(buf, nullptr);  // correctly rounded
+    }
+    if (cudaMemcpyToSymbol(c_pow10, p, sizeof p) != cudaSuccess) return EXSUM_ECUDA;
+    g_pow10_ready = true;
+  }
+  if (n_total == 0) return EXSUM_OK;
+  gen5_kernel<<<gen_grid(n_total), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, n_total,
+                                                                               d_out);
+  return cudaGetLastError() == cudaSuccess ? EXSUM_OK : EXSUM_ECUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,240 @@
+"""Exact summation entry points (the drop-in for ``exsum::exact_sum`` and friends).
+
+Reference surface (vector_ops.hpp:23-75):
+
+* ``exact_sum(values, method)``           vector_ops.cpp:121-130
+* ``exact_mean(values, method)``          vector_ops.cpp:157-170
+* ``parallel_exact_sum(values, plan)``    vector_ops.cpp:172-186  (see distributed.py)
+
+Every entry point runs the sm_100a kernels of ``libexsum_b200.so`` through its C
+ABI.  CUDA tensors are summed in place; host arrays (numpy / CPU tensors /
+sequences) go through ``exsum_context_sum`` (pipelined host->device copies).
+There is no CPU fallback: without a GPU these functions raise.  ``method`` is
+accepted for signature parity only — the reference guarantees both exact
+methods return identical bits (vector_ops.hpp:33-34), and so does the device path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import threading
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import ExsumPartial, lib
+from .accumulators import SmallAccumulator, bits_double
+
+__all__ = ["exact_sum", "exact_mean", "exact_sum_tensor", "exact_sum_segmented",
+           "merge_partials", "partial_from_tensor", "Workspace", "HostContext",
+           "PARTIAL_BYTES", "WORKSPACE_BYTES"]
+
+PARTIAL_BYTES = C.sizeof(ExsumPartial)
+WORKSPACE_BYTES = int(lib.exsum_cuda_workspace_bytes())
+_METHODS = ("small", "large")
+
+
+def _stream_handle(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class Workspace:
+    """Zero-initialised device workspace (exsum_cuda_workspace_init) bound to one device."""
+
+    def __init__(self, device: torch.device | int | str | None = None):
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        if dev.type != "cuda":
+            raise ValueError("Workspace needs a CUDA device")
+        self.device = dev
+        self.buf = torch.empty(WORKSPACE_BYTES, dtype=torch.uint8, device=dev)
+        _lib.call("exsum_cuda_workspace_init", self.buf.data_ptr(), WORKSPACE_BYTES,
+                  _stream_handle(dev))
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+
+_ws_cache: dict[tuple[int, int], Workspace] = {}
+_ws_lock = threading.Lock()
+
+
+def _workspace(device: torch.device) -> Workspace:
+    key = (device.index if device.index is not None else torch.cuda.current_device(),
+           _stream_handle(device))
+    with _ws_lock:
+        ws = _ws_cache.get(key)
+        if ws is None:
+            ws = _ws_cache[key] = Workspace(device)
+        return ws
+
+
+def _check_method(method: str) -> None:
+    if method not in _METHODS:
+        raise ValueError(f"unknown exact method: {method}")
+
+
+def _device_tensor(x: torch.Tensor) -> torch.Tensor:
+    if x.dtype != torch.float64:
+        raise TypeError("exact summation takes float64 values")
+    return x.reshape(-1) if x.is_contiguous() else x.contiguous().reshape(-1)
+
+
+def exact_sum_tensor(x: torch.Tensor, *, base_index: int = 0, result: torch.Tensor | None = None,
+                     partial: torch.Tensor | None = None,
+                     workspace: Workspace | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Asynchronous exact sum of a CUDA float64 tensor on the current stream.
+
+    Returns (result, partial): a 1-element float64 tensor with the correctly
+    rounded sum and a 592-byte uint8 tensor holding the exsum_partial record
+    (canonical chunks + Inf/NaN indices, offset by ``base_index``).
+    """
+    if not x.is_cuda:
+        raise ValueError("exact_sum_tensor needs a CUDA tensor")
+    x = _device_tensor(x)
+    dev = x.device
+    ws = workspace or _workspace(dev)
+    if result is None:
+        result = torch.empty(1, dtype=torch.float64, device=dev)
+    if partial is None:
+        partial = torch.empty(PARTIAL_BYTES, dtype=torch.uint8, device=dev)
+    _lib.call("exsum_cuda_sum", x.data_ptr(), x.numel(), base_index, result.data_ptr(),
+              partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev))
+    return result, partial
+
+
+class HostContext:
+    """exsum_context: device workspace + staging ring for host-resident arrays."""
+
+    def __init__(self, device: int = 0, staging_bytes: int = 256 << 20):
+        self.device = device
+        self._h = lib.exsum_context_create(device, staging_bytes)
+        if not self._h:
+            raise _lib.ExsumError("exsum_context_create", _lib.EXSUM_ECUDA)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.exsum_context_free(h)
+            self._h = None
+
+    def sum(self, values, want_partial: bool = False):
+        a = values.numpy() if isinstance(values, torch.Tensor) else values
+        a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
+        out = C.c_double()
+        part = ExsumPartial()
+        _lib.call("exsum_context_sum", self._h, a.ctypes.data, a.size, C.byref(out),
+                  C.byref(part) if want_partial else None)
+        return (out.value, part) if want_partial else out.value
+
+    def sum_ptr(self, ptr: int, n: int) -> float:
+        out = C.c_double()
+        _lib.call("exsum_context_sum", self._h, ptr, n, C.byref(out), None)
+        return out.value
+
+
+_ctx_cache: dict[int, HostContext] = {}
+
+
+def _host_context(device: int) -> HostContext:
+    with _ws_lock:
+        ctx = _ctx_cache.get(device)
+        if ctx is None:
+            ctx = _ctx_cache[device] = HostContext(device)
+        return ctx
+
+
+def exact_sum(values, method: str = "large", *, device: int | None = None) -> float:
+    """Correctly rounded exact sum (exsum::exact_sum, vector_ops.cpp:121-130)."""
+    _check_method(method)
+    if isinstance(values, torch.Tensor) and values.is_cuda:
+        r, _ = exact_sum_tensor(values)
+        return float(r.item())
+    if not torch.cuda.is_available():
+        raise RuntimeError("exact_sum runs on the GPU; no CUDA device is available")
+    dev = torch.cuda.current_device() if device is None else device
+    return _host_context(dev).sum(values)
+
+
+def partial_from_tensor(partial: torch.Tensor) -> ExsumPartial:
+    raw = bytes(partial.detach().to("cpu").contiguous().view(torch.uint8).numpy().tobytes())
+    if len(raw) != PARTIAL_BYTES:
+        raise ValueError("partial record must be 592 bytes")
+    return ExsumPartial.from_buffer_copy(raw)
+
+
+def exact_mean(values, method: str = "large") -> float:
+    """Correctly rounded exact mean (exsum::exact_mean, vector_ops.cpp:157-170).
+
+    The sum runs on the device; the final division of the 560-byte canonical
+    accumulator by n is exact integer long division on the host
+    (SmallAccumulator::mean, small_accumulator.cpp:350-421).
+    """
+    _check_method(method)
+    n = values.numel() if isinstance(values, torch.Tensor) else len(values)
+    if n == 0:
+        raise ValueError("exact_mean: empty input")
+    if isinstance(values, torch.Tensor) and values.is_cuda:
+        _, p = exact_sum_tensor(values)
+        part = partial_from_tensor(p)
+    else:
+        if not torch.cuda.is_available():
+            raise RuntimeError("exact_mean runs on the GPU; no CUDA device is available")
+        _, part = _host_context(torch.cuda.current_device()).sum(values, want_partial=True)
+    return SmallAccumulator.from_partial(part).mean(n)
+
+
+def exact_sum_segmented(x: torch.Tensor, offsets: torch.Tensor, *,
+                        partials: bool = False,
+                        workspace: Workspace | None = None):
+    """One exact sum per segment: out[i] = exact_sum(x[offsets[i]:offsets[i+1]]).
+
+    x: CUDA float64; offsets: CUDA int64/uint64 with nseg + 1 nondecreasing entries.
+    Returns a float64 tensor of nseg sums (and the uint8 [nseg, 592] partial
+    records if ``partials``; their Inf/NaN indices are local to each segment).
+    """
+    if not (x.is_cuda and offsets.is_cuda):
+        raise ValueError("exact_sum_segmented needs CUDA tensors")
+    x = _device_tensor(x)
+    offsets = offsets.contiguous()
+    if offsets.dtype not in (torch.int64, torch.uint64):
+        raise TypeError("offsets must be 64-bit integers")
+    nseg = offsets.numel() - 1
+    dev = x.device
+    out = torch.empty(max(nseg, 0), dtype=torch.float64, device=dev)
+    parts = torch.empty((max(nseg, 0), PARTIAL_BYTES), dtype=torch.uint8, device=dev) \
+        if partials else None
+    if nseg <= 0:
+        return (out, parts) if partials else out
+    ws = workspace or _workspace(dev)
+    _lib.call("exsum_cuda_sum_segmented", x.data_ptr(), offsets.data_ptr(), nseg,
+              out.data_ptr(), parts.data_ptr() if partials else None, ws.ptr,
+              WORKSPACE_BYTES, _stream_handle(dev))
+    return (out, parts) if partials else out
+
+
+def merge_partials(parts: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """Merge k partial records (uint8 [k, 592] on the device) and round.
+
+    The merge phase of parallel_exact_sum (vector_ops.cpp:64-70) with
+    index-ordered Inf/NaN resolution; result bits do not depend on k.
+    """
+    if not parts.is_cuda:
+        raise ValueError("merge_partials needs a CUDA tensor")
+    parts = parts.contiguous().view(torch.uint8).reshape(-1, PARTIAL_BYTES)
+    dev = parts.device
+    result = torch.empty(1, dtype=torch.float64, device=dev)
+    out = torch.empty(PARTIAL_BYTES, dtype=torch.uint8, device=dev)
+    _lib.call("exsum_cuda_merge", parts.data_ptr(), parts.shape[0], result.data_ptr(),
+              out.data_ptr(), _stream_handle(dev))
+    return result, out
+
+
+def result_bits(r: torch.Tensor | float) -> int:
+    v = float(r.item()) if isinstance(r, torch.Tensor) else float(r)
+    return int(np.array([v], dtype=np.float64).view(np.uint64)[0])
+
+
+def bits_to_float(b: int) -> float:
+    return bits_double(b)
