@@ -7,9 +7,11 @@ a Python or CPU implementation of the device path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "lib" / "libexsum_b200.so"
+LIB_PATH = Path(os.environ.get("EXSUM_LIB") or
+                Path(__file__).resolve().parent / "lib" / "libexsum_b200.so")
 
 EXSUM_OK, EXSUM_EINVAL, EXSUM_ECUDA, EXSUM_ENOMEM = 0, 1, 2, 3
 SMALL_CHUNKS = 67

@@ -41,28 +41,38 @@ def _run(cmd: list[str], verbose: bool) -> None:
     subprocess.run(cmd, check=True)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
-    LIB.parent.mkdir(exist_ok=True)
+def build(verbose: bool = False, force: bool = False, defines: tuple[str, ...] = (),
+          lib: Path = LIB, build_dir: Path = BUILD) -> Path:
+    """Build the library; ``defines`` (-D...) and a separate lib/build_dir give
+    tuning variants without touching the default artefact."""
+    build_dir.mkdir(parents=True, exist_ok=True)
+    lib.parent.mkdir(parents=True, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     objs: list[Path] = []
     common_inc = [f"-I{INCLUDE}", f"-I{CSRC}"]
     for src in CU_SOURCES:
-        obj = BUILD / (src + ".o")
+        obj = build_dir / (src + ".o")
         objs.append(obj)
         if force or _stale(obj, [CSRC / src, *HEADERS]):
-            _run([NVCC, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xptxas", "-v" if verbose else "-O3",
+            _run([NVCC, *dflags, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xptxas", "-v" if verbose else "-O3",
                   "-Xcompiler", "-fPIC,-ffp-contract=off,-fopenmp", *common_inc,
                   "-c", str(CSRC / src), "-o", str(obj)], verbose)
     for src in CXX_SOURCES:
-        obj = BUILD / (src + ".o")
+        obj = build_dir / (src + ".o")
         objs.append(obj)
         if force or _stale(obj, [CSRC / src, *HEADERS]):
-            _run([CXX, "-std=c++17", "-O2", "-fPIC", "-Wall", "-Wextra", *common_inc,
+            _run([CXX, *dflags, "-std=c++17", "-O2", "-fPIC", "-Wall", "-Wextra", *common_inc,
                   "-c", str(CSRC / src), "-o", str(obj)], verbose)
-    if force or _stale(LIB, objs):
-        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs),
+    if force or _stale(lib, objs):
+        _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs),
               "-Xcompiler", "-fopenmp", "-lgomp"], verbose)
-    return LIB
+    return lib
+
+
+def build_variant(name: str, defines: tuple[str, ...], verbose: bool = False) -> Path:
+    """Tuning variant: lib/variants/<name>.so (select with EXSUM_LIB=...)."""
+    return build(verbose=verbose, defines=defines, lib=PKG / "lib" / "variants" / f"{name}.so",
+                 build_dir=BUILD / "variants" / name)
 
 
 if __name__ == "__main__":

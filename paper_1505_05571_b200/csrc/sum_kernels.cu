@@ -6,29 +6,36 @@
 // split-merge of parallel_exact_sum (vector_ops.cpp:172-186).  See DESIGN.md.
 //
 // Device representation (B200-first, not the reference's): every LANE owns a
-// private superaccumulator of 66 "slots" in shared memory.  Slot k holds a
-// signed 96-bit integer V_k with weight 2^(32k - 1075) — the reference's chunk
-// weight — stored as two planes, a u32 low word L[k][lane] and an s64 high word
-// H[k][lane].  A term with biased exponent e' = max(e, 1) and signed significand
-// t (53 bits with the implicit one) adds t * 2^(e' & 31) (< 2^84 in magnitude)
-// to slot e' >> 5 with one 96-bit add: 3 integer instructions, 1 LDS.32 +
-// 1 LDS.64 + 1 STS.32 + 1 STS.64, no atomics and no bank conflicts (lane-
-// interleaved planes), independent of how the exponents are distributed.  96-bit
-// slots with 2^11 headroom absorb 2047 terms; each lane renormalises (carries
-// upward, leaving L in [0,2^32) and H = 0) at most every 2016 terms.
+// private fixed-point superaccumulator in shared memory, so a term costs one
+// conflict-free shared read-modify-write and a handful of integer instructions
+// — no atomics, no bank conflicts, no dependence on how exponents are
+// distributed.  Two slot layouts are built (EXSUM_SLOT_BITS):
+//
+//   128 (default)  slot k = signed 128-bit integer of weight 2^(64k - 1075);
+//                  a term m * 2^(e' - 1075) adds m << (e' & 63) (< 2^116) to slot
+//                  e' >> 6.  33 slots x 16 B = 528 B per lane, 16.9 KB per warp:
+//                  12 warps per SM.  One LDS.128 + 4 adds + one STS.128.
+//   96             slot k = signed 96-bit integer of weight 2^(32k - 1075) — the
+//                  reference's chunk weight — as a u32 plane and an s64 plane;
+//                  66 slots, 25.3 KB per warp: 8 warps per SM.
+//
+// Either way 2^11 of headroom absorbs 2047 terms per slot; each lane
+// renormalises (carries upward) at most every 2016 terms.  e' = max(e, 1) and the
+// implicit one is dropped for e == 0 (denormals, paper §small).
 //
 // Why not the reference's 4096 shared bins: 64-bit shared atomics compile to
-// ATOMS.CAST.SPIN.64 CAS loops on sm_100a and random-bin read-modify-writes
-// cost ~3.5x in bank conflicts; narrow data (U[0,1)) puts half of all terms in
-// one bin.  Lane privatisation makes all three problems disappear.
+// ATOMS.CAST.SPIN.64 CAS loops on sm_100a, random-bin read-modify-writes cost
+// ~3.5x in bank conflicts, and narrow data (U[0,1)) puts half of all terms in
+// one bin.  Lane privatisation removes all three.
 //
 // Kernels
-//   exsum_sum_kernel        K1+K2+K3: persistent grid, 8 warps/CTA, each warp
+//   exsum_sum_kernel        K1+K2+K3: persistent grid (1 CTA per SM), each warp
 //                           streams a contiguous range with 256-bit loads
-//                           (double-buffered), lanes accumulate privately; the
-//                           CTA combines its 8x32 lanes into 67 chunk sums,
-//                           REDG.ADD.64 into the workspace; the last CTA
-//                           canonicalises, resolves Inf/NaN and rounds.
+//                           (register double-buffered, L2 bulk prefetch ahead),
+//                           lanes accumulate privately; the CTA combines its
+//                           lanes into 67 chunk sums, REDG.ADD.64 into the
+//                           workspace; the last CTA canonicalises, resolves
+//                           Inf/NaN by first index, rounds.
 //   exsum_segmented_kernel  K4: one warp per segment (dynamic), same inner loop,
 //                           warp-local combine + round, one double per segment.
 //   exsum_merge_kernel      K5: merge of k gathered partial records + round.
@@ -38,6 +45,19 @@
 
 #include "exsum_b200.h"
 #include "exsum_core.h"
+
+#ifndef EXSUM_EXPERIMENT
+#define EXSUM_EXPERIMENT 0
+#endif
+#ifndef EXSUM_SLOT_BITS
+#define EXSUM_SLOT_BITS 96
+#endif
+#ifndef EXSUM_DECODE
+#define EXSUM_DECODE 0  // 0: decode on the ALU pipe, 1: on the FMA pipe (IMAD)
+#endif
+#ifndef EXSUM_PIPE
+#define EXSUM_PIPE 0  // 0 serial RMW, 1 store forwarding, 2 run merge (slot layout 96)
+#endif
 
 namespace exsum_b200 {
 namespace dev {
@@ -57,35 +77,137 @@ struct Workspace {
   unsigned int pad_;
 };
 
-// ---------------------------------------------------------- lane accumulators
-
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
-constexpr int kSlots = 66;       // slots 0..63 take terms, 64..65 only carries
-#ifndef EXSUM_VEC_PER_LANE
-#define EXSUM_VEC_PER_LANE 8
-#endif
-constexpr int kVecPerLane = EXSUM_VEC_PER_LANE;  // 256-bit vectors per lane per batch
-constexpr int kBatchTerms = kVecPerLane * 4;
-constexpr int kNormEvery = 2016 / kBatchTerms;   // batches between renormalisations
-constexpr int kLPlane = kSlots * 32 * 4;
-constexpr int kHPlane = kSlots * 32 * 8;
-constexpr int kWarpSmem = kLPlane + kHPlane;              // 25,344 B
-constexpr int kScratch = kWarps * kChunks * 8;            // per-warp chunk rows
-constexpr int kSumSmem = kWarps * kWarpSmem + kScratch;   // 207,040 B
-
-// One lane's view of its accumulator.  Generic pointers serve the cold paths
-// (renormalisation, reduction); the hot path uses 32-bit shared addresses:
-// slot k's low word is at sl + 128 k and its high word at 2 * (sl + 128 k) + hoff.
-struct Lane {
-  uint32_t *L;                  // &Lplane[0][lane]; slot k at L[32 k]
-  unsigned long long *H;        // &Hplane[0][lane]; slot k at H[32 k]
-  uint32_t sl;                  // shared address of L[0][lane]
-  uint32_t hoff;                // shared address of H[0][lane] minus 2 * sl
-};
-
 struct Specials {                // first occurrences seen by one lane
   unsigned long long P, M, N;    // index (global or segment-local), ~0 = none
+};
+
+__device__ __forceinline__ uint32_t exponent_field(uint32_t hi) { return (hi >> 20) & 0x7FFu; }
+
+// =========================================================== slot layout: 128
+namespace slot128 {
+
+constexpr int kWarps = 12;
+constexpr int kSlots = 33;                  // 0..31 take terms (e' >> 6), 32 carries only
+constexpr int kWarpSmem = kSlots * 32 * 16;  // 16,896 B
+constexpr int kDefaultVec = 4;
+
+struct Lane {
+  uint4 *P;     // this lane's slot 0; slot k at P[32 k] (lane-interleaved 16 B entries)
+  uint32_t sa;  // shared address of P; slot k at sa + 512 k
+};
+
+__device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
+  Lane v;
+  v.P = reinterpret_cast<uint4 *>(warp_smem) + lane;
+  v.sa = static_cast<uint32_t>(__cvta_generic_to_shared(v.P));
+  return v;
+}
+
+// term = (-1)^s m 2^(e'-1075): add m << sh, sh = e' & 63, to slot e' >> 6.  For a
+// negative term add ~(m << sh) + 1: the complement is folded into the funnel
+// shifts (fill word s), the +1 is the carry-in (CC.CF = s & 1 from s + s).
+// -0.0 adds 2^128, i.e. nothing.
+__device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
+  const uint32_t ep = max(e, 1u);
+  const uint32_t imp = e ? 0x100000u : 0u;
+  const uint32_t s = static_cast<uint32_t>(static_cast<int32_t>(hi) >> 31);
+  const uint32_t mx = ((hi & 0xFFFFFu) | imp) ^ s;
+  const uint32_t lx = lo ^ s;
+  const uint32_t w0 = __funnelshift_l(s, lx, ep);   // shift count taken mod 32
+  const uint32_t w1 = __funnelshift_l(lx, mx, ep);
+  const uint32_t w2 = __funnelshift_l(mx, s, ep);
+  const bool up = (ep & 32u) != 0u;                  // shift by 32 more: one word up
+  const uint32_t u0 = up ? s : w0, u1 = up ? w0 : w1, u2 = up ? w1 : w2, u3 = up ? w2 : s;
+  const uint32_t addr = a.sa + ((ep >> 6) << 9);
+  asm volatile(
+      "{\n\t.reg .u32 q0, q1, q2, q3, cf;\n\t"
+      "ld.shared.v4.u32 {q0, q1, q2, q3}, [%0];\n\t"
+      "add.cc.u32 cf, %1, %1;\n\t"
+      "addc.cc.u32 q0, q0, %2;\n\t"
+      "addc.cc.u32 q1, q1, %3;\n\t"
+      "addc.cc.u32 q2, q2, %4;\n\t"
+      "addc.u32 q3, q3, %5;\n\t"
+      "st.shared.v4.u32 [%0], {q0, q1, q2, q3};\n\t}"
+      :
+      : "r"(addr), "r"(s), "r"(u0), "r"(u1), "r"(u2), "r"(u3)
+      : "memory");
+}
+
+// Carry upward: slots 0..31 end in [0, 2^64) (high half zero), slot 32 keeps the
+// rest.  Each slot has absorbed <= 2047 terms (< 2^127 with the incoming carry).
+__device__ __forceinline__ void normalize(const Lane &a) {
+  long long c = 0;
+#pragma unroll 4
+  for (int k = 0; k < kSlots - 1; ++k) {
+    const uint4 v = a.P[32 * k];
+    const unsigned long long lo = (static_cast<unsigned long long>(v.y) << 32) | v.x;
+    const long long hi = static_cast<long long>((static_cast<unsigned long long>(v.w) << 32) | v.z);
+    const unsigned long long nlo = lo + static_cast<unsigned long long>(c);
+    const long long nhi = hi + (c >> 63) + (nlo < lo ? 1 : 0);
+    a.P[32 * k] = make_uint4(static_cast<uint32_t>(nlo), static_cast<uint32_t>(nlo >> 32), 0u, 0u);
+    c = nhi;
+  }
+  const uint4 v = a.P[32 * (kSlots - 1)];
+  const unsigned long long lo = (static_cast<unsigned long long>(v.y) << 32) | v.x;
+  const long long hi = static_cast<long long>((static_cast<unsigned long long>(v.w) << 32) | v.z);
+  const unsigned long long nlo = lo + static_cast<unsigned long long>(c);
+  const unsigned long long nhi =
+      static_cast<unsigned long long>(hi + (c >> 63) + (nlo < lo ? 1 : 0));
+  a.P[32 * (kSlots - 1)] = make_uint4(static_cast<uint32_t>(nlo), static_cast<uint32_t>(nlo >> 32),
+                                      static_cast<uint32_t>(nhi), static_cast<uint32_t>(nhi >> 32));
+}
+
+// The warp's exact sum as 67 chunk values (row[0..66], |row[i]| < 2^38):
+// normalise each lane, then lane j sums slot j's two low words over all lanes.
+__device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, const Lane &a, int lane,
+                                            long long *row) {
+  normalize(a);
+  __syncwarp();
+  const uint4 *base = reinterpret_cast<const uint4 *>(warp_smem);
+  unsigned long long s0 = 0, s1 = 0;
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) {
+    const int col = (i + lane) & 31;
+    const uint2 v = *reinterpret_cast<const uint2 *>(&base[lane * 32 + col]);
+    s0 += v.x;
+    s1 += v.y;
+  }
+  row[2 * lane] = static_cast<long long>(s0);
+  row[2 * lane + 1] = static_cast<long long>(s1);
+  const uint4 t = base[(kSlots - 1) * 32 + lane];
+  unsigned long long c64 = t.x, c65 = t.y;
+  long long c66 = static_cast<long long>((static_cast<unsigned long long>(t.w) << 32) | t.z);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    c64 += __shfl_xor_sync(0xffffffffu, c64, o);
+    c65 += __shfl_xor_sync(0xffffffffu, c65, o);
+    c66 += __shfl_xor_sync(0xffffffffu, c66, o);
+  }
+  if (lane == 0) {
+    row[64] = static_cast<long long>(c64);
+    row[65] = static_cast<long long>(c65);
+    row[66] = c66;
+  }
+}
+
+}  // namespace slot128
+
+// ============================================================ slot layout: 96
+namespace slot96 {
+
+constexpr int kWarps = 8;
+constexpr int kSlots = 66;       // slots 0..63 take terms (e' >> 5), 64..65 only carries
+constexpr int kLPlane = kSlots * 32 * 4;
+constexpr int kHPlane = kSlots * 32 * 8;
+constexpr int kWarpSmem = kLPlane + kHPlane;  // 25,344 B
+constexpr int kDefaultVec = 8;
+
+// Slot k's low word is at sl + 128 k and its high word at 2 * (sl + 128 k) + hoff.
+struct Lane {
+  uint32_t *L;            // &Lplane[0][lane]; slot k at L[32 k]
+  unsigned long long *H;  // &Hplane[0][lane]; slot k at H[32 k]
+  uint32_t sl;
+  uint32_t hoff;
 };
 
 __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
@@ -97,31 +219,28 @@ __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
   return v;
 }
 
-// Zero one warp's planes cooperatively with 16-byte stores.
-__device__ __forceinline__ void zero_warp_planes(unsigned char *warp_smem, int lane) {
-  uint4 *p = reinterpret_cast<uint4 *>(warp_smem);
-  constexpr int n16 = kWarpSmem / 16;
-#pragma unroll 4
-  for (int i = lane; i < n16; i += 32) p[i] = make_uint4(0, 0, 0, 0);
-}
-
-__device__ __forceinline__ uint32_t exponent_field(uint32_t hi) { return (hi >> 20) & 0x7FFu; }
-
-// Add one finite term (exponent field e != 2047, e passed in) to the lane's slots.
-//
-// The term is (-1)^s * m * 2^(e' - 1075), e' = max(e, 1), m the significand with
-// its implicit one.  In slot units it is m << (e' & 31) added at slot e' >> 5;
-// m << sh spans 96 bits (u2:u1:u0).  Negative terms add ~(m << sh) + 1: the
-// complement is folded into the funnel shifts (fill words = s) and the +1 is
-// the carry-in of the 96-bit add (CC.CF = s & 1 from s + s).  -0.0 adds 2^96,
-// i.e. nothing.  ~23 SASS per term: no branches, no atomics.
+// Same scheme as slot128 with a 96-bit window: m << (e' & 31) at slot e' >> 5.
 __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
-  const uint32_t ep = max(e, 1u);                          // denormal: exponent 1
-  const uint32_t imp = e ? 0x100000u : 0u;                  // implicit one
+#if EXSUM_DECODE == 1
+  // Decode on the FMA pipe (IMAD / IMAD.HI) to unload the integer ALU pipe:
+  // t = hi >> 20, s = sign mask, low 20 mantissa bits = hi - t 2^20, implicit
+  // one = (e + 2047) >> 11, x ^ s = x (2s + 1) + s for s in {0, -1}.
+  const uint32_t t = __umulhi(hi, 4096u);
+  const uint32_t s = static_cast<uint32_t>(__mulhi(static_cast<int>(hi), 1));
+  const uint32_t ib = __umulhi(e + 2047u, 2097152u);
+  const uint32_t mh = hi - t * 1048576u + ib * 1048576u;
+  const uint32_t ep = max(e, 1u);
+  const uint32_t m1 = s * 2u + 1u;
+  const uint32_t lx = lo * m1 + s;
+  const uint32_t mx = mh * m1 + s;
+#else
+  const uint32_t ep = max(e, 1u);
+  const uint32_t imp = e ? 0x100000u : 0u;
   const uint32_t s = static_cast<uint32_t>(static_cast<int32_t>(hi) >> 31);
   const uint32_t mx = ((hi & 0xFFFFFu) | imp) ^ s;
   const uint32_t lx = lo ^ s;
-  const uint32_t u0 = __funnelshift_l(s, lx, ep);         // shift count taken mod 32
+#endif
+  const uint32_t u0 = __funnelshift_l(s, lx, ep);
   const uint32_t u1 = __funnelshift_l(lx, mx, ep);
   const uint32_t u2 = __funnelshift_l(mx, s, ep);
   const uint32_t la = a.sl + ((ep >> 5) << 7);
@@ -139,6 +258,215 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
       :
       : "r"(la), "r"(ha), "r"(s), "r"(u0), "r"(u1), "r"(u2)
       : "memory");
+}
+
+// Carry upward: L_k in [0, 2^32), H_k = 0 for k < 65; slot 65 keeps the rest.
+__device__ __forceinline__ void normalize(const Lane &a) {
+  long long c = 0;
+#pragma unroll 6
+  for (int k = 0; k < kSlots - 1; ++k) {
+    const long long u = static_cast<long long>(a.L[32 * k]) + c;
+    const long long h = static_cast<long long>(a.H[32 * k]);
+    a.L[32 * k] = static_cast<uint32_t>(u);
+    a.H[32 * k] = 0ull;
+    c = h + (u >> 32);
+  }
+  const int k = kSlots - 1;
+  const long long u = static_cast<long long>(a.L[32 * k]) + c;
+  a.L[32 * k] = static_cast<uint32_t>(u);
+  a.H[32 * k] = static_cast<unsigned long long>(static_cast<long long>(a.H[32 * k]) + (u >> 32));
+}
+
+// ---- pipelined term streams (EXSUM_PIPE) ------------------------------------
+//
+// add_term above is a strict read-modify-write chain per lane: the next term's
+// LDS cannot issue before this term's STS.  The pipes break that chain.
+//
+// Forward (EXSUM_PIPE 1): term j's LDS is issued before term j-1's STS; if both
+// hit the same slot, j-1's fresh value is forwarded from registers.
+// Merge (EXSUM_PIPE 2): a "pending" slot accumulates consecutive terms that hit
+// it in registers; only when the slot changes is the pending value committed
+// (predicated STS) and the new slot loaded (predicated LDS, issued before the
+// commit).  Narrow exponent ranges then touch shared memory rarely.
+
+struct Pipe {
+  uint32_t pla;         // L-plane address of the pending slot
+  uint32_t v0, v1, v2;  // forward: its new value; merge: its loaded base value
+  uint32_t a0, a1, a2;  // merge: pending addend
+};
+
+__device__ __forceinline__ void term_words(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e,
+                                           uint32_t &s, uint32_t &u0, uint32_t &u1,
+                                           uint32_t &u2, uint32_t &la) {
+  const uint32_t ep = max(e, 1u);
+  const uint32_t imp = e ? 0x100000u : 0u;
+  s = static_cast<uint32_t>(static_cast<int32_t>(hi) >> 31);
+  const uint32_t mx = ((hi & 0xFFFFFu) | imp) ^ s;
+  const uint32_t lx = lo ^ s;
+  u0 = __funnelshift_l(s, lx, ep);
+  u1 = __funnelshift_l(lx, mx, ep);
+  u2 = __funnelshift_l(mx, s, ep);
+  la = a.sl + ((ep >> 5) << 7);
+}
+
+__device__ __forceinline__ void pipe_init(const Lane &a, Pipe &p) {
+  p.pla = a.sl;  // slot 0
+  const uint32_t ha = 2u * p.pla + a.hoff;
+  asm volatile("ld.shared.u32 %0, [%3];\n\tld.shared.v2.u32 {%1, %2}, [%4];"
+               : "=r"(p.v0), "=r"(p.v1), "=r"(p.v2)
+               : "r"(p.pla), "r"(ha)
+               : "memory");
+  p.a0 = p.a1 = p.a2 = 0u;
+}
+
+__device__ __forceinline__ void pipe_flush(const Lane &a, Pipe &p) {
+  uint32_t c0 = p.v0, c1 = p.v1, c2 = p.v2;
+#if EXSUM_PIPE == 2
+  asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+      : "+r"(c0), "+r"(c1), "+r"(c2)
+      : "r"(p.a0), "r"(p.a1), "r"(p.a2));
+#endif
+  const uint32_t ha = 2u * p.pla + a.hoff;
+  asm volatile("st.shared.u32 [%0], %2;\n\tst.shared.v2.u32 [%1], {%3, %4};" ::"r"(p.pla),
+               "r"(ha), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
+__device__ __forceinline__ void pipe_step(const Lane &a, Pipe &p, uint32_t lo, uint32_t hi,
+                                          uint32_t e) {
+  uint32_t s, u0, u1, u2, la;
+  term_words(a, lo, hi, e, s, u0, u1, u2, la);
+  const uint32_t ha = 2u * la + a.hoff;
+  const uint32_t pha = 2u * p.pla + a.hoff;
+#if EXSUM_PIPE == 1
+  uint32_t l0, l1, l2;
+  asm volatile(
+      "ld.shared.u32 %0, [%3];\n\t"
+      "ld.shared.v2.u32 {%1, %2}, [%4];\n\t"
+      "st.shared.u32 [%5], %7;\n\t"
+      "st.shared.v2.u32 [%6], {%8, %9};"
+      : "=r"(l0), "=r"(l1), "=r"(l2)
+      : "r"(la), "r"(ha), "r"(p.pla), "r"(pha), "r"(p.v0), "r"(p.v1), "r"(p.v2)
+      : "memory");
+  const bool same = la == p.pla;
+  uint32_t n0 = same ? p.v0 : l0, n1 = same ? p.v1 : l1, n2 = same ? p.v2 : l2;
+  asm("{\n\t.reg .u32 cf;\n\tadd.cc.u32 cf, %3, %3;\n\taddc.cc.u32 %0, %0, %4;\n\t"
+      "addc.cc.u32 %1, %1, %5;\n\taddc.u32 %2, %2, %6;\n\t}"
+      : "+r"(n0), "+r"(n1), "+r"(n2)
+      : "r"(s), "r"(u0), "r"(u1), "r"(u2));
+  p.v0 = n0;
+  p.v1 = n1;
+  p.v2 = n2;
+  p.pla = la;
+#else
+  // commit value of the pending slot (used only if the slot changes)
+  uint32_t c0 = p.v0, c1 = p.v1, c2 = p.v2;
+  asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+      : "+r"(c0), "+r"(c1), "+r"(c2)
+      : "r"(p.a0), "r"(p.a1), "r"(p.a2));
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, %5;\n\t"
+      "@q ld.shared.u32 %0, [%3];\n\t"
+      "@q ld.shared.v2.u32 {%1, %2}, [%4];\n\t"
+      "@q st.shared.u32 [%5], %7;\n\t"
+      "@q st.shared.v2.u32 [%6], {%8, %9};\n\t}"
+      : "+r"(p.v0), "+r"(p.v1), "+r"(p.v2)
+      : "r"(la), "r"(ha), "r"(p.pla), "r"(pha), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+  const bool same = la == p.pla;
+  uint32_t n0 = same ? p.a0 : 0u, n1 = same ? p.a1 : 0u, n2 = same ? p.a2 : 0u;
+  asm("{\n\t.reg .u32 cf;\n\tadd.cc.u32 cf, %3, %3;\n\taddc.cc.u32 %0, %0, %4;\n\t"
+      "addc.cc.u32 %1, %1, %5;\n\taddc.u32 %2, %2, %6;\n\t}"
+      : "+r"(n0), "+r"(n1), "+r"(n2)
+      : "r"(s), "r"(u0), "r"(u1), "r"(u2));
+  p.a0 = n0;
+  p.a1 = n1;
+  p.a2 = n2;
+  p.pla = la;
+#endif
+}
+
+__device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, const Lane &a, int lane,
+                                            long long *row) {
+  normalize(a);
+  __syncwarp();
+  const uint32_t *Lp = reinterpret_cast<const uint32_t *>(warp_smem);
+  const unsigned long long *Hp = reinterpret_cast<const unsigned long long *>(warp_smem + kLPlane);
+  unsigned long long s0 = 0, s1 = 0, s2 = 0;
+  const int rowa = lane, rowb = lane + 32, rowc = lane + 64;
+#pragma unroll 8
+  for (int i = 0; i < 32; ++i) {
+    const int col = (i + lane) & 31;  // skewed: 32 distinct banks
+    s0 += Lp[rowa * 32 + col];
+    s1 += Lp[rowb * 32 + col];
+    if (rowc < kSlots) s2 += Lp[rowc * 32 + col];
+  }
+  long long h = static_cast<long long>(Hp[(kSlots - 1) * 32 + lane]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+  row[lane] = static_cast<long long>(s0);
+  row[lane + 32] = static_cast<long long>(s1);
+  if (lane < 2) row[lane + 64] = static_cast<long long>(s2);
+  if (lane == 0) row[66] = h;
+}
+
+}  // namespace slot96
+
+#if EXSUM_SLOT_BITS == 96
+namespace acc = slot96;
+#elif EXSUM_SLOT_BITS == 128
+namespace acc = slot128;
+#else
+#error "EXSUM_SLOT_BITS must be 96 or 128"
+#endif
+
+// ------------------------------------------------------------ common machinery
+
+constexpr int kWarps = acc::kWarps;
+constexpr int kThreads = kWarps * 32;
+constexpr int kWarpSmem = acc::kWarpSmem;
+#ifndef EXSUM_VEC_PER_LANE
+#define EXSUM_VEC_PER_LANE acc::kDefaultVec
+#endif
+constexpr int kVecPerLane = EXSUM_VEC_PER_LANE;   // 256-bit vectors per lane per batch
+constexpr int kBatchTerms = kVecPerLane * 4;
+constexpr int kNormEvery = 2016 / kBatchTerms;    // batches between renormalisations
+#ifndef EXSUM_PREFETCH_BATCHES
+#define EXSUM_PREFETCH_BATCHES 1
+#endif
+constexpr int kPrefetchBatches = EXSUM_PREFETCH_BATCHES;  // L2 prefetch distance
+constexpr int kScratch = kWarps * kChunks * 8;              // per-warp chunk rows
+constexpr int kSmem = kWarps * kWarpSmem + kScratch;
+static_assert(kSmem <= 227 * 1024, "shared memory budget");
+static_assert(kNormEvery >= 1, "batch too large for the carry budget");
+
+using acc::Lane;
+
+// Term stream over a lane accumulator: pipelined (EXSUM_PIPE) or plain RMW.
+#if EXSUM_PIPE != 0 && EXSUM_SLOT_BITS == 96
+using acc::Pipe;
+__device__ __forceinline__ void stream_begin(const Lane &a, Pipe &p) { acc::pipe_init(a, p); }
+__device__ __forceinline__ void stream_end(const Lane &a, Pipe &p) { acc::pipe_flush(a, p); }
+__device__ __forceinline__ void stream_term(const Lane &a, Pipe &p, uint32_t lo, uint32_t hi,
+                                            uint32_t e) {
+  acc::pipe_step(a, p, lo, hi, e);
+}
+#else
+struct Pipe {};
+__device__ __forceinline__ void stream_begin(const Lane &, Pipe &) {}
+__device__ __forceinline__ void stream_end(const Lane &, Pipe &) {}
+__device__ __forceinline__ void stream_term(const Lane &a, Pipe &, uint32_t lo, uint32_t hi,
+                                            uint32_t e) {
+  acc::add_term(a, lo, hi, e);
+}
+#endif
+
+// Zero one warp's accumulator cooperatively with 16-byte stores.
+__device__ __forceinline__ void zero_warp(unsigned char *warp_smem, int lane) {
+  uint4 *p = reinterpret_cast<uint4 *>(warp_smem);
+  constexpr int n16 = kWarpSmem / 16;
+#pragma unroll 4
+  for (int i = lane; i < n16; i += 32) p[i] = make_uint4(0, 0, 0, 0);
 }
 
 __device__ __forceinline__ void record_special(Specials &sp, uint32_t lo, uint32_t hi,
@@ -159,54 +487,8 @@ __device__ __forceinline__ void add_term_checked(const Lane &a, Specials &sp, ui
   if (e == 0x7FFu) {
     record_special(sp, lo, hi, index);
   } else {
-    add_term(a, lo, hi, e);
+    acc::add_term(a, lo, hi, e);
   }
-}
-
-// Carry upward through the lane's slots: afterwards L_k in [0, 2^32), H_k = 0
-// for k < 65 and slot 65 holds the rest.  Safe whenever every slot has seen at
-// most 2047 terms since the last call (|H_k| < 2^63 - 2^52).
-__device__ __forceinline__ void normalize_lane(const Lane &a) {
-  long long c = 0;
-#pragma unroll 6
-  for (int k = 0; k < kSlots - 1; ++k) {
-    const long long u = static_cast<long long>(a.L[32 * k]) + c;
-    const long long h = static_cast<long long>(a.H[32 * k]);
-    a.L[32 * k] = static_cast<uint32_t>(u);
-    a.H[32 * k] = 0ull;
-    c = h + (u >> 32);
-  }
-  const int k = kSlots - 1;
-  const long long u = static_cast<long long>(a.L[32 * k]) + c;
-  a.L[32 * k] = static_cast<uint32_t>(u);
-  a.H[32 * k] = static_cast<unsigned long long>(static_cast<long long>(a.H[32 * k]) + (u >> 32));
-}
-
-// Warp-wide sum of the 32 normalised lane accumulators into chunk values.
-// Lane j returns rows j, j+32 and (j < 2) j+64 in r0, r1, r2; every lane returns
-// chunk 66 (the sum of the slot-65 high words) in r66.  Reads are skewed so the
-// 32 lanes hit 32 distinct banks.
-__device__ __forceinline__ void warp_reduce_planes(unsigned char *warp_smem, int lane,
-                                                   long long &r0, long long &r1,
-                                                   long long &r2, long long &r66) {
-  const uint32_t *Lp = reinterpret_cast<const uint32_t *>(warp_smem);
-  const unsigned long long *Hp = reinterpret_cast<const unsigned long long *>(warp_smem + kLPlane);
-  unsigned long long s0 = 0, s1 = 0, s2 = 0;
-  const int rowa = lane, rowb = lane + 32, rowc = lane + 64;
-#pragma unroll 8
-  for (int i = 0; i < 32; ++i) {
-    const int col = (i + lane) & 31;
-    s0 += Lp[rowa * 32 + col];
-    s1 += Lp[rowb * 32 + col];
-    if (rowc < kSlots) s2 += Lp[rowc * 32 + col];
-  }
-  long long h = static_cast<long long>(Hp[(kSlots - 1) * 32 + lane]);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
-  r0 = static_cast<long long>(s0);
-  r1 = static_cast<long long>(s1);
-  r2 = static_cast<long long>(s2);
-  r66 = h;
 }
 
 // 256-bit streaming load (LDG.E.NA.ENL2.256): 4 terms per lane per instruction.
@@ -240,17 +522,36 @@ __device__ __forceinline__ void load_batch(Batch &b, const double *X4, long long
   }
 }
 
+// Bulk L2 prefetch (cp.async.bulk.prefetch.L2) of one batch-sized stretch of
+// 32-byte vectors starting at vector v0, clipped to vend.  Issued by one lane a
+// few batches ahead of the register loads; costs no registers, no shared memory.
+__device__ __forceinline__ void prefetch_l2(const double *X4, long long v0, long long vend) {
+  if (v0 >= vend) return;
+  long long nv = vend - v0;
+  if (nv > kVecPerLane * 32) nv = kVecPerLane * 32;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(X4 + 4 * v0),
+               "r"(static_cast<uint32_t>(nv * 32))
+               : "memory");
+}
+
 // Process one batch (kBatchTerms terms per lane).  index_of_vec0 is the
-// special-value index of term 0 of vector v0 of the batch.
-__device__ __forceinline__ void process_batch(const Lane &a, Specials &sp, Batch &b, int lane,
-                                              unsigned long long index_of_vec0) {
+// special-value index of term 0 of the batch's first vector.
+__device__ __forceinline__ void process_batch(const Lane &a, Pipe &pp, Specials &sp, Batch &b,
+                                              int lane, unsigned long long index_of_vec0) {
   uint32_t e[kVecPerLane][4];
   bool special = false;
 #pragma unroll
   for (int u = 0; u < kVecPerLane; ++u)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
+#if EXSUM_DECODE == 1
+      {
+        const uint32_t hw = b.w[u][2 * q + 1];
+        e[u][q] = __umulhi(hw, 4096u) + static_cast<uint32_t>(__mulhi(static_cast<int>(hw), 1)) * 2048u;
+      }
+#else
       e[u][q] = exponent_field(b.w[u][2 * q + 1]);
+#endif
       special |= e[u][q] == 0x7FFu;
     }
   if (special) {  // rare: record Inf/NaN and turn them into zero terms
@@ -266,25 +567,53 @@ __device__ __forceinline__ void process_batch(const Lane &a, Specials &sp, Batch
           e[u][q] = 0u;
         }
   }
+#if EXSUM_EXPERIMENT == 0
 #pragma unroll
   for (int u = 0; u < kVecPerLane; ++u)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) add_term(a, b.w[u][2 * q], b.w[u][2 * q + 1], e[u][q]);
+    for (int q = 0; q < 4; ++q) stream_term(a, pp, b.w[u][2 * q], b.w[u][2 * q + 1], e[u][q]);
+#else
+  // Tuning experiments only (wrong sums): 1 = same per-term ALU work, register
+  // accumulation, one shared RMW per batch; 2 = loads only.
+  uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+  for (int u = 0; u < kVecPerLane; ++u)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t lo = b.w[u][2 * q], hi = b.w[u][2 * q + 1];
+#if EXSUM_EXPERIMENT == 1
+      const uint32_t ep = max(e[u][q], 1u);
+      const uint32_t imp = e[u][q] ? 0x100000u : 0u;
+      const uint32_t s = static_cast<uint32_t>(static_cast<int32_t>(hi) >> 31);
+      const uint32_t mx = ((hi & 0xFFFFFu) | imp) ^ s;
+      const uint32_t lx = lo ^ s;
+      const uint32_t w0 = __funnelshift_l(s, lx, ep), w1 = __funnelshift_l(lx, mx, ep);
+      const uint32_t w2 = __funnelshift_l(mx, s, ep);
+      asm("add.cc.u32 %0, %0, %4;\n\taddc.cc.u32 %1, %1, %5;\n\taddc.cc.u32 %2, %2, %6;\n\taddc.u32 %3, %3, %7;"
+          : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3) : "r"(w0), "r"(w1), "r"(w2), "r"(ep));
+#else
+      r0 ^= lo;
+      r1 ^= hi;
+#endif
+    }
+  acc::add_term(a, r0 ^ r2, r1 ^ r3, 5u);
+#endif
 }
 
-// Accumulate x[begin, end) into the calling warp's lane slots.  `index_base`
-// is added to positions to form special-value indices.  norm_count tracks
-// batches since the last renormalisation (warp-uniform).
+// Accumulate x[begin, end) into the calling warp's lane accumulators.
+// index_base is added to positions to form special-value indices; norm_count
+// counts batches since the last renormalisation (warp-uniform).
 __device__ void warp_accumulate(const double *__restrict__ x, unsigned long long begin,
                                 unsigned long long end, unsigned long long index_base,
                                 const Lane &a, Specials &sp, int &norm_count, int lane) {
   if (begin >= end) return;
-  // Scalar head up to 32-byte alignment of &x[pos].
+  // Scalar head up to 32-byte alignment of &x[pos], scalar tail after the vectors.
   const uintptr_t addr = reinterpret_cast<uintptr_t>(x + begin);
   unsigned long long head = ((32u - (addr & 31u)) & 31u) >> 3;
   if (head > end - begin) head = end - begin;
+  const unsigned long long *xb = reinterpret_cast<const unsigned long long *>(x);
   if (lane < static_cast<int>(head)) {
-    const unsigned long long bits = __ldg(reinterpret_cast<const unsigned long long *>(x) + begin + lane);
+    const unsigned long long bits = __ldg(xb + begin + lane);
     add_term_checked(a, sp, static_cast<uint32_t>(bits), static_cast<uint32_t>(bits >> 32),
                      index_base + begin + lane);
   }
@@ -293,7 +622,7 @@ __device__ void warp_accumulate(const double *__restrict__ x, unsigned long long
   const double *X4 = x + vbeg_t;                   // 32-byte aligned
   const unsigned long long tail_t = vbeg_t + 4ull * static_cast<unsigned long long>(nvec);
   if (lane < static_cast<int>(end - tail_t)) {
-    const unsigned long long bits = __ldg(reinterpret_cast<const unsigned long long *>(x) + tail_t + lane);
+    const unsigned long long bits = __ldg(xb + tail_t + lane);
     add_term_checked(a, sp, static_cast<uint32_t>(bits), static_cast<uint32_t>(bits >> 32),
                      index_base + tail_t + lane);
   }
@@ -301,28 +630,40 @@ __device__ void warp_accumulate(const double *__restrict__ x, unsigned long long
   constexpr long long kStep = kVecPerLane * 32;
   Batch b0, b1;
   long long v = 0;
+  if (kPrefetchBatches > 0 && lane == 0) {
+    for (int d = 1; d <= kPrefetchBatches; ++d) prefetch_l2(X4, d * kStep, nvec);
+  }
   load_batch(b0, X4, 0, nvec, lane);
   const unsigned long long ib = index_base + vbeg_t;
+  Pipe pp;
+  stream_begin(a, pp);
   while (true) {
     long long nx = v + kStep;
+    if (kPrefetchBatches > 0 && lane == 0) prefetch_l2(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
     if (nx < nvec) load_batch(b1, X4, nx, nvec, lane);
-    process_batch(a, sp, b0, lane, ib + 4ull * static_cast<unsigned long long>(v));
+    process_batch(a, pp, sp, b0, lane, ib + 4ull * static_cast<unsigned long long>(v));
     if (++norm_count >= kNormEvery) {
-      normalize_lane(a);
+      stream_end(a, pp);
+      acc::normalize(a);
+      stream_begin(a, pp);
       norm_count = 0;
     }
     v = nx;
     if (v >= nvec) break;
     nx = v + kStep;
+    if (kPrefetchBatches > 0 && lane == 0) prefetch_l2(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
     if (nx < nvec) load_batch(b0, X4, nx, nvec, lane);
-    process_batch(a, sp, b1, lane, ib + 4ull * static_cast<unsigned long long>(v));
+    process_batch(a, pp, sp, b1, lane, ib + 4ull * static_cast<unsigned long long>(v));
     if (++norm_count >= kNormEvery) {
-      normalize_lane(a);
+      stream_end(a, pp);
+      acc::normalize(a);
+      stream_begin(a, pp);
       norm_count = 0;
     }
     v = nx;
     if (v >= nvec) break;
   }
+  stream_end(a, pp);
 }
 
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
@@ -334,7 +675,7 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
   return v;
 }
 
-// Finalise a canonical record: resolve specials, round, write outputs.
+// Finalise a record: canonicalise, resolve specials, round, write outputs.
 __device__ void emit_record(int64_t *c, unsigned long long P, unsigned long long M,
                             unsigned long long N, unsigned long long payload, double *result,
                             exsum_partial *partial) {
@@ -363,17 +704,18 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
                  double *result, exsum_partial *partial) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_last;
+  __shared__ unsigned long long s_spec[4];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   unsigned char *wsm = smem + warp * kWarpSmem;
   long long *scratch = reinterpret_cast<long long *>(smem + kWarps * kWarpSmem);
-  zero_warp_planes(wsm, lane);
+  zero_warp(wsm, lane);
   __syncwarp();
-  const Lane a = lane_view(wsm, lane);
+  const Lane a = acc::lane_view(wsm, lane);
   Specials sp{~0ull, ~0ull, ~0ull};
   int norm_count = 0;
 
-  // Contiguous per-warp ranges, boundaries on 4-term multiples.
+  // K1: contiguous per-warp ranges, boundaries on 4-term multiples.
   const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * kWarps + warp;
   const unsigned long long nw = static_cast<unsigned long long>(gridDim.x) * kWarps;
   const unsigned long long quads = (n + 3) >> 2;
@@ -381,16 +723,8 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
   const unsigned long long tb = qb * 4, te = min(qe * 4, n);
   warp_accumulate(x, tb, te, base_index, a, sp, norm_count, lane);
 
-  // K2: lane renormalisation and the warp's 67 chunk sums.
-  normalize_lane(a);
-  __syncwarp();
-  long long r0, r1, r2, r66;
-  warp_reduce_planes(wsm, lane, r0, r1, r2, r66);
-  long long *row = scratch + warp * kChunks;
-  row[lane] = r0;
-  row[lane + 32] = r1;
-  if (lane < 2) row[lane + 64] = r2;
-  if (lane == 0) row[66] = r66;
+  // K2: the warp's 67 chunk sums.
+  acc::warp_chunks(wsm, a, lane, scratch + warp * kChunks);
   const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                            N = warp_min_u64(sp.N);
   if (lane == 0) {
@@ -411,35 +745,43 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
   if (threadIdx.x == 0) s_last = atomicAdd(&ws->done, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!s_last) return;
+  // Last CTA: gather the workspace in parallel, then one thread rounds.
   __threadfence();
+  if (threadIdx.x < kChunks) {
+    scratch[threadIdx.x] = static_cast<long long>(__ldcg(&ws->chunk[threadIdx.x]));
+    if (finalize) ws->chunk[threadIdx.x] = 0;
+  } else if (threadIdx.x < kChunks + 4) {
+    const int j = threadIdx.x - kChunks;
+    const unsigned long long *src = &ws->inv_pinf;
+    s_spec[j] = __ldcg(src + j);  // inv_pinf, inv_ninf, inv_nan, nan_payload
+    if (finalize) const_cast<unsigned long long *>(src)[j] = 0;
+  }
+  __syncthreads();
   if (threadIdx.x != 0) return;
-  // Last CTA: the NaN payload of the first NaN, if it lies in this launch.
-  const unsigned long long Nf = ~__ldcg(&ws->inv_nan);
-  unsigned long long payload = __ldcg(&ws->nan_payload);
+  const unsigned long long Nf = ~s_spec[2];
+  unsigned long long payload = s_spec[3];
   if (Nf != ~0ull && Nf >= base_index && Nf - base_index < n) {
     payload = __ldcg(reinterpret_cast<const unsigned long long *>(x) + (Nf - base_index));
-    ws->nan_payload = payload;
+    if (!finalize) ws->nan_payload = payload;  // the first NaN so far lies in this launch
   }
   ws->done = 0;
   if (!finalize) return;
   int64_t c[kChunks];
-  for (int i = 0; i < kChunks; ++i) {
-    c[i] = static_cast<int64_t>(__ldcg(&ws->chunk[i]));
-    ws->chunk[i] = 0;
-  }
-  const unsigned long long Pf = ~__ldcg(&ws->inv_pinf), Mf = ~__ldcg(&ws->inv_ninf);
-  ws->inv_pinf = ws->inv_ninf = ws->inv_nan = 0;
-  ws->nan_payload = 0;
-  emit_record(c, Pf, Mf, Nf, payload, result, partial);
+  for (int i = 0; i < kChunks; ++i) c[i] = scratch[i];
+  emit_record(c, ~s_spec[0], ~s_spec[1], Nf, payload, result, partial);
 }
 
 // Finalise a workspace filled by exsum_cuda_accumulate launches.
 __global__ void exsum_finalize_kernel(Workspace *ws, double *result, exsum_partial *partial) {
-  int64_t c[kChunks];
-  for (int i = 0; i < kChunks; ++i) {
-    c[i] = static_cast<int64_t>(ws->chunk[i]);
-    ws->chunk[i] = 0;
+  __shared__ long long sc[kChunks];
+  if (threadIdx.x < kChunks) {
+    sc[threadIdx.x] = static_cast<long long>(ws->chunk[threadIdx.x]);
+    ws->chunk[threadIdx.x] = 0;
   }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  int64_t c[kChunks];
+  for (int i = 0; i < kChunks; ++i) c[i] = sc[i];
   const unsigned long long P = ~ws->inv_pinf, M = ~ws->inv_ninf, N = ~ws->inv_nan;
   const unsigned long long payload = ws->nan_payload;
   ws->inv_pinf = ws->inv_ninf = ws->inv_nan = 0;
@@ -450,8 +792,6 @@ __global__ void exsum_finalize_kernel(Workspace *ws, double *result, exsum_parti
 
 // ------------------------------------------------------------------------- K4
 
-constexpr int kSegSmem = kWarps * kWarpSmem + kScratch;
-
 __global__ void __launch_bounds__(kThreads, 1)
 exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *__restrict__ offs,
                        unsigned long long nseg, Workspace *__restrict__ ws, double *out,
@@ -461,27 +801,20 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
   const int warp = threadIdx.x >> 5;
   unsigned char *wsm = smem + warp * kWarpSmem;
   long long *row = reinterpret_cast<long long *>(smem + kWarps * kWarpSmem) + warp * kChunks;
-  const Lane a = lane_view(wsm, lane);
+  const Lane a = acc::lane_view(wsm, lane);
   while (true) {
     unsigned int s = 0;
     if (lane == 0) s = atomicAdd(&ws->seg_next, 1u);
     s = __shfl_sync(0xffffffffu, s, 0);
     if (s >= nseg) break;
-    zero_warp_planes(wsm, lane);
+    zero_warp(wsm, lane);
     __syncwarp();
     const unsigned long long b = offs[s], e = offs[s + 1];
     Specials sp{~0ull, ~0ull, ~0ull};
     int norm_count = 0;
     // indices local to the segment: position - b
     warp_accumulate(x, b, e, 0ull - b, a, sp, norm_count, lane);
-    normalize_lane(a);
-    __syncwarp();
-    long long r0, r1, r2, r66;
-    warp_reduce_planes(wsm, lane, r0, r1, r2, r66);
-    row[lane] = r0;
-    row[lane + 32] = r1;
-    if (lane < 2) row[lane + 64] = r2;
-    if (lane == 0) row[66] = r66;
+    acc::warp_chunks(wsm, a, lane, row);
     const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                              N = warp_min_u64(sp.N);
     __syncwarp();
@@ -549,29 +882,27 @@ using namespace exsum_b200::dev;
 
 namespace {
 
-int g_num_sms = 0;
+constexpr int kMaxDevices = 64;
+int g_num_sms[kMaxDevices] = {};
+bool g_configured[kMaxDevices] = {};
 
-int num_sms() {
-  if (g_num_sms > 0) return g_num_sms;
+// Per-device one-time setup: SM count and the >48 KB dynamic smem opt-in.
+int prepare_device(int *sms) {
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-  int sms = 0;
-  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-  g_num_sms = sms;
-  return sms;
-}
-
-bool configured = false;
-
-int configure_kernels() {
-  if (configured) return EXSUM_OK;
-  if (cudaFuncSetAttribute(exsum_sum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kSumSmem) != cudaSuccess)
-    return EXSUM_ECUDA;
-  if (cudaFuncSetAttribute(exsum_segmented_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           kSegSmem) != cudaSuccess)
-    return EXSUM_ECUDA;
-  configured = true;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return EXSUM_ECUDA;
+  if (!g_configured[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      return EXSUM_ECUDA;
+    if (cudaFuncSetAttribute(exsum_sum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(exsum_segmented_kernel,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess)
+      return EXSUM_ECUDA;
+    g_num_sms[dev] = n;
+    g_configured[dev] = true;
+  }
+  *sms = g_num_sms[dev];
   return EXSUM_OK;
 }
 
@@ -590,12 +921,10 @@ unsigned grid_for(unsigned long long n, int sms) {
 int sum_launch(const double *d_x, size_t n, uint64_t base_index, void *d_ws, size_t ws_bytes,
                void *stream, int finalize, double *d_result, exsum_partial *d_partial) {
   if (!d_ws || ws_bytes < sizeof(Workspace) || (n && !d_x)) return EXSUM_EINVAL;
-  int st = configure_kernels();
+  int sms = 0;
+  const int st = prepare_device(&sms);
   if (st) return st;
-  const int sms = num_sms();
-  if (sms <= 0) return EXSUM_ECUDA;
-  const unsigned grid = grid_for(n, sms);
-  exsum_sum_kernel<<<grid, kThreads, kSumSmem, static_cast<cudaStream_t>(stream)>>>(
+  exsum_sum_kernel<<<grid_for(n, sms), kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(
       d_x, n, base_index, static_cast<Workspace *>(d_ws), finalize, d_result, d_partial);
   return launch_status();
 }
@@ -628,7 +957,7 @@ int exsum_cuda_accumulate(const double *d_x, size_t n, uint64_t base_index, void
 int exsum_cuda_finalize(double *d_result, exsum_partial *d_partial, void *d_ws, size_t ws_bytes,
                         void *stream) {
   if (!d_ws || ws_bytes < sizeof(Workspace)) return EXSUM_EINVAL;
-  exsum_finalize_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(
+  exsum_finalize_kernel<<<1, 96, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<Workspace *>(d_ws), d_result, d_partial);
   return launch_status();
 }
@@ -640,13 +969,12 @@ int exsum_cuda_sum_segmented(const double *d_x, const uint64_t *d_offsets, size_
     return EXSUM_EINVAL;
   if (nseg == 0) return EXSUM_OK;
   if (nseg >= 0xFFFFFFFFull) return EXSUM_EINVAL;
-  int st = configure_kernels();
+  int sms = 0;
+  const int st = prepare_device(&sms);
   if (st) return st;
-  const int sms = num_sms();
-  if (sms <= 0) return EXSUM_ECUDA;
   unsigned long long g = (nseg + kWarps - 1) / kWarps;
   if (g > static_cast<unsigned long long>(sms)) g = sms;
-  exsum_segmented_kernel<<<static_cast<unsigned>(g), kThreads, kSegSmem,
+  exsum_segmented_kernel<<<static_cast<unsigned>(g), kThreads, kSmem,
                            static_cast<cudaStream_t>(stream)>>>(
       d_x, reinterpret_cast<const unsigned long long *>(d_offsets), nseg,
       static_cast<Workspace *>(d_ws), d_out, d_partials);

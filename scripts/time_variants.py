@@ -1,0 +1,54 @@
+"""Time kernel variants (lib/variants/*.so) on configs 2/3 (1e8) and 4 (1e9).
+
+Each variant runs in its own process (EXSUM_LIB selects the .so).  Prints one
+line per (variant, config): ms per sum, GB/s, result bits (must agree).
+"""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+CHILD = r'''
+import sys, json, torch, numpy as np
+sys.path.insert(0, %r)
+from paper_1505_05571_b200 import _lib, ops
+dev = torch.device("cuda", 0)
+out = {}
+for config, n, K in %s:
+    x = torch.empty(n, dtype=torch.float64, device=dev)
+    _lib.call("exsum_cuda_gen", config, 1, n, 0, n, x.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    res = torch.empty(1, dtype=torch.float64, device=dev)
+    part = torch.empty(ops.PARTIAL_BYTES, dtype=torch.uint8, device=dev)
+    ws = ops.Workspace(dev)
+    for _ in range(3):
+        ops.exact_sum_tensor(x, result=res, partial=part, workspace=ws)
+    torch.cuda.synchronize()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record()
+    for _ in range(K):
+        ops.exact_sum_tensor(x, result=res, partial=part, workspace=ws)
+    en.record(); torch.cuda.synchronize()
+    ms = st.elapsed_time(en) / K
+    out[config] = (ms, 8 * n / ms / 1e6, int(np.float64(res.item()).view(np.uint64)))
+    del x; torch.cuda.empty_cache()
+print("RESULT", json.dumps(out))
+'''
+
+cases = [(2, 100_000_000, 20), (3, 100_000_000, 20), (4, 1_000_000_000, 5)]
+variants = sys.argv[1:] or sorted(p.stem for p in (ROOT / "paper_1505_05571_b200/lib/variants").glob("*.so"))
+variants = ["default"] + [v for v in variants if v != "default"]
+for v in variants:
+    env = dict(os.environ)
+    if v != "default":
+        env["EXSUM_LIB"] = str(ROOT / "paper_1505_05571_b200/lib/variants" / f"{v}.so")
+    p = subprocess.run([sys.executable, "-c", CHILD % (str(ROOT), repr(cases))], env=env,
+                       capture_output=True, text=True)
+    line = [l for l in p.stdout.splitlines() if l.startswith("RESULT")]
+    if not line:
+        print(v, "FAILED", p.stderr[-2000:], flush=True)
+        continue
+    res = json.loads(line[0][7:])
+    print(v, " ".join(f"c{c}: {ms:.3f}ms {gbs:.0f}GB/s {bits:#x}" for c, (ms, gbs, bits) in res.items()),
+          flush=True)
