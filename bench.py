@@ -1,0 +1,343 @@
+"""Benchmark: exact float64 summation on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+One step = one exact, correctly rounded sum of the whole workload already
+resident in HBM (exsum_cuda_sum: stream -> per-lane superaccumulators -> CTA
+combine -> round; for N > 1 also the all-gather of the 592-byte records over
+NCCL and the device merge).  Prints ONE JSON line (rank 0).
+
+Workloads (BASELINE.json configs, synthetic, seeded counter-based generator):
+  --config 2 (default)  N = 1e8 U[0,1) per GPU (weak scaling; global array N x 1e8)
+  --config 3            N = 1e8 random sign/exponent/mantissa + 1% denormals per GPU
+  --config 4            N = 1e9 heavy cancellation, sharded (strong scaling)
+Inputs are 0.8-8 GB per GPU, far larger than the 126 MB L2, so no flush is
+needed between steps.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref: the
+unmodified /root/reference sources; parallel_exact_sum with every host thread)
+on the same workload, rank 0 only, each step a bounded sample of the array.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "exact-sum GB/s (terms/s) per GPU and 8-GPU, % of HBM roofline; bit-exact"
+WORKLOADS = {
+    1: dict(n=1_000, per_gpu=True, desc="config1: N=1e3 U[-1,1) (small superaccumulator case)"),
+    2: dict(n=100_000_000, per_gpu=True, desc="config2: N=1e8 float64 U[0,1) per GPU (narrow exponent range)"),
+    3: dict(n=100_000_000, per_gpu=True, desc="config3: N=1e8 float64, uniform sign/exponent 1..2046/mantissa + 1% denormals per GPU"),
+    4: dict(n=1_000_000_000, per_gpu=False, desc="config4: N=1e9 float64 heavy cancellation, shuffled, sharded across GPUs"),
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=0, help="timed steps (default: ~0.5 s)")
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
+    p.add_argument("--n", type=float, default=0, help="override terms (per GPU for weak configs)")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def bits(v: float) -> int:
+    return int(np.array([v], dtype=np.float64).view(np.uint64)[0])
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons (NVML) while the timed region runs."""
+
+    REASONS = {  # nvmlClocksEventReason* bits
+        0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - clocks are reported as unavailable
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.reasons |= {n for b, n in self.REASONS.items() if mask & b}
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def report(self):
+        if not self.nv or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------- CPU legs
+
+def cpu_reference_rate(x: np.ndarray, budget_s: float):
+    """Reference parallel_exact_sum (all host threads) over x; repeated until
+    budget_s.  Returns (GB/s, cores, kind, sample description, result bits)."""
+    from oracle.port import checker
+    chk = checker()
+    threads = os.cpu_count() or 1
+    chk.set_threads(threads)
+    chk.parallel_exact_sum(x[: min(x.size, 1 << 20)], threads)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        r = chk.parallel_exact_sum(x, threads)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    gbs = 8.0 * x.size * reps / el / 1e9
+    sample = (f"{x.size:.3g} terms of the same workload x {reps} passes, "
+              f"parallel_exact_sum(parts={threads}), {el:.2f} s wall")
+    return gbs, threads, chk.kind, sample, bits(r)
+
+
+def run_reference_arm(args, wl, n_total):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference; the others exit 0 without work
+    from paper_1505_05571_b200 import _lib
+    from oracle.port import checker
+    chk = checker()
+    threads = os.cpu_count() or 1
+    chk.set_threads(threads)
+    x = np.empty(n_total, dtype=np.float64)
+    _lib.call("exsum_host_gen", args.config, args.seed, n_total, 0, n_total, x.ctypes.data)
+    # bounded sample per step: whole run (warmup + steps) within ~90 s
+    t0 = time.perf_counter()
+    chk.parallel_exact_sum(x, threads)
+    t_full = time.perf_counter() - t0
+    steps = args.steps or 10
+    per_step_budget = 90.0 / max(1, steps + args.warmup)
+    m = n_total if t_full <= per_step_budget else max(1 << 16, int(n_total * per_step_budget / t_full))
+    sample = x[:m]
+    for _ in range(args.warmup):
+        chk.parallel_exact_sum(sample, threads)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        r = chk.parallel_exact_sum(sample, threads)
+    el = time.perf_counter() - t0
+    gbs = 8.0 * m * steps / el / 1e9
+    desc = (f"first {m:.4g} of {n_total:.4g} terms per step, parallel_exact_sum(parts={threads}) "
+            f"on {threads} host threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": round(el / steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak" if wl["per_gpu"] else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based generator, BASELINE.json shapes)",
+        "config": {"workload": wl["desc"], "n_total": n_total, "sample_terms": m},
+        "terms_per_s": round(gbs * 1e9 / 8, 1),
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads,
+                         "kind": chk.kind, "sample": desc},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "result_bits": hex(bits(r)),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU arm
+
+def main():
+    args = parse()
+    wl = WORKLOADS[args.config]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit("--gpus > 1 must be launched with torch.distributed.run (one rank per GPU)")
+    n_arg = int(args.n) if args.n else wl["n"]
+    n_total = n_arg * world if wl["per_gpu"] else n_arg
+    if args.impl == "reference":
+        return run_reference_arm(args, wl, n_total)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1505_05571_b200 import _lib, ops
+    from paper_1505_05571_b200.distributed import exchange_partials, shard_bounds
+
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+    begin, end = shard_bounds(n_total, world, rank)
+    n_local = end - begin
+    x = torch.empty(n_local, dtype=torch.float64, device=dev)
+    _lib.call("exsum_cuda_gen", args.config, args.seed, n_total, begin, n_local, x.data_ptr(),
+              stream.cuda_stream)
+    ws = ops.Workspace(dev)
+    res = torch.empty(1, dtype=torch.float64, device=dev)
+    part = torch.empty(ops.PARTIAL_BYTES, dtype=torch.uint8, device=dev)
+
+    def step(kernel_events=None):
+        if kernel_events is not None:
+            kernel_events[0].record(stream)
+        ops.exact_sum_tensor(x, base_index=begin, result=res, partial=part, workspace=ws)
+        if kernel_events is not None:
+            kernel_events[1].record(stream)
+        if world > 1:
+            return ops.merge_partials(exchange_partials(part))[0]
+        return res
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    # steps: default ~0.5 s of timed region (clock sampling needs a few hundred ms)
+    t0 = time.perf_counter()
+    for _ in range(5):
+        step()
+    torch.cuda.synchronize()
+    per = (time.perf_counter() - t0) / 5
+    steps = args.steps or max(10, min(20000, int(0.5 / max(per, 1e-6))))
+
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for i in range(steps):
+            out = step(kev[i])
+        stop.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = start.elapsed_time(stop)
+    k_ms = sum(a.elapsed_time(b) for a, b in kev) / steps
+    t = torch.tensor([ms, k_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, k_ms = float(t[0]), float(t[1])
+    result_bits = bits(float(out.item()))
+
+    value = 8.0 * n_total * steps / (ms / 1e3) / 1e9          # whole-job GB/s
+    achieved = 8.0 * n_local / (k_ms / 1e3) / 1e9              # dominant kernel, per GPU
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    traffic = None
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(f"config{args.config}", {}).get("dram_bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            traffic = None
+
+    # e2e through the C ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
+        hx.copy_(x)
+        ctx = ops.HostContext(local, staging_bytes=512 << 20)
+        ctx.sum_ptr(hx.data_ptr(), n_local)  # warm
+        e2e_steps = max(3, min(20, steps))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            if world > 1:
+                v, rec = ctx.sum(hx.numpy(), want_partial=True)
+                recs = exchange_partials(torch.frombuffer(bytearray(bytes(rec)), dtype=torch.uint8).to(dev))
+                e_res = float(ops.merge_partials(recs)[0].item())
+            else:
+                e_res = ctx.sum_ptr(hx.data_ptr(), n_local)
+        el = time.perf_counter() - t0
+        te = torch.tensor([el], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        el = float(te[0])
+        assert bits(e_res) == result_bits, "e2e path disagrees with the device path"
+        e2e = {"value": round(8.0 * n_total * e2e_steps / el / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": 8 * n_local + (ops.PARTIAL_BYTES if world > 1 else 0),
+               "d2h_bytes_per_step": 8 + (ops.PARTIAL_BYTES if world > 1 else 0),
+               "path": "exsum_context_sum (pinned host -> 2 x 256 MB staging ring, copy/compute overlap)"}
+        del hx, ctx
+
+    cpu = None
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        h = x.cpu().numpy()
+        from oracle.port import checker
+        chk = checker()
+        parity = bits(chk.exact_sum(h)) == result_bits
+        gbs, cores, kind, sample, rb = cpu_reference_rate(h, budget_s=3.0)
+        parity = parity and rb == result_bits
+        cpu = {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": kind,
+               "sample": sample}
+        del h
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+            "steps": steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms / steps, 4),
+            "higher_is_better": True, "scaling": "weak" if wl["per_gpu"] else "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based generator, BASELINE.json shapes)",
+            "config": {"workload": wl["desc"], "n_total": n_total, "n_per_gpu": n_local,
+                       "parallelism": f"shard{world}" + (" + NCCL all-gather of 592 B records" if world > 1 else ""),
+                       "l2": "inputs >= 800 MB per GPU > 126 MB L2; no flush needed"},
+            "terms_per_s": round(value * 1e9 / 8, 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "kernel": "exsum_sum_kernel", "kernel_ms": round(k_ms, 4),
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": steps * (2 if world > 1 else 1),
+            "clocks": clocks.report(),
+            "result_bits": hex(result_bits),
+            "bit_exact_vs_oracle": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,86 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes binding of the C restatement (oracle/port).
+
+Built by ``make -C oracle port`` into oracle/lib/libexsum_port.so (our own
+sources, so it can also be rebuilt on a GPU box that has no /root/reference).
+Same method names as oracle/ref.py so tests can use either as the checker.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+PORT_SO = HERE / "lib" / "libexsum_port.so"
+
+
+def ensure_built() -> Path:
+    src = HERE / "port" / "exsum_port.c"
+    if not PORT_SO.exists() or PORT_SO.stat().st_mtime < src.stat().st_mtime:
+        subprocess.run(["make", "-s", "-C", str(HERE), "port"], check=True)
+    return PORT_SO
+
+
+class Port:
+    kind = "port"
+
+    def __init__(self):
+        L = self.lib = C.CDLL(str(ensure_built()))
+        vp, sz, i32, dbl, u64 = C.c_void_p, C.c_size_t, C.c_int, C.c_double, C.c_uint64
+        for name, res, args in [
+            ("port_exact_sum", dbl, [vp, sz, i32]),
+            ("port_parallel_exact_sum", dbl, [vp, sz, i32, sz, i32]),
+            ("port_canonical", i32, [vp, sz, vp, C.POINTER(u64), C.POINTER(u64)]),
+            ("port_segmented_sum", None, [vp, vp, sz, vp, i32]),
+            ("port_max_threads", i32, []),
+        ]:
+            f = getattr(L, name)
+            f.restype, f.argtypes = res, args
+        self._threads = 0
+
+    @staticmethod
+    def _arr(x) -> np.ndarray:
+        return np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+
+    def exact_sum(self, x, method: str = "large") -> float:
+        a = self._arr(x)
+        return self.lib.port_exact_sum(a.ctypes.data, a.size, 0 if method == "small" else 1)
+
+    def parallel_exact_sum(self, x, parts: int, threshold: int = 1000) -> float:
+        a = self._arr(x)
+        return self.lib.port_parallel_exact_sum(a.ctypes.data, a.size, parts, threshold,
+                                                self._threads)
+
+    def canonical(self, x):
+        a = self._arr(x)
+        ch = np.zeros(67, dtype=np.int64)
+        ib, nb = C.c_uint64(), C.c_uint64()
+        top = self.lib.port_canonical(a.ctypes.data, a.size, ch.ctypes.data, C.byref(ib),
+                                      C.byref(nb))
+        return ch, top, ib.value, nb.value
+
+    def segmented_sum(self, x, offsets, threads: int = 0) -> np.ndarray:
+        a = self._arr(x)
+        o = np.ascontiguousarray(offsets, dtype=np.uint64)
+        out = np.zeros(o.size - 1, dtype=np.float64)
+        self.lib.port_segmented_sum(a.ctypes.data, o.ctypes.data, o.size - 1, out.ctypes.data,
+                                    threads or self._threads)
+        return out
+
+    def set_threads(self, n: int) -> None:
+        self._threads = n
+
+    def max_threads(self) -> int:
+        return self.lib.port_max_threads()
+
+
+def checker():
+    """The compiled reference when present (oracle/_ref), else the C restatement."""
+    from . import ref
+    if ref.available():
+        r = ref.get()
+        r.kind = "reference"
+        return r
+    return Port()

@@ -1,0 +1,78 @@
+"""Multi-GPU exact sum: the reference's split-merge, one shard per GPU.
+
+Reference: parallel_exact_sum (vector_ops.cpp:172-186) splits the array into
+contiguous segments (split, vector_ops.cpp:37-49), sums each into its own
+accumulator and merges the partials (merge_partials, vector_ops.cpp:64-70).
+Here a segment is a GPU's shard: each rank reduces its shard on its device to
+a 592-byte exsum_partial record (canonical 67-chunk accumulator + global
+first-index record of +Inf/-Inf/NaN), the records are exchanged with ONE
+all-gather (NCCL over NVLink on CUDA tensors), and every rank merges the k
+records with exsum_cuda_merge.  Because the canonical form is unique and the
+special values are resolved by global index, the result bits equal the serial
+exact_sum for every world size.
+
+(The reference's own parallel merge resolves Inf/NaN per part, which can lose
+a NaN payload when opposite infinities sit in other parts; SURVEY.md §0.  This
+path deliberately keeps the serial semantics of exact_sum.)
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._lib import ExsumPartial
+from .ops import PARTIAL_BYTES, exact_sum_tensor, merge_partials, partial_from_tensor
+
+__all__ = ["shard_bounds", "exchange_partials", "merge_records", "parallel_exact_sum"]
+
+
+def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous split with the remainder spread over the first shards
+    (split, vector_ops.cpp:37-49)."""
+    p = max(world, 1)
+    base, extra = divmod(n, p)
+    begin = rank * base + min(rank, extra)
+    return begin, begin + base + (1 if rank < extra else 0)
+
+
+def exchange_partials(record: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather one 592-byte record per rank -> uint8 [world, 592] (rank order)."""
+    if record.numel() != PARTIAL_BYTES or record.dtype != torch.uint8:
+        raise ValueError("record must be a 592-byte uint8 tensor")
+    world = dist.get_world_size(group)
+    out = torch.empty(world * PARTIAL_BYTES, dtype=torch.uint8, device=record.device)
+    dist.all_gather_into_tensor(out, record.contiguous().reshape(-1), group=group)
+    return out.view(world, PARTIAL_BYTES)
+
+
+def merge_records(records: torch.Tensor):
+    """Merge gathered records.  CUDA tensors: exsum_cuda_merge on the device,
+    returning (result tensor[1], merged record tensor[592]).  CPU tensors (host
+    objects, e.g. records assembled by host code): exsum_partial_merge, returning
+    (float, ExsumPartial)."""
+    records = records.contiguous().view(torch.uint8).reshape(-1, PARTIAL_BYTES)
+    if records.is_cuda:
+        return merge_partials(records)
+    k = records.shape[0]
+    arr = (ExsumPartial * k).from_buffer_copy(records.numpy().tobytes())
+    out, merged = C.c_double(), ExsumPartial()
+    _lib.call("exsum_partial_merge", arr, k, C.byref(merged), C.byref(out))
+    return out.value, merged
+
+
+def parallel_exact_sum(shard: torch.Tensor, *, base_index: int, group=None) -> torch.Tensor:
+    """Exact sum of the logical array whose slice [base_index, base_index + len)
+    is this rank's CUDA float64 ``shard``.  Returns the rounded sum (1-element
+    float64 tensor on the shard's device), identical on every rank."""
+    if not shard.is_cuda:
+        raise ValueError("parallel_exact_sum runs on the GPU: shard must be a CUDA tensor")
+    _, rec = exact_sum_tensor(shard, base_index=base_index)
+    result, _ = merge_partials(exchange_partials(rec, group))
+    return result
+
+
+def record_to_partial(rec: torch.Tensor) -> ExsumPartial:
+    return partial_from_tensor(rec)

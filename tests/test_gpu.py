@@ -1,0 +1,224 @@
+"""GPU parity: the sm_100a path through the C ABI vs the reference (-m gpu).
+
+Bit-exact on every case: rounded result bits AND the 67 canonical chunks of the
+exsum_partial record, against (a) golden vectors produced by the compiled
+reference, (b) the checker (oracle/_ref when present, else the C restatement
+oracle/port) at BASELINE sizes, (c) size-independent properties.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import bits_of
+
+pytestmark = pytest.mark.gpu
+
+ops = pytest.importorskip("paper_1505_05571_b200.ops")
+from paper_1505_05571_b200 import _lib  # noqa: E402
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dev_sum(x: torch.Tensor, base_index: int = 0):
+    r, p = ops.exact_sum_tensor(x, base_index=base_index)
+    return bits_of(r.item()), ops.partial_from_tensor(p)
+
+
+def gen(config, n, seed=1, first=0, total=None, device="cuda"):
+    x = torch.empty(n, dtype=torch.float64, device=device)
+    _lib.call("exsum_cuda_gen", config, seed, total or n, first, n, x.data_ptr(), stream())
+    return x
+
+
+def to_dev(x: np.ndarray, offset: int = 0) -> torch.Tensor:
+    """Device copy of x starting `offset` doubles into its allocation (misaligned starts)."""
+    buf = torch.zeros(x.size + offset, dtype=torch.float64, device="cuda")
+    if x.size:
+        buf[offset:] = torch.from_numpy(np.ascontiguousarray(x))
+    return buf[offset:]
+
+
+# ------------------------------------------------------------------ golden
+
+def test_golden_device_sum(golden, cuda):
+    for c in golden:
+        for off in (0, 1, 3):
+            got, part = dev_sum(to_dev(c["x"], off))
+            assert got == c["large"], (c["tag"], off)
+            assert list(part.acc.chunk) == c["chunks"], (c["tag"], off)
+            assert (part.acc.inf_bits, part.acc.nan_bits) == (c["inf_bits"], c["nan_bits"]), c["tag"]
+
+
+def test_golden_host_buffers(golden, cuda):
+    ctx = ops.HostContext(0, staging_bytes=1 << 20)  # tiny ring: many pipelined chunks
+    for c in golden:
+        assert bits_of(ctx.sum(c["x"])) == c["large"], c["tag"]
+    assert bits_of(ops.exact_sum(golden[5]["x"])) == golden[5]["large"]
+
+
+def test_golden_segmented(golden, cuda):
+    xs = [c["x"] for c in golden]
+    offs = np.zeros(len(xs) + 1, dtype=np.int64)
+    offs[1:] = np.cumsum([x.size for x in xs])
+    flat = torch.from_numpy(np.concatenate(xs)).cuda()
+    out, parts = ops.exact_sum_segmented(flat, torch.from_numpy(offs).cuda(), partials=True)
+    got = out.cpu().numpy().view(np.uint64)
+    recs = parts.cpu().numpy()
+    for i, c in enumerate(golden):
+        assert int(got[i]) == c["large"], c["tag"]
+        p = _lib.ExsumPartial.from_buffer_copy(recs[i].tobytes())
+        assert list(p.acc.chunk) == c["chunks"], c["tag"]
+
+
+def test_golden_split_merge_on_device(golden, cuda):
+    rng = np.random.default_rng(3)
+    for c in golden:
+        x = c["x"]
+        for k in (2, 5):
+            cuts = [0] + sorted(int(v) for v in rng.integers(0, x.size + 1, k - 1)) + [x.size]
+            recs = []
+            for i in range(k):
+                _, p = ops.exact_sum_tensor(to_dev(x[cuts[i]:cuts[i + 1]]), base_index=cuts[i])
+                recs.append(p)
+            r, merged = ops.merge_partials(torch.stack(recs))
+            assert bits_of(r.item()) == c["large"], (c["tag"], k)
+            assert list(ops.partial_from_tensor(merged).acc.chunk) == c["chunks"], c["tag"]
+
+
+def test_accumulate_finalize_incremental(golden, cuda):
+    x = np.concatenate([c["x"] for c in golden if c["group"] == "random"])
+    want = bits_of(__import__("oracle.port", fromlist=["Port"]).Port().exact_sum(x))
+    ws = ops.Workspace()
+    d = to_dev(x)
+    for lo in range(0, x.size, 997):
+        hi = min(lo + 997, x.size)
+        _lib.call("exsum_cuda_accumulate", d[lo:hi].data_ptr(), hi - lo, lo, ws.ptr,
+                  ops.WORKSPACE_BYTES, stream())
+    res = torch.empty(1, dtype=torch.float64, device="cuda")
+    _lib.call("exsum_cuda_finalize", res.data_ptr(), None, ws.ptr, ops.WORKSPACE_BYTES, stream())
+    assert bits_of(res.item()) == want
+
+
+# ---------------------------------------------------- edge cases, specials
+
+def test_edges(cuda):
+    f = lambda b: np.array([b], dtype=np.uint64).view(np.float64)[0]  # noqa: E731
+    cases = {
+        "empty": ([], 0),
+        "neg_zeros": ([-0.0] * 1000, 0),
+        "denormals": ([f(1)] * 100_000, 100_000),
+        "overflow_to_inf": ([1.7976931348623157e308] * 3, 0x7FF0000000000000),
+        "neg_overflow": ([-1.7976931348623157e308] * 3, 0xFFF0000000000000),
+        "inf_then_nan": ([np.inf] + [1.0] * 5000 + [f(0x7FF0000000000ABC)], 0x7FF0000000000ABC),
+        "both_inf_then_nan": ([np.inf, -np.inf] + [f(0x7FF0000000000ABC)], 0x7FF8000000000000),
+        "nan_first": ([f(0xFFF0000000000001), np.inf, -np.inf], 0xFFF0000000000001),
+        "neg_inf": ([-np.inf, 5.0, -np.inf], 0xFFF0000000000000),
+    }
+    for name, (vals, want) in cases.items():
+        got, _ = dev_sum(to_dev(np.array(vals, dtype=np.float64)))
+        assert got == want, name
+
+
+def test_small_sizes_all_offsets(cuda, checker):
+    rng = np.random.default_rng(9)
+    for n in list(range(0, 70)) + [127, 128, 129, 1023, 1024, 1025, 4095, 4096, 4097]:
+        b = rng.integers(0, 2 ** 64 - 1, size=n, dtype=np.uint64)
+        e = rng.integers(0, 2048, size=n, dtype=np.uint64)
+        b = (b & np.uint64(0x800FFFFFFFFFFFFF)) | (e << np.uint64(52))
+        x = b.view(np.float64)
+        want = bits_of(checker.exact_sum(x))
+        for off in (0, 1, 2, 3):
+            got, _ = dev_sum(to_dev(x, off))
+            assert got == want, (n, off)
+
+
+def test_carry_stress_slot_top(cuda, checker):
+    # 1e7 copies of the largest finite value: exercises the top slots and the
+    # carry slots above them (exact sum ~1.8e315 -> +Inf), then the same with a
+    # cancelling half, then max-mantissa terms in one slot beyond the budget.
+    big = np.full(10_000_000, 1.7976931348623157e308)
+    for x in (big, np.concatenate([big, -big[:-3]]),
+              np.full(3_000_000, float.fromhex("0x1.fffffffffffffp+1000"))):
+        got, part = dev_sum(to_dev(x))
+        ch, top, ib, nb = checker.canonical(x)
+        assert got == bits_of(checker.exact_sum(x))
+        assert list(part.acc.chunk) == list(ch)
+
+
+# ---------------------------------------------------- BASELINE configs
+
+@pytest.mark.parametrize("config", [1, 2, 3, 4])
+def test_configs_moderate(config, cuda, checker):
+    for n, seed in ((1000, 1), (65_537, 2), (1_000_003, 3)):
+        x = gen(config, n, seed)
+        h = x.cpu().numpy()
+        got, part = dev_sum(x)
+        ch, top, ib, nb = checker.canonical(h)
+        assert got == bits_of(checker.exact_sum(h)), (config, n)
+        assert list(part.acc.chunk) == list(ch), (config, n)
+
+
+def test_config1_small_superaccumulator(cuda, checker):
+    # BASELINE config 1: N = 1000 U[-1,1), the reference's small method
+    x = gen(1, 1000, 42)
+    h = x.cpu().numpy()
+    assert dev_sum(x)[0] == bits_of(checker.exact_sum(h, "small"))
+
+
+@pytest.mark.parametrize("config,n", [(2, 100_000_000), (3, 100_000_000), (4, 1_000_000_000)])
+def test_configs_full_size(config, n, cuda, checker):
+    x = gen(config, n, 1)
+    got, part = dev_sum(x)
+    h = x.cpu().numpy()
+    ch, top, ib, nb = checker.canonical(h)
+    assert list(part.acc.chunk) == list(ch)
+    assert got == bits_of(checker.exact_sum(h))
+    # properties at full size: order independence, negation symmetry
+    assert dev_sum(torch.flip(x, (0,)))[0] == got
+    neg = dev_sum(-x)[0]
+    assert neg == (got ^ (1 << 63) if got & ~(1 << 63) else 0)
+    del x, h
+
+
+def test_config4_shards_any_world_size(cuda):
+    n = 1_000_000_000
+    x = gen(4, n, 1)
+    want, _ = dev_sum(x)
+    from paper_1505_05571_b200.distributed import shard_bounds
+    for world in (2, 4, 8):
+        recs = []
+        for r in range(world):
+            b, e = shard_bounds(n, world, r)
+            recs.append(ops.exact_sum_tensor(x[b:e], base_index=b)[1])
+        res, _ = ops.merge_partials(torch.stack(recs))
+        assert bits_of(res.item()) == want, world
+
+
+def test_config5_segmented(cuda, checker):
+    for nseg, seed in ((4096, 3), (65_536, 1)):
+        offs = np.zeros(nseg + 1, dtype=np.uint64)
+        _lib.call("exsum_host_gen_offsets", seed, nseg, 1000, 100_000, offs.ctypes.data)
+        total = int(offs[-1])
+        x = torch.empty(total, dtype=torch.float64, device="cuda")
+        _lib.call("exsum_cuda_gen_segmented", seed, total, x.data_ptr(), stream())
+        out = ops.exact_sum_segmented(x, torch.from_numpy(offs.astype(np.int64)).cuda())
+        got = out.cpu().numpy().view(np.uint64)
+        want = checker.segmented_sum(x.cpu().numpy(), offs).view(np.uint64)
+        assert np.array_equal(got, want), int((got != want).sum())
+        kinds = (want >> np.uint64(52)) & np.uint64(0x7FF)
+        assert (kinds == 0x7FF).any() and (kinds != 0x7FF).any()  # both outcomes occur
+        del x
+
+
+def test_workspace_reuse_and_streams(cuda):
+    x = gen(3, 3_000_000, 5)
+    a = dev_sum(x)[0]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        b = dev_sum(x)[0]
+    torch.cuda.synchronize()
+    assert a == b == dev_sum(x)[0]
