@@ -53,7 +53,7 @@
 #define EXSUM_SLOT_BITS 96
 #endif
 #ifndef EXSUM_DECODE
-#define EXSUM_DECODE 0  // 0: decode on the ALU pipe, 1: on the FMA pipe (IMAD)
+#define EXSUM_DECODE 2  // 0: ALU-pipe decode, 1: FMA-pipe decode, 2: pipe-balanced
 #endif
 #ifndef EXSUM_PIPE
 #define EXSUM_PIPE 0  // 0 serial RMW, 1 store forwarding, 2 run merge (slot layout 96)
@@ -200,7 +200,7 @@ constexpr int kSlots = 66;       // slots 0..63 take terms (e' >> 5), 64..65 onl
 constexpr int kLPlane = kSlots * 32 * 4;
 constexpr int kHPlane = kSlots * 32 * 8;
 constexpr int kWarpSmem = kLPlane + kHPlane;  // 25,344 B
-constexpr int kDefaultVec = 8;
+constexpr int kDefaultVec = 10;
 
 // Slot k's low word is at sl + 128 k and its high word at 2 * (sl + 128 k) + hoff.
 struct Lane {
@@ -220,6 +220,42 @@ __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
 }
 
 // Same scheme as slot128 with a 96-bit window: m << (e' & 31) at slot e' >> 5.
+#if EXSUM_DECODE == 2
+// Pipe-balanced form (the B200 integer ALU pipe and the FMA pipe each retire 16
+// lanes/clk/SMSP; SHF/LOP3/IADD3/VIMNMX/ISETP go to the ALU, IMAD/VIADD to the
+// FMA pipe).  Per term: 11 ALU + 9 FMA + 4 LSU.  e (exponent field) and s (sign
+// mask) come precomputed from the batch decode.
+__device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
+  uint32_t s, ep, d, mhi, mh, m1, lx, mx, k, la, ha, u0, u1, u2;
+  asm("shr.s32 %0, %1, 31;" : "=r"(s) : "r"(hi));                         // ALU: sign mask
+  asm("max.u32 %0, %1, 1;" : "=r"(ep) : "r"(e));                         // ALU
+  asm("mad.lo.u32 %0, %1, -1, %2;" : "=r"(d) : "r"(e), "r"(ep));          // FMA: 1 iff e == 0
+  asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x100000u));  // ALU: (a&b)|c
+  asm("mad.lo.u32 %0, %1, -1048576, %2;" : "=r"(mh) : "r"(d), "r"(mhi));  // FMA: drop implicit 1
+  asm("mad.lo.u32 %0, %1, 2, 1;" : "=r"(m1) : "r"(s));                    // FMA: +-1
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(lx) : "r"(lo), "r"(m1), "r"(s));  // FMA: lo ^ s
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(mx) : "r"(mh), "r"(m1), "r"(s));  // FMA: mh ^ s
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(s), "r"(lx), "r"(ep));   // ALU
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lx), "r"(mx), "r"(ep));  // ALU
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mx), "r"(s), "r"(ep));   // ALU
+  asm("shr.u32 %0, %1, 5;" : "=r"(k) : "r"(ep));                          // ALU
+  asm("mad.lo.u32 %0, %1, 128, %2;" : "=r"(la) : "r"(k), "r"(a.sl));     // FMA
+  asm("mad.lo.u32 %0, %1, 2, %2;" : "=r"(ha) : "r"(la), "r"(a.hoff));     // FMA
+  asm volatile(
+      "{\n\t.reg .u32 l, h0, h1, cf;\n\t"
+      "ld.shared.u32 l, [%0];\n\t"
+      "ld.shared.v2.u32 {h0, h1}, [%1];\n\t"
+      "add.cc.u32 cf, %2, %2;\n\t"
+      "addc.cc.u32 l, l, %3;\n\t"
+      "addc.cc.u32 h0, h0, %4;\n\t"
+      "addc.u32 h1, h1, %5;\n\t"
+      "st.shared.u32 [%0], l;\n\t"
+      "st.shared.v2.u32 [%1], {h0, h1};\n\t}"
+      :
+      : "r"(la), "r"(ha), "r"(s), "r"(u0), "r"(u1), "r"(u2)
+      : "memory");
+}
+#else
 __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
 #if EXSUM_DECODE == 1
   // Decode on the FMA pipe (IMAD / IMAD.HI) to unload the integer ALU pipe:
@@ -259,6 +295,7 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
       : "r"(la), "r"(ha), "r"(s), "r"(u0), "r"(u1), "r"(u2)
       : "memory");
 }
+#endif
 
 // Carry upward: L_k in [0, 2^32), H_k = 0 for k < 65; slot 65 keeps the rest.
 __device__ __forceinline__ void normalize(const Lane &a) {
@@ -386,28 +423,35 @@ __device__ __forceinline__ void pipe_step(const Lane &a, Pipe &p, uint32_t lo, u
 #endif
 }
 
+// The warp's exact sum as 67 chunk values, straight from the (unnormalised)
+// slots: slot k = L_k + 2^32 H_k feeds chunk k (L_k), chunk k+1 (low word of H_k)
+// and chunk k+2 (signed high word of H_k); every addend is < 2^32 in magnitude,
+// so 32-lane sums stay below 2^38.  The high word of the carry-only slot 65
+// belongs to chunk 67 and is folded into chunk 66.  Reads are bank-skewed.
 __device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, const Lane &a, int lane,
                                             long long *row) {
-  normalize(a);
+  (void)a;
   __syncwarp();
   const uint32_t *Lp = reinterpret_cast<const uint32_t *>(warp_smem);
-  const unsigned long long *Hp = reinterpret_cast<const unsigned long long *>(warp_smem + kLPlane);
-  unsigned long long s0 = 0, s1 = 0, s2 = 0;
-  const int rowa = lane, rowb = lane + 32, rowc = lane + 64;
-#pragma unroll 8
-  for (int i = 0; i < 32; ++i) {
-    const int col = (i + lane) & 31;  // skewed: 32 distinct banks
-    s0 += Lp[rowa * 32 + col];
-    s1 += Lp[rowb * 32 + col];
-    if (rowc < kSlots) s2 += Lp[rowc * 32 + col];
-  }
-  long long h = static_cast<long long>(Hp[(kSlots - 1) * 32 + lane]);
+  const uint32_t *Hw = reinterpret_cast<const uint32_t *>(warp_smem + kLPlane);  // H as 2 words
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
-  row[lane] = static_cast<long long>(s0);
-  row[lane + 32] = static_cast<long long>(s1);
-  if (lane < 2) row[lane + 64] = static_cast<long long>(s2);
-  if (lane == 0) row[66] = h;
+  for (int r = 0; r < 3; ++r) {
+    const int c = 32 * r + lane;  // chunk index this lane sums
+    if (c >= kChunks) break;
+    long long acc = 0;
+#pragma unroll 8
+    for (int i = 0; i < 32; ++i) {
+      const int col = (i + lane) & 31;
+      if (c < kSlots) acc += Lp[c * 32 + col];
+      if (c >= 1) acc += Hw[2 * ((c - 1) * 32 + col)];  // low word of H_{c-1}
+      if (c >= 2 && c - 2 < kSlots - 1)
+        acc += static_cast<int32_t>(Hw[2 * ((c - 2) * 32 + col) + 1]);  // high word of H_{c-2}
+      if (c == kChunks - 1)
+        acc += static_cast<long long>(static_cast<int32_t>(Hw[2 * ((kSlots - 1) * 32 + col) + 1]))
+               << 32;  // high word of H_65 (chunk 67) folded into chunk 66
+    }
+    row[c] = acc;
+  }
 }
 
 }  // namespace slot96
@@ -435,6 +479,15 @@ constexpr int kNormEvery = 2016 / kBatchTerms;    // batches between renormalisa
 #define EXSUM_PREFETCH_BATCHES 1
 #endif
 constexpr int kPrefetchBatches = EXSUM_PREFETCH_BATCHES;  // L2 prefetch distance
+#ifndef EXSUM_CHECK_GROUP
+#define EXSUM_CHECK_GROUP 0  // vectors per Inf/NaN-check group (0: whole batch)
+#endif
+#ifndef EXSUM_PREFETCH_LANES
+#define EXSUM_PREFETCH_LANES 0
+#endif
+#ifndef EXSUM_BUFFERS
+#define EXSUM_BUFFERS 1  // register batch buffers (1: rely on the L2 prefetch)
+#endif
 constexpr int kScratch = kWarps * kChunks * 8;              // per-warp chunk rows
 constexpr int kSmem = kWarps * kWarpSmem + kScratch;
 static_assert(kSmem <= 227 * 1024, "shared memory budget");
@@ -526,6 +579,11 @@ __device__ __forceinline__ void load_batch(Batch &b, const double *X4, long long
 // 32-byte vectors starting at vector v0, clipped to vend.  Issued by one lane a
 // few batches ahead of the register loads; costs no registers, no shared memory.
 __device__ __forceinline__ void prefetch_l2(const double *X4, long long v0, long long vend) {
+#if EXSUM_PREFETCH_LANES
+  // per-lane variant: every lane prefetches the 256 B of its own vectors
+  (void)vend;
+  return;
+#endif
   if (v0 >= vend) return;
   long long nv = vend - v0;
   if (nv > kVecPerLane * 32) nv = kVecPerLane * 32;
@@ -536,10 +594,61 @@ __device__ __forceinline__ void prefetch_l2(const double *X4, long long v0, long
 
 // Process one batch (kBatchTerms terms per lane).  index_of_vec0 is the
 // special-value index of term 0 of the batch's first vector.
+#if EXSUM_CHECK_GROUP > 0 && EXSUM_EXPERIMENT == 0
+// Grouped form: the Inf/NaN test and the adds run per group of G vectors, so the
+// first group is processed while the batch's later loads are still in flight.
+__device__ __forceinline__ void process_batch(const Lane &a, Pipe &pp, Specials &sp, Batch &b,
+                                              int lane, unsigned long long index_of_vec0) {
+  constexpr int G = EXSUM_CHECK_GROUP;
+  static_assert(kVecPerLane % G == 0, "group must divide the batch");
+#pragma unroll
+  for (int g = 0; g < kVecPerLane; g += G) {
+    uint32_t e[G][4];
+    uint32_t emax = 0;
+#pragma unroll
+    for (int u = 0; u < G; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        e[u][q] = exponent_field(b.w[g + u][2 * q + 1]);
+        emax = max(emax, e[u][q]);
+      }
+    if (emax == 0x7FFu) {  // rare: record Inf/NaN and turn them into zero terms
+#pragma unroll
+      for (int u = 0; u < G; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (e[u][q] == 0x7FFu) {
+            record_special(sp, b.w[g + u][2 * q], b.w[g + u][2 * q + 1],
+                           index_of_vec0 + 4ull * static_cast<unsigned long long>((g + u) * 32 + lane) + q);
+            b.w[g + u][2 * q] = 0u;
+            b.w[g + u][2 * q + 1] = 0u;
+            e[u][q] = 0u;
+          }
+    }
+#pragma unroll
+    for (int u = 0; u < G; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        stream_term(a, pp, b.w[g + u][2 * q], b.w[g + u][2 * q + 1], e[u][q]);
+  }
+}
+#else
 __device__ __forceinline__ void process_batch(const Lane &a, Pipe &pp, Specials &sp, Batch &b,
                                               int lane, unsigned long long index_of_vec0) {
   uint32_t e[kVecPerLane][4];
   bool special = false;
+#if EXSUM_DECODE == 2
+  // exponent fields; "any Inf/NaN" = (max exponent == 2047), 3-input max chains
+  uint32_t emax = 0;
+#pragma unroll
+  for (int u = 0; u < kVecPerLane; ++u)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      e[u][q] = exponent_field(b.w[u][2 * q + 1]);
+      emax = max(emax, e[u][q]);
+    }
+  special = emax == 0x7FFu;
+#else
 #pragma unroll
   for (int u = 0; u < kVecPerLane; ++u)
 #pragma unroll
@@ -554,6 +663,7 @@ __device__ __forceinline__ void process_batch(const Lane &a, Pipe &pp, Specials 
 #endif
       special |= e[u][q] == 0x7FFu;
     }
+#endif
   if (special) {  // rare: record Inf/NaN and turn them into zero terms
 #pragma unroll
     for (int u = 0; u < kVecPerLane; ++u)
@@ -599,6 +709,7 @@ __device__ __forceinline__ void process_batch(const Lane &a, Pipe &pp, Specials 
   acc::add_term(a, r0 ^ r2, r1 ^ r3, 5u);
 #endif
 }
+#endif
 
 // Accumulate x[begin, end) into the calling warp's lane accumulators.
 // index_base is added to positions to form special-value indices; norm_count
@@ -628,6 +739,41 @@ __device__ void warp_accumulate(const double *__restrict__ x, unsigned long long
   }
   if (nvec <= 0) return;
   constexpr long long kStep = kVecPerLane * 32;
+#if EXSUM_BUFFERS == 1
+  // Single register buffer: the L2 bulk prefetch (kPrefetchBatches ahead) hides
+  // DRAM latency, the register load only waits for L2; frees 32-64 registers
+  // for instruction-level parallelism.
+  Batch b0;
+  const unsigned long long ib = index_base + vbeg_t;
+  if (lane == 0) {
+    for (int d = 0; d <= kPrefetchBatches; ++d) prefetch_l2(X4, d * kStep, nvec);
+  }
+  Pipe pp;
+  stream_begin(a, pp);
+  for (long long v = 0; v < nvec; v += kStep) {
+    load_batch(b0, X4, v, nvec, lane);
+#if EXSUM_PREFETCH_LANES
+    {
+      const long long pv = v + (kPrefetchBatches + 1) * kStep;
+#pragma unroll
+      for (int u = 0; u < kVecPerLane; u += 4) {
+        const long long q = pv + u * 32 + lane * 4;  // 4 consecutive vectors = 128 B
+        if (q < nvec) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(X4 + 4 * q));
+      }
+    }
+#else
+    if (lane == 0) prefetch_l2(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
+#endif
+    process_batch(a, pp, sp, b0, lane, ib + 4ull * static_cast<unsigned long long>(v));
+    if (++norm_count >= kNormEvery) {
+      stream_end(a, pp);
+      acc::normalize(a);
+      stream_begin(a, pp);
+      norm_count = 0;
+    }
+  }
+  stream_end(a, pp);
+#else
   Batch b0, b1;
   long long v = 0;
   if (kPrefetchBatches > 0 && lane == 0) {
@@ -664,6 +810,7 @@ __device__ void warp_accumulate(const double *__restrict__ x, unsigned long long
     if (v >= nvec) break;
   }
   stream_end(a, pp);
+#endif
 }
 
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
@@ -675,24 +822,163 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
   return v;
 }
 
-// Finalise a record: canonicalise, resolve specials, round, write outputs.
-__device__ void emit_record(int64_t *c, unsigned long long P, unsigned long long M,
-                            unsigned long long N, unsigned long long payload, double *result,
-                            exsum_partial *partial) {
-  const int top = exsum_canonicalize(c);
+// Warp-parallel finalisation (all 32 lanes of one warp): the same canonical form
+// and rounding as emit_record / exsum_core.h, without a 67-step serial chain.
+//   1. carry propagation by repeated shuffle passes until no lane holds a carry
+//      (two or three passes for accumulated chunk sums);
+//   2. canonical top / fold of a -1 top chunk via ballots;
+//   3. magnitude digits of a negative value by the two's-complement rule
+//      (zero below the lowest nonzero digit z, -d_z at z, ~d_i above);
+//   4. lane 0 rounds a 3-digit window at the leading digit with a sticky ballot.
+// row: 67 chunk values in shared memory (any representation with |c| < 2^62).
+__device__ void warp_emit(const long long *row, unsigned long long P, unsigned long long M,
+                          unsigned long long N, unsigned long long payload, double *result,
+                          exsum_partial *partial, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  long long v[3];
+  v[0] = row[lane];
+  v[1] = row[lane + 32];
+  v[2] = lane < 3 ? row[lane + 64] : 0;
+  // 1. carries: chunk i keeps its low 32 bits, passes the rest to i + 1; chunk 66 keeps all.
+  while (true) {
+    long long c[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) c[r] = (32 * r + lane < kChunks - 1) ? (v[r] >> 32) : 0;
+    if (!__any_sync(FULL, (c[0] | c[1] | c[2]) != 0)) break;
+    long long in[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const long long up = __shfl_up_sync(FULL, c[r], 1);
+      const long long wrap = r ? __shfl_sync(FULL, c[r - 1], 31) : 0;
+      in[r] = lane ? up : wrap;
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int idx = 32 * r + lane;
+      if (idx < kChunks - 1) v[r] &= 0xFFFFFFFFll;
+      if (idx < kChunks) v[r] += in[r];
+    }
+  }
+  const long long d66 = __shfl_sync(FULL, v[2], 2);
+  // 2. canonical top.
+  auto top_of = [&](unsigned b0, unsigned b1, unsigned b2) -> int {
+    if (b2) return 64 + 31 - __clz(static_cast<int>(b2));
+    if (b1) return 32 + 31 - __clz(static_cast<int>(b1));
+    if (b0) return 31 - __clz(static_cast<int>(b0));
+    return -1;
+  };
+  const bool neg = d66 < 0;
+  int top;
+  if (!neg) {
+    top = top_of(__ballot_sync(FULL, v[0] != 0), __ballot_sync(FULL, v[1] != 0),
+                 __ballot_sync(FULL, lane < 3 && v[2] != 0));
+  } else if (d66 <= -2) {
+    top = kChunks - 1;
+  } else {  // d66 == -1: fold into the highest digit below that is not all ones
+    const long long FF = 0xFFFFFFFFll;
+    top = top_of(__ballot_sync(FULL, v[0] != FF), __ballot_sync(FULL, v[1] != FF),
+                 __ballot_sync(FULL, lane < 2 && v[2] != FF));
+    if (top < 0) top = 0;
+  }
+  // canonical chunks: digits below top, the (signed) top, zeros above
+  long long ch[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int idx = 32 * r + lane;
+    ch[r] = idx < top ? v[r] : idx > top ? 0 : (neg && top < kChunks - 1 ? v[r] - (1ll << 32) : v[r]);
+  }
+  // 3. magnitude digits m_i (index 0..67; 67 only for the -2^32 top borrow)
+  unsigned m[3];
+  int h = -1;
+  unsigned long long sticky_mask_lo[3];
+  if (top >= 0) {
+    unsigned z = 0;  // lowest index with a nonzero low word D_i (neg only); top+1 if none
+    if (neg) {
+      const unsigned n0 = __ballot_sync(FULL, static_cast<unsigned>(ch[0]) != 0u),
+                     n1 = __ballot_sync(FULL, static_cast<unsigned>(ch[1]) != 0u),
+                     n2 = __ballot_sync(FULL, lane < 3 && static_cast<unsigned>(ch[2]) != 0u);
+      z = n0 ? __ffs(n0) - 1 : n1 ? 32 + __ffs(n1) - 1 : n2 ? 64 + __ffs(n2) - 1 : top + 1;
+      if (z > static_cast<unsigned>(top)) z = top + 1;
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int idx = 32 * r + lane;
+      const unsigned dlo = static_cast<unsigned>(ch[r]);
+      if (!neg) {
+        m[r] = idx <= top ? dlo : 0u;
+      } else if (idx > top + 1 || idx < static_cast<int>(z)) {
+        m[r] = 0u;
+      } else if (idx == top + 1) {
+        m[r] = (z > static_cast<unsigned>(top)) ? 1u : 0u;  // only for an all-zero tail below -2^32
+      } else if (idx == static_cast<int>(z)) {
+        m[r] = 0u - dlo;
+      } else {
+        m[r] = ~dlo;
+      }
+    }
+    const unsigned b0 = __ballot_sync(FULL, m[0] != 0), b1 = __ballot_sync(FULL, m[1] != 0),
+                   b2 = __ballot_sync(FULL, lane < 4 && m[2] != 0);
+    h = top_of(b0, b1, b2);
+    sticky_mask_lo[0] = b0;
+    sticky_mask_lo[1] = b1;
+    sticky_mask_lo[2] = b2;
+  }
+  // gather the 3-digit window m[h-2..h] to lane 0
+  auto digit = [&](int i) -> unsigned {  // collective: all lanes call with the same i
+    const int r = i >= 0 ? i >> 5 : 0;
+    const unsigned val = r == 0 ? m[0] : r == 1 ? m[1] : m[2];
+    const unsigned got = __shfl_sync(FULL, val, i >= 0 ? (i & 31) : 0);
+    return i >= 0 ? got : 0u;
+  };
+  unsigned w0 = 0, w1 = 0, w2 = 0;
+  bool sticky = false;
+  if (h >= 0) {
+    w2 = digit(h);
+    w1 = digit(h - 1);
+    w0 = digit(h - 2);
+    // any nonzero magnitude digit strictly below h - 2
+    const int lim = h - 2;
+    if (lim > 0) {
+      const unsigned long long all_lo =
+          sticky_mask_lo[0] | (sticky_mask_lo[1] << 32);  // digits 0..63
+      const unsigned long long below =
+          lim >= 64 ? all_lo : (all_lo & ((1ull << lim) - 1ull));
+      sticky = below != 0ull || (lim > 64 && (sticky_mask_lo[2] & ((1u << (lim - 64)) - 1u)));
+    }
+  }
   uint64_t ib, nb;
   exsum_resolve_specials(P, M, N, payload, &ib, &nb);
-  if (result) *result = __longlong_as_double(static_cast<long long>(exsum_result_bits(ib, nb, c, top)));
+  if (lane == 0 && result) {
+    uint64_t bits;
+    if (nb) {
+      bits = nb;
+    } else if (ib) {
+      bits = ib;
+    } else if (top < 0) {
+      bits = 0;
+    } else {
+      const uint32_t win[3] = {w0, w1, w2};
+      const int base = h - 2;  // digit index of win[0] (may be negative: then win[0..] padded)
+      bits = exsum_round_digits(win, 3, neg, -1075 + 32 * base, sticky);
+    }
+    *result = __longlong_as_double(static_cast<long long>(bits));
+  }
   if (partial) {
-    for (int i = 0; i < kChunks; ++i) partial->acc.chunk[i] = c[i];
-    partial->acc.inf_bits = ib;
-    partial->acc.nan_bits = nb;
-    partial->acc.adds_until_propagate = kCarryTerms;
-    partial->acc.reserved_ = 0;
-    partial->first_pos_inf = P;
-    partial->first_neg_inf = M;
-    partial->first_nan = N;
-    partial->nan_payload = payload;
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int idx = 32 * r + lane;
+      if (idx < kChunks) partial->acc.chunk[idx] = ch[r];
+    }
+    if (lane == 0) {
+      partial->acc.inf_bits = ib;
+      partial->acc.nan_bits = nb;
+      partial->acc.adds_until_propagate = kCarryTerms;
+      partial->acc.reserved_ = 0;
+      partial->first_pos_inf = P;
+      partial->first_neg_inf = M;
+      partial->first_nan = N;
+      partial->nan_payload = payload;
+    }
   }
 }
 
@@ -709,18 +995,23 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
   const int warp = threadIdx.x >> 5;
   unsigned char *wsm = smem + warp * kWarpSmem;
   long long *scratch = reinterpret_cast<long long *>(smem + kWarps * kWarpSmem);
-  zero_warp(wsm, lane);
-  __syncwarp();
-  const Lane a = acc::lane_view(wsm, lane);
-  Specials sp{~0ull, ~0ull, ~0ull};
-  int norm_count = 0;
-
   // K1: contiguous per-warp ranges, boundaries on 4-term multiples.
   const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * kWarps + warp;
   const unsigned long long nw = static_cast<unsigned long long>(gridDim.x) * kWarps;
   const unsigned long long quads = (n + 3) >> 2;
   const unsigned long long qb = quads * gw / nw, qe = quads * (gw + 1) / nw;
   const unsigned long long tb = qb * 4, te = min(qe * 4, n);
+  if (lane == 0 && te > tb) {  // start the first batches' DRAM reads before zeroing smem
+    const uintptr_t p0 = reinterpret_cast<uintptr_t>(x + tb) & ~uintptr_t{15};
+    const uintptr_t p1 = reinterpret_cast<uintptr_t>(x + min(te, tb + 2ull * kBatchTerms * 32));
+    const uint32_t bytes = static_cast<uint32_t>((p1 - p0 + 15) & ~uintptr_t{15});
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"(bytes) : "memory");
+  }
+  zero_warp(wsm, lane);
+  __syncwarp();
+  const Lane a = acc::lane_view(wsm, lane);
+  Specials sp{~0ull, ~0ull, ~0ull};
+  int norm_count = 0;
   warp_accumulate(x, tb, te, base_index, a, sp, norm_count, lane);
 
   // K2: the warp's 67 chunk sums.
@@ -757,18 +1048,16 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
     if (finalize) const_cast<unsigned long long *>(src)[j] = 0;
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
+  if (warp != 0) return;
   const unsigned long long Nf = ~s_spec[2];
   unsigned long long payload = s_spec[3];
   if (Nf != ~0ull && Nf >= base_index && Nf - base_index < n) {
     payload = __ldcg(reinterpret_cast<const unsigned long long *>(x) + (Nf - base_index));
-    if (!finalize) ws->nan_payload = payload;  // the first NaN so far lies in this launch
+    if (!finalize && lane == 0) ws->nan_payload = payload;  // first NaN so far is in this launch
   }
-  ws->done = 0;
+  if (lane == 0) ws->done = 0;
   if (!finalize) return;
-  int64_t c[kChunks];
-  for (int i = 0; i < kChunks; ++i) c[i] = scratch[i];
-  emit_record(c, ~s_spec[0], ~s_spec[1], Nf, payload, result, partial);
+  warp_emit(scratch, ~s_spec[0], ~s_spec[1], Nf, payload, result, partial, lane);
 }
 
 // Finalise a workspace filled by exsum_cuda_accumulate launches.
@@ -779,15 +1068,16 @@ __global__ void exsum_finalize_kernel(Workspace *ws, double *result, exsum_parti
     ws->chunk[threadIdx.x] = 0;
   }
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  int64_t c[kChunks];
-  for (int i = 0; i < kChunks; ++i) c[i] = sc[i];
+  if (threadIdx.x >= 32) return;
   const unsigned long long P = ~ws->inv_pinf, M = ~ws->inv_ninf, N = ~ws->inv_nan;
   const unsigned long long payload = ws->nan_payload;
-  ws->inv_pinf = ws->inv_ninf = ws->inv_nan = 0;
-  ws->nan_payload = 0;
-  ws->done = 0;
-  emit_record(c, P, M, N, payload, result, partial);
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    ws->inv_pinf = ws->inv_ninf = ws->inv_nan = 0;
+    ws->nan_payload = 0;
+    ws->done = 0;
+  }
+  warp_emit(sc, P, M, N, payload, result, partial, threadIdx.x);
 }
 
 // ------------------------------------------------------------------------- K4
@@ -818,13 +1108,9 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
     const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                              N = warp_min_u64(sp.N);
     __syncwarp();
-    if (lane == 0) {
-      int64_t c[kChunks];
-      for (int i = 0; i < kChunks; ++i) c[i] = row[i];
-      const unsigned long long payload =
-          N != ~0ull ? __ldg(reinterpret_cast<const unsigned long long *>(x) + b + N) : 0ull;
-      emit_record(c, P, M, N, payload, out + s, partials ? partials + s : nullptr);
-    }
+    const unsigned long long payload =
+        N != ~0ull ? __ldg(reinterpret_cast<const unsigned long long *>(x) + b + N) : 0ull;
+    warp_emit(row, P, M, N, payload, out + s, partials ? partials + s : nullptr, lane);
     __syncwarp();
   }
   // Last warp out resets the claim counters for the next launch.
@@ -865,11 +1151,7 @@ __global__ void exsum_merge_kernel(const exsum_partial *parts, unsigned long lon
     sPay = pay;
   }
   __syncthreads();
-  if (t == 0) {
-    int64_t c[kChunks];
-    for (int i = 0; i < kChunks; ++i) c[i] = sc[i];
-    emit_record(c, sP, sM, sN, sPay, result, out);
-  }
+  if (t < 32) warp_emit(sc, sP, sM, sN, sPay, result, out, t);
 }
 
 }  // namespace dev
