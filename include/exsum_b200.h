@@ -133,6 +133,16 @@ int exsum_cuda_workspace_init(void *d_ws, size_t ws_bytes, void *stream);
 int exsum_cuda_sum(const double *d_x, size_t n, uint64_t base_index, double *d_result,
                    exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream);
 
+/* exsum_cuda_sum with launch flags.  EXSUM_SUM_OVERLAP: programmatic dependent
+ * launch — the grid may start while the previous kernel in `stream` is still
+ * finishing (it waits for that kernel before touching d_ws).  Only valid when
+ * d_x is not written by the immediately preceding kernel of the stream (e.g.
+ * back-to-back sums over resident data). */
+#define EXSUM_SUM_OVERLAP 1u
+int exsum_cuda_sum_ex(const double *d_x, size_t n, uint64_t base_index, double *d_result,
+                      exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
+                      unsigned flags);
+
 /* Incremental form (LargeAccumulator::add(span) across calls, large_accumulator.hpp:61):
  * accumulate d_x into the workspace without rounding; then finalize. */
 int exsum_cuda_accumulate(const double *d_x, size_t n, uint64_t base_index, void *d_ws,

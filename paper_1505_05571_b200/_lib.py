@@ -87,6 +87,7 @@ _SIGNATURES = {
     "exsum_cuda_workspace_bytes": (_sz, []),
     "exsum_cuda_workspace_init": (_i32, [_vp, _sz, _vp]),
     "exsum_cuda_sum": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "exsum_cuda_sum_ex": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _sz, _vp, C.c_uint]),
     "exsum_cuda_accumulate": (_i32, [_vp, _sz, _u64, _vp, _sz, _vp]),
     "exsum_cuda_finalize": (_i32, [_vp, _vp, _vp, _sz, _vp]),
     "exsum_cuda_sum_segmented": (_i32, [_vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp]),

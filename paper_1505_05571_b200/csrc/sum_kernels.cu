@@ -55,8 +55,14 @@
 #ifndef EXSUM_DECODE
 #define EXSUM_DECODE 2  // 0: ALU-pipe decode, 1: FMA-pipe decode, 2: pipe-balanced
 #endif
+#ifndef EXSUM_HSPLIT
+#define EXSUM_HSPLIT 0  // slot96: high word as two 32-bit planes (all accesses 32-bit)
+#endif
 #ifndef EXSUM_PIPE
 #define EXSUM_PIPE 0  // 0 serial RMW, 1 store forwarding, 2 run merge (slot layout 96)
+#endif
+#if EXSUM_HSPLIT && (EXSUM_DECODE != 2 || EXSUM_PIPE != 0 || EXSUM_SLOT_BITS != 96)
+#error "EXSUM_HSPLIT needs EXSUM_DECODE=2, EXSUM_PIPE=0, EXSUM_SLOT_BITS=96"
 #endif
 
 namespace exsum_b200 {
@@ -200,7 +206,7 @@ constexpr int kSlots = 66;       // slots 0..63 take terms (e' >> 5), 64..65 onl
 constexpr int kLPlane = kSlots * 32 * 4;
 constexpr int kHPlane = kSlots * 32 * 8;
 constexpr int kWarpSmem = kLPlane + kHPlane;  // 25,344 B
-constexpr int kDefaultVec = 10;
+constexpr int kDefaultVec = 6;
 
 // Slot k's low word is at sl + 128 k and its high word at 2 * (sl + 128 k) + hoff.
 struct Lane {
@@ -240,6 +246,27 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mx), "r"(s), "r"(ep));   // ALU
   asm("shr.u32 %0, %1, 5;" : "=r"(k) : "r"(ep));                          // ALU
   asm("mad.lo.u32 %0, %1, 128, %2;" : "=r"(la) : "r"(k), "r"(a.sl));     // FMA
+#if EXSUM_HSPLIT
+  // three 32-bit planes: every access is a conflict-free 32-bit LDS/STS at
+  // la + {0, kPlane, 2 kPlane} (immediate offsets, no second address)
+  (void)ha;
+  asm volatile(
+      "{\n\t.reg .u32 l, h0, h1, cf;\n\t"
+      "ld.shared.u32 l, [%0];\n\t"
+      "ld.shared.u32 h0, [%0+8448];\n\t"
+      "ld.shared.u32 h1, [%0+16896];\n\t"
+      "add.cc.u32 cf, %1, %1;\n\t"
+      "addc.cc.u32 l, l, %2;\n\t"
+      "addc.cc.u32 h0, h0, %3;\n\t"
+      "addc.u32 h1, h1, %4;\n\t"
+      "st.shared.u32 [%0], l;\n\t"
+      "st.shared.u32 [%0+8448], h0;\n\t"
+      "st.shared.u32 [%0+16896], h1;\n\t}"
+      :
+      : "r"(la), "r"(s), "r"(u0), "r"(u1), "r"(u2)
+      : "memory");
+  return;
+#endif
   asm("mad.lo.u32 %0, %1, 2, %2;" : "=r"(ha) : "r"(la), "r"(a.hoff));     // FMA
   asm volatile(
       "{\n\t.reg .u32 l, h0, h1, cf;\n\t"
@@ -298,6 +325,28 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
 #endif
 
 // Carry upward: L_k in [0, 2^32), H_k = 0 for k < 65; slot 65 keeps the rest.
+#if EXSUM_HSPLIT
+__device__ __forceinline__ void normalize(const Lane &a) {
+  uint32_t *H0 = a.L + kSlots * 32, *H1 = a.L + 2 * kSlots * 32;
+  long long c = 0;
+#pragma unroll 6
+  for (int k = 0; k < kSlots - 1; ++k) {
+    const long long u = static_cast<long long>(a.L[32 * k]) + c;
+    const long long h = static_cast<long long>((static_cast<unsigned long long>(H1[32 * k]) << 32) | H0[32 * k]);
+    a.L[32 * k] = static_cast<uint32_t>(u);
+    H0[32 * k] = 0u;
+    H1[32 * k] = 0u;
+    c = h + (u >> 32);
+  }
+  const int k = kSlots - 1;
+  const long long u = static_cast<long long>(a.L[32 * k]) + c;
+  const long long h = static_cast<long long>((static_cast<unsigned long long>(H1[32 * k]) << 32) | H0[32 * k]);
+  const unsigned long long nh = static_cast<unsigned long long>(h + (u >> 32));
+  a.L[32 * k] = static_cast<uint32_t>(u);
+  H0[32 * k] = static_cast<uint32_t>(nh);
+  H1[32 * k] = static_cast<uint32_t>(nh >> 32);
+}
+#else
 __device__ __forceinline__ void normalize(const Lane &a) {
   long long c = 0;
 #pragma unroll 6
@@ -313,6 +362,7 @@ __device__ __forceinline__ void normalize(const Lane &a) {
   a.L[32 * k] = static_cast<uint32_t>(u);
   a.H[32 * k] = static_cast<unsigned long long>(static_cast<long long>(a.H[32 * k]) + (u >> 32));
 }
+#endif
 
 // ---- pipelined term streams (EXSUM_PIPE) ------------------------------------
 //
@@ -433,7 +483,15 @@ __device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, const Lane
   (void)a;
   __syncwarp();
   const uint32_t *Lp = reinterpret_cast<const uint32_t *>(warp_smem);
+#if EXSUM_HSPLIT
+  const uint32_t *H0 = Lp + kSlots * 32, *H1 = Lp + 2 * kSlots * 32;
+#define EXSUM_HLO(k, col) H0[(k) * 32 + (col)]
+#define EXSUM_HHI(k, col) H1[(k) * 32 + (col)]
+#else
   const uint32_t *Hw = reinterpret_cast<const uint32_t *>(warp_smem + kLPlane);  // H as 2 words
+#define EXSUM_HLO(k, col) Hw[2 * ((k) * 32 + (col))]
+#define EXSUM_HHI(k, col) Hw[2 * ((k) * 32 + (col)) + 1]
+#endif
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     const int c = 32 * r + lane;  // chunk index this lane sums
@@ -443,13 +501,15 @@ __device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, const Lane
     for (int i = 0; i < 32; ++i) {
       const int col = (i + lane) & 31;
       if (c < kSlots) acc += Lp[c * 32 + col];
-      if (c >= 1) acc += Hw[2 * ((c - 1) * 32 + col)];  // low word of H_{c-1}
+      if (c >= 1) acc += EXSUM_HLO(c - 1, col);  // low word of H_{c-1}
       if (c >= 2 && c - 2 < kSlots - 1)
-        acc += static_cast<int32_t>(Hw[2 * ((c - 2) * 32 + col) + 1]);  // high word of H_{c-2}
+        acc += static_cast<int32_t>(EXSUM_HHI(c - 2, col));  // high word of H_{c-2}
       if (c == kChunks - 1)
-        acc += static_cast<long long>(static_cast<int32_t>(Hw[2 * ((kSlots - 1) * 32 + col) + 1]))
+        acc += static_cast<long long>(static_cast<int32_t>(EXSUM_HHI(kSlots - 1, col)))
                << 32;  // high word of H_65 (chunk 67) folded into chunk 66
     }
+#undef EXSUM_HLO
+#undef EXSUM_HHI
     row[c] = acc;
   }
 }
@@ -479,6 +539,9 @@ constexpr int kNormEvery = 2016 / kBatchTerms;    // batches between renormalisa
 #define EXSUM_PREFETCH_BATCHES 1
 #endif
 constexpr int kPrefetchBatches = EXSUM_PREFETCH_BATCHES;  // L2 prefetch distance
+#ifndef EXSUM_ROLL
+#define EXSUM_ROLL 1  // rolling single-buffer loads with batch-end Inf/NaN fix-up
+#endif
 #ifndef EXSUM_CHECK_GROUP
 #define EXSUM_CHECK_GROUP 0  // vectors per Inf/NaN-check group (0: whole batch)
 #endif
@@ -739,7 +802,64 @@ __device__ void warp_accumulate(const double *__restrict__ x, unsigned long long
   }
   if (nvec <= 0) return;
   constexpr long long kStep = kVecPerLane * 32;
-#if EXSUM_BUFFERS == 1
+#if EXSUM_ROLL
+  // Rolling single buffer: after a vector's four terms are added, its registers
+  // are immediately refilled with the same vector of the next batch, so every
+  // load is in flight for almost a whole batch without a second register set.
+  // Inf/NaN: terms are added unconditionally; if the batch's maximum exponent
+  // field is 2047 the batch is re-read and each Inf/NaN term is recorded and
+  // its (garbage) contribution cancelled by adding its sign-flipped twin — exact
+  // in the modular slot arithmetic, and before any renormalisation.
+  Batch b0;
+  const unsigned long long ib = index_base + vbeg_t;
+  if (lane == 0) {
+    for (int d = 0; d <= kPrefetchBatches; ++d) prefetch_l2(X4, d * kStep, nvec);
+  }
+  load_batch(b0, X4, 0, nvec, lane);
+  for (long long v = 0; v < nvec; v += kStep) {
+    const long long nv = v + kStep;
+    const bool full_next = nv + kStep <= nvec;
+    if (lane == 0) prefetch_l2(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
+    uint32_t emax = 0;
+#pragma unroll
+    for (int u = 0; u < kVecPerLane; ++u) {
+      uint32_t e[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        e[q] = exponent_field(b0.w[u][2 * q + 1]);
+        emax = max(emax, e[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc::add_term(a, b0.w[u][2 * q], b0.w[u][2 * q + 1], e[q]);
+      const long long vv = nv + u * 32 + lane;
+      if (full_next || vv < nvec) {
+        ldg256(X4 + 4 * vv, b0.w[u]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) b0.w[u][q] = 0u;
+      }
+    }
+    if (__builtin_expect(emax == 0x7FFu, 0)) {
+      const unsigned long long *xb = reinterpret_cast<const unsigned long long *>(X4);
+      for (int u = 0; u < kVecPerLane; ++u) {
+        const long long vec = v + u * 32 + lane;
+        if (vec >= nvec) break;
+        for (int q = 0; q < 4; ++q) {
+          const unsigned long long bits = __ldcg(xb + 4 * vec + q);
+          const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
+          if (exponent_field(hi) == 0x7FFu) {
+            record_special(sp, lo, hi, ib + 4ull * static_cast<unsigned long long>(vec) + q);
+            acc::add_term(a, lo, hi ^ 0x80000000u, 0x7FFu);  // cancel the garbage add
+          }
+        }
+      }
+    }
+    if (++norm_count >= kNormEvery) {
+      acc::normalize(a);
+      norm_count = 0;
+    }
+  }
+#elif EXSUM_BUFFERS == 1
   // Single register buffer: the L2 bulk prefetch (kPrefetchBatches ahead) hides
   // DRAM latency, the register load only waits for L2; frees 32-64 registers
   // for instruction-level parallelism.
@@ -995,6 +1115,9 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
   const int warp = threadIdx.x >> 5;
   unsigned char *wsm = smem + warp * kWarpSmem;
   long long *scratch = reinterpret_cast<long long *>(smem + kWarps * kWarpSmem);
+  // Programmatic dependent launch: let the next sum in the stream start its CTAs
+  // on SMs this grid releases (no-op unless launched with EXSUM_SUM_OVERLAP).
+  asm volatile("griddepcontrol.launch_dependents;");
   // K1: contiguous per-warp ranges, boundaries on 4-term multiples.
   const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * kWarps + warp;
   const unsigned long long nw = static_cast<unsigned long long>(gridDim.x) * kWarps;
@@ -1018,6 +1141,9 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
   acc::warp_chunks(wsm, a, lane, scratch + warp * kChunks);
   const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                            N = warp_min_u64(sp.N);
+  // The workspace is shared with the previous sum in the stream: wait for that
+  // grid (complete, memory flushed) before the first workspace access.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (lane == 0) {
     if (P != ~0ull) atomicMax(&ws->inv_pinf, ~P);
     if (M != ~0ull) atomicMax(&ws->inv_ninf, ~M);
@@ -1201,13 +1327,29 @@ unsigned grid_for(unsigned long long n, int sms) {
 }
 
 int sum_launch(const double *d_x, size_t n, uint64_t base_index, void *d_ws, size_t ws_bytes,
-               void *stream, int finalize, double *d_result, exsum_partial *d_partial) {
+               void *stream, int finalize, double *d_result, exsum_partial *d_partial,
+               unsigned flags = 0) {
   if (!d_ws || ws_bytes < sizeof(Workspace) || (n && !d_x)) return EXSUM_EINVAL;
   int sms = 0;
   const int st = prepare_device(&sms);
   if (st) return st;
-  exsum_sum_kernel<<<grid_for(n, sms), kThreads, kSmem, static_cast<cudaStream_t>(stream)>>>(
-      d_x, n, base_index, static_cast<Workspace *>(d_ws), finalize, d_result, d_partial);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid_for(n, sms));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cudaLaunchAttribute attr[1];
+  if (flags & EXSUM_SUM_OVERLAP) {
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
+  if (cudaLaunchKernelEx(&cfg, exsum_sum_kernel, d_x, static_cast<unsigned long long>(n),
+                         static_cast<unsigned long long>(base_index),
+                         static_cast<Workspace *>(d_ws), finalize, d_result, d_partial) !=
+      cudaSuccess)
+    return EXSUM_ECUDA;
   return launch_status();
 }
 
@@ -1228,6 +1370,12 @@ int exsum_cuda_workspace_init(void *d_ws, size_t ws_bytes, void *stream) {
 int exsum_cuda_sum(const double *d_x, size_t n, uint64_t base_index, double *d_result,
                    exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream) {
   return sum_launch(d_x, n, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial);
+}
+
+int exsum_cuda_sum_ex(const double *d_x, size_t n, uint64_t base_index, double *d_result,
+                      exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
+                      unsigned flags) {
+  return sum_launch(d_x, n, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial, flags);
 }
 
 int exsum_cuda_accumulate(const double *d_x, size_t n, uint64_t base_index, void *d_ws,

@@ -82,13 +82,16 @@ def _device_tensor(x: torch.Tensor) -> torch.Tensor:
 
 
 def exact_sum_tensor(x: torch.Tensor, *, base_index: int = 0, result: torch.Tensor | None = None,
-                     partial: torch.Tensor | None = None,
-                     workspace: Workspace | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+                     partial: torch.Tensor | None = None, workspace: Workspace | None = None,
+                     overlap: bool = False) -> tuple[torch.Tensor, torch.Tensor]:
     """Asynchronous exact sum of a CUDA float64 tensor on the current stream.
 
     Returns (result, partial): a 1-element float64 tensor with the correctly
     rounded sum and a 592-byte uint8 tensor holding the exsum_partial record
     (canonical chunks + Inf/NaN indices, offset by ``base_index``).
+    ``overlap=True`` launches with programmatic dependent launch (EXSUM_SUM_OVERLAP):
+    back-to-back sums over resident data overlap one sum's epilogue with the
+    next one's streaming; ``x`` must not be written by the preceding kernel.
     """
     if not x.is_cuda:
         raise ValueError("exact_sum_tensor needs a CUDA tensor")
@@ -99,8 +102,9 @@ def exact_sum_tensor(x: torch.Tensor, *, base_index: int = 0, result: torch.Tens
         result = torch.empty(1, dtype=torch.float64, device=dev)
     if partial is None:
         partial = torch.empty(PARTIAL_BYTES, dtype=torch.uint8, device=dev)
-    _lib.call("exsum_cuda_sum", x.data_ptr(), x.numel(), base_index, result.data_ptr(),
-              partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev))
+    _lib.call("exsum_cuda_sum_ex", x.data_ptr(), x.numel(), base_index, result.data_ptr(),
+              partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev),
+              1 if overlap else 0)
     return result, partial
 
 

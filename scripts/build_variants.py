@@ -5,16 +5,16 @@ from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1505_05571_b200.build import build_variant  # noqa: E402
 
-B = ("EXSUM_BUFFERS=1", "EXSUM_DECODE=2")
+R = ("EXSUM_ROLL=1",)
 VARIANTS = {
-    "v10_p1": B + ("EXSUM_VEC_PER_LANE=10", "EXSUM_PREFETCH_BATCHES=1"),
-    "v12_p1": B + ("EXSUM_VEC_PER_LANE=12", "EXSUM_PREFETCH_BATCHES=1"),
-    "v16_p1": B + ("EXSUM_VEC_PER_LANE=16", "EXSUM_PREFETCH_BATCHES=1"),
-    "v12_p0": B + ("EXSUM_VEC_PER_LANE=12", "EXSUM_PREFETCH_BATCHES=0"),
-    "v12_p1_g2": B + ("EXSUM_VEC_PER_LANE=12", "EXSUM_PREFETCH_BATCHES=1", "EXSUM_CHECK_GROUP=2"),
-    "v12_p1_g4": B + ("EXSUM_VEC_PER_LANE=12", "EXSUM_PREFETCH_BATCHES=1", "EXSUM_CHECK_GROUP=4"),
-    "v16_p1_g4": B + ("EXSUM_VEC_PER_LANE=16", "EXSUM_PREFETCH_BATCHES=1", "EXSUM_CHECK_GROUP=4"),
-    "v10_p1_g2": B + ("EXSUM_VEC_PER_LANE=10", "EXSUM_PREFETCH_BATCHES=1", "EXSUM_CHECK_GROUP=2"),
+    "roll_v6": R + ("EXSUM_VEC_PER_LANE=6",),
+    "roll_v5": R + ("EXSUM_VEC_PER_LANE=5",),
+    "roll_v4": R + ("EXSUM_VEC_PER_LANE=4",),
+    "roll_v3": R + ("EXSUM_VEC_PER_LANE=3",),
+    "roll_v4_p2": R + ("EXSUM_VEC_PER_LANE=4", "EXSUM_PREFETCH_BATCHES=2"),
+    "roll_v4_p3": R + ("EXSUM_VEC_PER_LANE=4", "EXSUM_PREFETCH_BATCHES=3"),
+    "roll_v6_p2": R + ("EXSUM_VEC_PER_LANE=6", "EXSUM_PREFETCH_BATCHES=2"),
+    "roll_v2_p4": R + ("EXSUM_VEC_PER_LANE=2", "EXSUM_PREFETCH_BATCHES=4"),
 }
 names = sys.argv[1:] or list(VARIANTS)
 verbose = "-v" in names
