@@ -72,7 +72,7 @@ class ClockSampler:
     }
 
     def __init__(self, index: int):
-        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.samples, self.reasons, self.max_mhz, self.power = [], set(), None, []
         self._stop = threading.Event()
         try:
             import pynvml
@@ -88,6 +88,7 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 self.reasons |= {n for b, n in self.REASONS.items() if mask & b}
             except Exception:  # noqa: BLE001
@@ -108,7 +109,8 @@ class ClockSampler:
         if not self.nv or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
         return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+                "reasons": sorted(self.reasons), "samples": len(self.samples),
+                "power_w_median": statistics.median(self.power) if self.power else None}
 
 
 # --------------------------------------------------------------- CPU legs

@@ -206,7 +206,7 @@ constexpr int kSlots = 66;       // slots 0..63 take terms (e' >> 5), 64..65 onl
 constexpr int kLPlane = kSlots * 32 * 4;
 constexpr int kHPlane = kSlots * 32 * 8;
 constexpr int kWarpSmem = kLPlane + kHPlane;  // 25,344 B
-constexpr int kDefaultVec = 6;
+constexpr int kDefaultVec = 8;
 
 // Slot k's low word is at sl + 128 k and its high word at 2 * (sl + 128 k) + hoff.
 struct Lane {
@@ -214,6 +214,8 @@ struct Lane {
   unsigned long long *H;  // &Hplane[0][lane]; slot k at H[32 k]
   uint32_t sl;
   uint32_t hoff;
+  uint32_t two;   // 2 and 128, opaque to ptxas: keeps the address arithmetic
+  uint32_t c128;  // IMADs on the FMA pipe instead of LEAs on the ALU pipe
 };
 
 __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
@@ -222,6 +224,8 @@ __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
   v.H = reinterpret_cast<unsigned long long *>(warp_smem + kLPlane) + lane;
   v.sl = static_cast<uint32_t>(__cvta_generic_to_shared(v.L));
   v.hoff = static_cast<uint32_t>(__cvta_generic_to_shared(v.H)) - 2u * v.sl;
+  v.two = (blockDim.x >> 30) + 2u;
+  v.c128 = v.two * 64u;
   return v;
 }
 
@@ -245,7 +249,7 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lx), "r"(mx), "r"(ep));  // ALU
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mx), "r"(s), "r"(ep));   // ALU
   asm("shr.u32 %0, %1, 5;" : "=r"(k) : "r"(ep));                          // ALU
-  asm("mad.lo.u32 %0, %1, 128, %2;" : "=r"(la) : "r"(k), "r"(a.sl));     // FMA
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(k), "r"(a.c128), "r"(a.sl));  // FMA
 #if EXSUM_HSPLIT
   // three 32-bit planes: every access is a conflict-free 32-bit LDS/STS at
   // la + {0, kPlane, 2 kPlane} (immediate offsets, no second address)
@@ -267,7 +271,7 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
       : "memory");
   return;
 #endif
-  asm("mad.lo.u32 %0, %1, 2, %2;" : "=r"(ha) : "r"(la), "r"(a.hoff));     // FMA
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));  // FMA
   asm volatile(
       "{\n\t.reg .u32 l, h0, h1, cf;\n\t"
       "ld.shared.u32 l, [%0];\n\t"
@@ -818,25 +822,42 @@ __device__ void warp_accumulate(const double *__restrict__ x, unsigned long long
   load_batch(b0, X4, 0, nvec, lane);
   for (long long v = 0; v < nvec; v += kStep) {
     const long long nv = v + kStep;
-    const bool full_next = nv + kStep <= nvec;
     if (lane == 0) prefetch_l2(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
     uint32_t emax = 0;
+    if (nv + kStep <= nvec) {
+      // steady state: the next batch is complete, unguarded loads at immediate
+      // offsets from one pointer
+      const double *pn = X4 + 4 * (nv + lane);
 #pragma unroll
-    for (int u = 0; u < kVecPerLane; ++u) {
-      uint32_t e[4];
+      for (int u = 0; u < kVecPerLane; ++u) {
+        uint32_t e[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        e[q] = exponent_field(b0.w[u][2 * q + 1]);
-        emax = max(emax, e[q]);
+        for (int q = 0; q < 4; ++q) {
+          e[q] = exponent_field(b0.w[u][2 * q + 1]);
+          emax = max(emax, e[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc::add_term(a, b0.w[u][2 * q], b0.w[u][2 * q + 1], e[q]);
+        ldg256(pn + 4 * 32 * u, b0.w[u]);
       }
+    } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc::add_term(a, b0.w[u][2 * q], b0.w[u][2 * q + 1], e[q]);
-      const long long vv = nv + u * 32 + lane;
-      if (full_next || vv < nvec) {
-        ldg256(X4 + 4 * vv, b0.w[u]);
-      } else {
+      for (int u = 0; u < kVecPerLane; ++u) {
+        uint32_t e[4];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) b0.w[u][q] = 0u;
+        for (int q = 0; q < 4; ++q) {
+          e[q] = exponent_field(b0.w[u][2 * q + 1]);
+          emax = max(emax, e[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc::add_term(a, b0.w[u][2 * q], b0.w[u][2 * q + 1], e[q]);
+        const long long vv = nv + u * 32 + lane;
+        if (vv < nvec) {
+          ldg256(X4 + 4 * vv, b0.w[u]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) b0.w[u][q] = 0u;
+        }
       }
     }
     if (__builtin_expect(emax == 0x7FFu, 0)) {
