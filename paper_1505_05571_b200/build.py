@@ -47,14 +47,15 @@ def build(verbose: bool = False, force: bool = False, defines: tuple[str, ...] =
     tuning variants without touching the default artefact."""
     build_dir.mkdir(parents=True, exist_ok=True)
     lib.parent.mkdir(parents=True, exist_ok=True)
-    dflags = [f"-D{d}" for d in defines]
+    dflags = [f"-D{d}" for d in defines if not d.startswith("NVCC:")]
+    nvcc_extra = [d[5:] for d in defines if d.startswith("NVCC:")]
     objs: list[Path] = []
     common_inc = [f"-I{INCLUDE}", f"-I{CSRC}"]
     for src in CU_SOURCES:
         obj = build_dir / (src + ".o")
         objs.append(obj)
         if force or _stale(obj, [CSRC / src, *HEADERS]):
-            _run([NVCC, *dflags, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xptxas", "-v" if verbose else "-O3",
+            _run([NVCC, *dflags, *nvcc_extra, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xptxas", "-v" if verbose else "-O3",
                   "-Xcompiler", "-fPIC,-ffp-contract=off,-fopenmp", *common_inc,
                   "-c", str(CSRC / src), "-o", str(obj)], verbose)
     for src in CXX_SOURCES:

@@ -235,8 +235,13 @@ __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
 // lanes/clk/SMSP; SHF/LOP3/IADD3/VIMNMX/ISETP go to the ALU, IMAD/VIADD to the
 // FMA pipe).  Per term: 11 ALU + 9 FMA + 4 LSU.  e (exponent field) and s (sign
 // mask) come precomputed from the batch decode.
-__device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
-  uint32_t s, ep, d, mhi, mh, m1, lx, mx, k, la, ha, u0, u1, u2;
+// The term as three 32-bit words of its complemented, shifted significand
+// (u2:u1:u0 = s ? ~(m << sh) : m << sh; the +1 of a negative term is the carry-in
+// s + s), plus e' = max(e, 1).
+__device__ __forceinline__ void decode96(uint32_t lo, uint32_t hi, uint32_t e, uint32_t &s,
+                                         uint32_t &u0, uint32_t &u1, uint32_t &u2,
+                                         uint32_t &ep) {
+  uint32_t d, mhi, mh, m1, lx, mx;
   asm("shr.s32 %0, %1, 31;" : "=r"(s) : "r"(hi));                         // ALU: sign mask
   asm("max.u32 %0, %1, 1;" : "=r"(ep) : "r"(e));                         // ALU
   asm("mad.lo.u32 %0, %1, -1, %2;" : "=r"(d) : "r"(e), "r"(ep));          // FMA: 1 iff e == 0
@@ -248,6 +253,31 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(s), "r"(lx), "r"(ep));   // ALU
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lx), "r"(mx), "r"(ep));  // ALU
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mx), "r"(s), "r"(ep));   // ALU
+}
+
+// Read-modify-write of slot k with a 96-bit two's-complement value (no carry-in).
+__device__ __forceinline__ void slot_add96(const Lane &a, uint32_t k, uint32_t v0, uint32_t v1,
+                                           uint32_t v2) {
+  uint32_t la, ha;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(k), "r"(a.c128), "r"(a.sl));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));
+  asm volatile(
+      "{\n\t.reg .u32 l, h0, h1;\n\t"
+      "ld.shared.u32 l, [%0];\n\t"
+      "ld.shared.v2.u32 {h0, h1}, [%1];\n\t"
+      "add.cc.u32 l, l, %2;\n\t"
+      "addc.cc.u32 h0, h0, %3;\n\t"
+      "addc.u32 h1, h1, %4;\n\t"
+      "st.shared.u32 [%0], l;\n\t"
+      "st.shared.v2.u32 [%1], {h0, h1};\n\t}"
+      :
+      : "r"(la), "r"(ha), "r"(v0), "r"(v1), "r"(v2)
+      : "memory");
+}
+
+__device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
+  uint32_t s, ep, k, la, ha, u0, u1, u2;
+  decode96(lo, hi, e, s, u0, u1, u2, ep);
   asm("shr.u32 %0, %1, 5;" : "=r"(k) : "r"(ep));                          // ALU
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(k), "r"(a.c128), "r"(a.sl));  // FMA
 #if EXSUM_HSPLIT
@@ -543,6 +573,13 @@ constexpr int kNormEvery = 2016 / kBatchTerms;    // batches between renormalisa
 #define EXSUM_PREFETCH_BATCHES 1
 #endif
 constexpr int kPrefetchBatches = EXSUM_PREFETCH_BATCHES;  // L2 prefetch distance
+#ifndef EXSUM_UNIFORM_FAST
+#define EXSUM_UNIFORM_FAST 1  // register fast path when a warp's batch hits one slot per lane
+#endif
+#ifndef EXSUM_UNIFORM_BACKOFF
+#define EXSUM_UNIFORM_BACKOFF 7
+#endif
+constexpr int kUniformBackoff = EXSUM_UNIFORM_BACKOFF;
 #ifndef EXSUM_ROLL
 #define EXSUM_ROLL 1  // rolling single-buffer loads with batch-end Inf/NaN fix-up
 #endif
@@ -820,6 +857,7 @@ __device__ void warp_accumulate(const double *__restrict__ x, unsigned long long
     for (int d = 0; d <= kPrefetchBatches; ++d) prefetch_l2(X4, d * kStep, nvec);
   }
   load_batch(b0, X4, 0, nvec, lane);
+  int backoff = 0;
   for (long long v = 0; v < nvec; v += kStep) {
     const long long nv = v + kStep;
     if (lane == 0) prefetch_l2(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
@@ -828,6 +866,65 @@ __device__ void warp_accumulate(const double *__restrict__ x, unsigned long long
       // steady state: the next batch is complete, unguarded loads at immediate
       // offsets from one pointer
       const double *pn = X4 + 4 * (nv + lane);
+#if EXSUM_UNIFORM_FAST
+      // Slot of a term = top six exponent bits (hi bits 25..30; e = 0 maps to
+      // slot 0 like e' = 1).  All terms of the batch share a slot iff the AND and
+      // the OR of their high words agree on those bits: 3-input LOP3 chains, no
+      // per-term exponent kept live.  Slot 63 may hold Inf/NaN: never "uniform".
+      // Wide data rarely turns uniform: after a non-uniform batch the test is
+      // skipped for the next kUniformBackoff batches (warp-uniform counter).
+      bool fast = false;
+      uint32_t kbits = 0u;
+      if (backoff > 0) {
+        --backoff;
+      } else {
+        uint32_t hor = 0u, hand = 0xFFFFFFFFu;
+#pragma unroll
+        for (int u = 0; u < kVecPerLane; ++u)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            hor |= b0.w[u][2 * q + 1];
+            hand &= b0.w[u][2 * q + 1];
+          }
+        kbits = hor & 0x7E000000u;
+        const bool uniform = kbits == (hand & 0x7E000000u) && kbits != 0x7E000000u;
+        fast = __all_sync(0xffffffffu, uniform);
+        if (!fast) backoff = kUniformBackoff;
+      }
+      if (fast) {
+        // every lane's batch lies in one slot: sum it in registers (|sum| < 2^89),
+        // then one read-modify-write of that slot
+        uint32_t r0 = 0, r1 = 0, r2 = 0;
+#pragma unroll
+        for (int u = 0; u < kVecPerLane; ++u) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t sg, u0, u1, u2, ep;
+            acc::decode96(b0.w[u][2 * q], b0.w[u][2 * q + 1], exponent_field(b0.w[u][2 * q + 1]),
+                          sg, u0, u1, u2, ep);
+            asm("{\n\t.reg .u32 cf;\n\tadd.cc.u32 cf, %3, %3;\n\taddc.cc.u32 %0, %0, %4;\n\t"
+                "addc.cc.u32 %1, %1, %5;\n\taddc.u32 %2, %2, %6;\n\t}"
+                : "+r"(r0), "+r"(r1), "+r"(r2)
+                : "r"(sg), "r"(u0), "r"(u1), "r"(u2));
+          }
+          ldg256(pn + 4 * 32 * u, b0.w[u]);
+        }
+        acc::slot_add96(a, kbits >> 25, r0, r1, r2);
+      } else {
+#pragma unroll
+        for (int u = 0; u < kVecPerLane; ++u) {
+          uint32_t e[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            e[q] = exponent_field(b0.w[u][2 * q + 1]);
+            emax = max(emax, e[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc::add_term(a, b0.w[u][2 * q], b0.w[u][2 * q + 1], e[q]);
+          ldg256(pn + 4 * 32 * u, b0.w[u]);
+        }
+      }
+#else
 #pragma unroll
       for (int u = 0; u < kVecPerLane; ++u) {
         uint32_t e[4];
@@ -840,6 +937,7 @@ __device__ void warp_accumulate(const double *__restrict__ x, unsigned long long
         for (int q = 0; q < 4; ++q) acc::add_term(a, b0.w[u][2 * q], b0.w[u][2 * q + 1], e[q]);
         ldg256(pn + 4 * 32 * u, b0.w[u]);
       }
+#endif
     } else {
 #pragma unroll
       for (int u = 0; u < kVecPerLane; ++u) {
