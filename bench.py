@@ -40,6 +40,7 @@ WORKLOADS = {
     2: dict(n=100_000_000, per_gpu=True, desc="config2: N=1e8 float64 U[0,1) per GPU (narrow exponent range)"),
     3: dict(n=100_000_000, per_gpu=True, desc="config3: N=1e8 float64, uniform sign/exponent 1..2046/mantissa + 1% denormals per GPU"),
     4: dict(n=1_000_000_000, per_gpu=False, desc="config4: N=1e9 float64 heavy cancellation, shuffled, sharded across GPUs"),
+    5: dict(n=65_536, per_gpu=False, desc="config5: 65,536 segments, lengths log-uniform [1e3,1e5], N(0,1)*10^k (k in [-300,300]) with 1e-4 Inf/-Inf/NaN; one exact sum per segment"),
 }
 
 
@@ -146,6 +147,8 @@ def run_reference_arm(args, wl, n_total):
     chk = checker()
     threads = os.cpu_count() or 1
     chk.set_threads(threads)
+    if args.config == 5:
+        return run_reference_segmented(args, wl, chk, threads)
     x = np.empty(n_total, dtype=np.float64)
     _lib.call("exsum_host_gen", args.config, args.seed, n_total, 0, n_total, x.ctypes.data)
     # bounded sample per step: whole run (warmup + steps) within ~90 s
@@ -182,6 +185,178 @@ def run_reference_arm(args, wl, n_total):
     print(json.dumps(line), flush=True)
 
 
+def run_reference_segmented(args, wl, chk, threads):
+    """Reference CPU arm for config 5: exact_sum(large) per segment, OpenMP over
+    segments on a bounded sample of the segment list.  The
+    values come from the device generator (copied to the host before timing)."""
+    import torch
+    from paper_1505_05571_b200 import _lib
+    nseg_total = int(args.n) if args.n else wl["n"]
+    offs = np.zeros(nseg_total + 1, dtype=np.uint64)
+    _lib.call("exsum_host_gen_offsets", args.seed, nseg_total, 1000, 100_000, offs.ctypes.data)
+    m = min(nseg_total, 8192)
+    nt = int(offs[m])
+    xd = torch.empty(nt, dtype=torch.float64, device="cuda")
+    _lib.call("exsum_cuda_gen_segmented", args.seed, 0, nt, xd.data_ptr(),
+              torch.cuda.current_stream().cuda_stream)
+    x = xd.cpu().numpy()
+    del xd
+    loc = offs[: m + 1]
+    steps = args.steps or 10
+    for _ in range(args.warmup):
+        chk.segmented_sum(x, loc, threads)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        chk.segmented_sum(x, loc, threads)
+    el = time.perf_counter() - t0
+    bytes_step = 8 * nt + 16 * m + 8
+    gbs = bytes_step * steps / el / 1e9
+    desc = f"first {m} of {nseg_total} segments ({nt:.3g} terms) per step, exact_sum per segment, OpenMP {threads} threads"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": round(el / steps * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based generator, BASELINE.json shapes)",
+        "config": {"workload": wl["desc"], "segments": nseg_total, "sample_segments": m},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": chk.kind,
+                         "sample": desc},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+# ------------------------------------------------------- config 5 (segments)
+
+def run_segmented(args, wl):
+    """Config 5: one exact sum per segment (exsum_cuda_sum_segmented).  Segments
+    are independent, so N GPUs split the segment list (no collective)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1505_05571_b200 import _lib, ops
+    from paper_1505_05571_b200.distributed import shard_bounds
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream(dev)
+    nseg_total = int(args.n) if args.n else wl["n"]
+    offs = np.zeros(nseg_total + 1, dtype=np.uint64)
+    _lib.call("exsum_host_gen_offsets", args.seed, nseg_total, 1000, 100_000, offs.ctypes.data)
+    sb, se = shard_bounds(nseg_total, world, rank)
+    t0, t1 = int(offs[sb]), int(offs[se])
+    n_local = t1 - t0
+    x = torch.empty(n_local, dtype=torch.float64, device=dev)
+    _lib.call("exsum_cuda_gen_segmented", args.seed, t0, n_local, x.data_ptr(), stream.cuda_stream)
+    loc = (offs[sb:se + 1] - offs[sb]).astype(np.int64)
+    o = torch.from_numpy(loc).to(dev)
+    ws = ops.Workspace(dev)
+    nseg = se - sb
+    out = torch.empty(nseg, dtype=torch.float64, device=dev)
+    bytes_step = 8 * n_local + 8 * (nseg + 1) + 8 * nseg  # algorithmic: values, offsets, sums
+
+    def step():
+        return ops.exact_sum_segmented(x, o, workspace=ws)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    step()
+    torch.cuda.synchronize()
+    per = time.perf_counter() - t
+    steps = args.steps or max(5, min(2000, int(0.5 / max(per, 1e-6))))
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for _ in range(steps):
+            res = step()
+        stop.record(stream)
+        torch.cuda.synchronize()
+    ms = start.elapsed_time(stop)
+    tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt[0])
+    total_bytes = 8 * int(offs[-1]) + 16 * nseg_total + 8
+    value = total_bytes * steps / (ms / 1e3) / 1e9
+    achieved = bytes_step / (ms / steps / 1e3) / 1e9
+
+    # e2e: pinned host values/offsets -> device (torch copies) -> segmented sums -> host
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.empty(n_local, dtype=torch.float64, pin_memory=True)
+        hx.copy_(x)
+        ho = torch.from_numpy(loc).pin_memory()
+        hout = torch.empty(nseg, dtype=torch.float64, pin_memory=True)
+        dx = torch.empty_like(x)
+        do = torch.empty_like(o)
+        e_steps = 3
+        torch.cuda.synchronize()
+        tq = time.perf_counter()
+        for _ in range(e_steps):
+            dx.copy_(hx, non_blocking=True)
+            do.copy_(ho, non_blocking=True)
+            r = ops.exact_sum_segmented(dx, do, workspace=ws)
+            hout.copy_(r, non_blocking=True)
+            torch.cuda.synchronize()
+        el = time.perf_counter() - tq
+        assert np.array_equal(hout.numpy().view(np.uint64), res.cpu().numpy().view(np.uint64))
+        e2e = {"value": round(bytes_step * world * e_steps / el / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": 8 * n_local + 8 * (nseg + 1),
+               "d2h_bytes_per_step": 8 * nseg,
+               "path": "pinned host -> torch H2D copies -> exsum_cuda_sum_segmented -> D2H sums"}
+        del hx, dx
+
+    cpu, parity = None, None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle.port import checker
+        chk = checker()
+        threads = os.cpu_count() or 1
+        m = min(nseg, 4096)  # bounded sample: first 4096 segments (~9e7 terms)
+        hxs = x[: int(loc[m])].cpu().numpy()
+        want = chk.segmented_sum(hxs, loc[: m + 1], threads)
+        parity = bool(np.array_equal(want.view(np.uint64), res[:m].cpu().numpy().view(np.uint64)))
+        t = time.perf_counter()
+        reps = 0
+        while time.perf_counter() - t < 3.0:
+            chk.segmented_sum(hxs, loc[: m + 1], threads)
+            reps += 1
+        el = time.perf_counter() - t
+        sb_bytes = 8 * hxs.size + 16 * m + 8
+        cpu = {"value": round(sb_bytes * reps / el / 1e9, 3), "unit": "GB/s", "cores": threads,
+               "kind": chk.kind,
+               "sample": f"first {m} segments ({hxs.size:.3g} terms) x {reps}, exact_sum(large) per "
+                         f"segment, OpenMP over segments on {threads} threads"}
+    if rank == 0:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+        peak = float(peaks.get("hbm_gbs", 6650.0))
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
+            "steps": steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms / steps, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded counter-based generator, BASELINE.json shapes)",
+            "config": {"workload": wl["desc"], "segments": nseg_total, "n_total": int(offs[-1]),
+                       "parallelism": f"segments split over {world} GPU(s), no collective",
+                       "l2": "11.3 GB input > 126 MB L2"},
+            "terms_per_s": round(int(offs[-1]) * steps / (ms / 1e3), 1),
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "kernel": "exsum_segmented_kernel", "kernel_ms": round(ms / steps, 4)},
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": steps, "clocks": clocks.report(),
+            "bit_exact_vs_oracle_first4096": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------- GPU arm
 
 def main():
@@ -194,6 +369,8 @@ def main():
     n_total = n_arg * world if wl["per_gpu"] else n_arg
     if args.impl == "reference":
         return run_reference_arm(args, wl, n_total)
+    if args.config == 5:
+        return run_segmented(args, wl)
 
     import torch
     import torch.distributed as dist

@@ -181,10 +181,12 @@ int exsum_cuda_gen(int config, uint64_t seed, uint64_t n_total, uint64_t first,
                    size_t count, double *d_out, void *stream);
 int exsum_host_gen(int config, uint64_t seed, uint64_t n_total, uint64_t first,
                    size_t count, double *out);
-/* Config 5: nseg segment lengths log-uniform in [lo, hi]; offsets (nseg+1). */
+/* Config 5: nseg segment lengths log-uniform in [lo, hi]; offsets (nseg+1);
+ * values (normal * 10^k with 1e-4 specials) for global indices [first, first+count). */
 int exsum_host_gen_offsets(uint64_t seed, size_t nseg, uint64_t lo, uint64_t hi,
                            uint64_t *offsets);
-int exsum_cuda_gen_segmented(uint64_t seed, uint64_t n_total, double *d_out, void *stream);
+int exsum_cuda_gen_segmented(uint64_t seed, uint64_t first, size_t count, double *d_out,
+                             void *stream);
 
 /* Library build/version info: "exsum_b200 <version> sm_100a". */
 const char *exsum_version(void);

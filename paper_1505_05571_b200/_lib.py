@@ -98,7 +98,7 @@ _SIGNATURES = {
     "exsum_cuda_gen": (_i32, [_i32, _u64, _u64, _u64, _sz, _vp, _vp]),
     "exsum_host_gen": (_i32, [_i32, _u64, _u64, _u64, _sz, _vp]),
     "exsum_host_gen_offsets": (_i32, [_u64, _sz, _u64, _u64, _vp]),
-    "exsum_cuda_gen_segmented": (_i32, [_u64, _u64, _vp, _vp]),
+    "exsum_cuda_gen_segmented": (_i32, [_u64, _u64, _sz, _vp, _vp]),
     "exsum_version": (C.c_char_p, []),
 }
 

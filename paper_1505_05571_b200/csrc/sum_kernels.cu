@@ -6,39 +6,39 @@
 // split-merge of parallel_exact_sum (vector_ops.cpp:172-186).  See DESIGN.md.
 //
 // Device representation (B200-first, not the reference's): every LANE owns a
-// private fixed-point superaccumulator in shared memory, so a term costs one
-// conflict-free shared read-modify-write and a handful of integer instructions
-// — no atomics, no bank conflicts, no dependence on how exponents are
-// distributed.  Two slot layouts are built (EXSUM_SLOT_BITS):
-//
-//   128 (default)  slot k = signed 128-bit integer of weight 2^(64k - 1075);
-//                  a term m * 2^(e' - 1075) adds m << (e' & 63) (< 2^116) to slot
-//                  e' >> 6.  33 slots x 16 B = 528 B per lane, 16.9 KB per warp:
-//                  12 warps per SM.  One LDS.128 + 4 adds + one STS.128.
-//   96             slot k = signed 96-bit integer of weight 2^(32k - 1075) — the
-//                  reference's chunk weight — as a u32 plane and an s64 plane;
-//                  66 slots, 25.3 KB per warp: 8 warps per SM.
-//
-// Either way 2^11 of headroom absorbs 2047 terms per slot; each lane
-// renormalises (carries upward) at most every 2016 terms.  e' = max(e, 1) and the
-// implicit one is dropped for e == 0 (denormals, paper §small).
+// private fixed-point superaccumulator in shared memory — 66 slots, slot k a
+// signed 96-bit integer of weight 2^(32k - 1075) (the reference's chunk weight)
+// stored as a u32 plane L[k][lane] and an s64 plane H[k][lane] (25.3 KB per
+// warp, 8 warps per SM).  A term (-1)^s m 2^(e' - 1075), e' = max(e, 1), adds
+// m << (e' & 31) (< 2^84) to slot e' >> 5: one conflict-free read-modify-write,
+// no atomics, independent of the exponent distribution.  2^11 of headroom per
+// slot = 2047 terms; each lane renormalises at most every 2016 terms.
 //
 // Why not the reference's 4096 shared bins: 64-bit shared atomics compile to
 // ATOMS.CAST.SPIN.64 CAS loops on sm_100a, random-bin read-modify-writes cost
-// ~3.5x in bank conflicts, and narrow data (U[0,1)) puts half of all terms in
-// one bin.  Lane privatisation removes all three.
+// ~3.5x in bank conflicts, and U[0,1) puts half of all terms in one bin.
+//
+// Per-term cost (~25 SASS: 12 ALU, 8 FMA, 4 LSU) is balanced between the
+// integer ALU and FMA pipes (IMAD forms for xor-with-sign and addresses).
+// Loads are 256-bit (LDG.E.NA.ENL2.256), "rolling": a vector's registers are
+// refilled with the next batch's vector right after its four terms are added,
+// with a cp.async.bulk L2 prefetch one batch further ahead.  When every lane's
+// batch falls in one slot (narrow exponent ranges) the batch is summed in
+// registers and the slot gets one read-modify-write.  The sustained rate is
+// bounded by the 1 kW power cap, so fewer instructions and fewer shared-memory
+// accesses per term translate directly into throughput.
 //
 // Kernels
 //   exsum_sum_kernel        K1+K2+K3: persistent grid (1 CTA per SM), each warp
-//                           streams a contiguous range with 256-bit loads
-//                           (register double-buffered, L2 bulk prefetch ahead),
-//                           lanes accumulate privately; the CTA combines its
+//                           streams a contiguous range; the CTA combines its
 //                           lanes into 67 chunk sums, REDG.ADD.64 into the
 //                           workspace; the last CTA canonicalises, resolves
-//                           Inf/NaN by first index, rounds.
-//   exsum_segmented_kernel  K4: one warp per segment (dynamic), same inner loop,
-//                           warp-local combine + round, one double per segment.
+//                           Inf/NaN by first index and rounds (warp-parallel).
+//                           Launchable with programmatic dependent launch.
+//   exsum_segmented_kernel  K4: one warp per segment (dynamic claim), compact
+//                           loop body (instruction-cache bound otherwise).
 //   exsum_merge_kernel      K5: merge of k gathered partial records + round.
+//   exsum_finalize_kernel   round a workspace filled by incremental launches.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -46,23 +46,23 @@
 #include "exsum_b200.h"
 #include "exsum_core.h"
 
-#ifndef EXSUM_EXPERIMENT
-#define EXSUM_EXPERIMENT 0
+#ifndef EXSUM_VEC_PER_LANE
+#define EXSUM_VEC_PER_LANE 8  // single-sum kernel: 256-bit vectors per lane per batch
 #endif
-#ifndef EXSUM_SLOT_BITS
-#define EXSUM_SLOT_BITS 96
+#ifndef EXSUM_SEG_VEC
+#define EXSUM_SEG_VEC 8  // segmented kernel: vectors per lane per batch
 #endif
-#ifndef EXSUM_DECODE
-#define EXSUM_DECODE 2  // 0: ALU-pipe decode, 1: FMA-pipe decode, 2: pipe-balanced
+#ifndef EXSUM_SEG_SPLIT
+#define EXSUM_SEG_SPLIT 0  // segmented kernel: separate unguarded steady-state body
 #endif
-#ifndef EXSUM_HSPLIT
-#define EXSUM_HSPLIT 0  // slot96: high word as two 32-bit planes (all accesses 32-bit)
+#ifndef EXSUM_PREFETCH_BATCHES
+#define EXSUM_PREFETCH_BATCHES 1  // L2 bulk-prefetch distance, in batches
 #endif
-#ifndef EXSUM_PIPE
-#define EXSUM_PIPE 0  // 0 serial RMW, 1 store forwarding, 2 run merge (slot layout 96)
+#ifndef EXSUM_UNIFORM_FAST
+#define EXSUM_UNIFORM_FAST 1  // single-sum kernel: register fast path for one-slot batches
 #endif
-#if EXSUM_HSPLIT && (EXSUM_DECODE != 2 || EXSUM_PIPE != 0 || EXSUM_SLOT_BITS != 96)
-#error "EXSUM_HSPLIT needs EXSUM_DECODE=2, EXSUM_PIPE=0, EXSUM_SLOT_BITS=96"
+#ifndef EXSUM_UNIFORM_BACKOFF
+#define EXSUM_UNIFORM_BACKOFF 7  // batches to skip the one-slot test after a miss
 #endif
 
 namespace exsum_b200 {
@@ -89,126 +89,23 @@ struct Specials {                // first occurrences seen by one lane
 
 __device__ __forceinline__ uint32_t exponent_field(uint32_t hi) { return (hi >> 20) & 0x7FFu; }
 
-// =========================================================== slot layout: 128
-namespace slot128 {
-
-constexpr int kWarps = 12;
-constexpr int kSlots = 33;                  // 0..31 take terms (e' >> 6), 32 carries only
-constexpr int kWarpSmem = kSlots * 32 * 16;  // 16,896 B
-constexpr int kDefaultVec = 4;
-
-struct Lane {
-  uint4 *P;     // this lane's slot 0; slot k at P[32 k] (lane-interleaved 16 B entries)
-  uint32_t sa;  // shared address of P; slot k at sa + 512 k
-};
-
-__device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
-  Lane v;
-  v.P = reinterpret_cast<uint4 *>(warp_smem) + lane;
-  v.sa = static_cast<uint32_t>(__cvta_generic_to_shared(v.P));
-  return v;
-}
-
-// term = (-1)^s m 2^(e'-1075): add m << sh, sh = e' & 63, to slot e' >> 6.  For a
-// negative term add ~(m << sh) + 1: the complement is folded into the funnel
-// shifts (fill word s), the +1 is the carry-in (CC.CF = s & 1 from s + s).
-// -0.0 adds 2^128, i.e. nothing.
-__device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
-  const uint32_t ep = max(e, 1u);
-  const uint32_t imp = e ? 0x100000u : 0u;
-  const uint32_t s = static_cast<uint32_t>(static_cast<int32_t>(hi) >> 31);
-  const uint32_t mx = ((hi & 0xFFFFFu) | imp) ^ s;
-  const uint32_t lx = lo ^ s;
-  const uint32_t w0 = __funnelshift_l(s, lx, ep);   // shift count taken mod 32
-  const uint32_t w1 = __funnelshift_l(lx, mx, ep);
-  const uint32_t w2 = __funnelshift_l(mx, s, ep);
-  const bool up = (ep & 32u) != 0u;                  // shift by 32 more: one word up
-  const uint32_t u0 = up ? s : w0, u1 = up ? w0 : w1, u2 = up ? w1 : w2, u3 = up ? w2 : s;
-  const uint32_t addr = a.sa + ((ep >> 6) << 9);
-  asm volatile(
-      "{\n\t.reg .u32 q0, q1, q2, q3, cf;\n\t"
-      "ld.shared.v4.u32 {q0, q1, q2, q3}, [%0];\n\t"
-      "add.cc.u32 cf, %1, %1;\n\t"
-      "addc.cc.u32 q0, q0, %2;\n\t"
-      "addc.cc.u32 q1, q1, %3;\n\t"
-      "addc.cc.u32 q2, q2, %4;\n\t"
-      "addc.u32 q3, q3, %5;\n\t"
-      "st.shared.v4.u32 [%0], {q0, q1, q2, q3};\n\t}"
-      :
-      : "r"(addr), "r"(s), "r"(u0), "r"(u1), "r"(u2), "r"(u3)
-      : "memory");
-}
-
-// Carry upward: slots 0..31 end in [0, 2^64) (high half zero), slot 32 keeps the
-// rest.  Each slot has absorbed <= 2047 terms (< 2^127 with the incoming carry).
-__device__ __forceinline__ void normalize(const Lane &a) {
-  long long c = 0;
-#pragma unroll 4
-  for (int k = 0; k < kSlots - 1; ++k) {
-    const uint4 v = a.P[32 * k];
-    const unsigned long long lo = (static_cast<unsigned long long>(v.y) << 32) | v.x;
-    const long long hi = static_cast<long long>((static_cast<unsigned long long>(v.w) << 32) | v.z);
-    const unsigned long long nlo = lo + static_cast<unsigned long long>(c);
-    const long long nhi = hi + (c >> 63) + (nlo < lo ? 1 : 0);
-    a.P[32 * k] = make_uint4(static_cast<uint32_t>(nlo), static_cast<uint32_t>(nlo >> 32), 0u, 0u);
-    c = nhi;
-  }
-  const uint4 v = a.P[32 * (kSlots - 1)];
-  const unsigned long long lo = (static_cast<unsigned long long>(v.y) << 32) | v.x;
-  const long long hi = static_cast<long long>((static_cast<unsigned long long>(v.w) << 32) | v.z);
-  const unsigned long long nlo = lo + static_cast<unsigned long long>(c);
-  const unsigned long long nhi =
-      static_cast<unsigned long long>(hi + (c >> 63) + (nlo < lo ? 1 : 0));
-  a.P[32 * (kSlots - 1)] = make_uint4(static_cast<uint32_t>(nlo), static_cast<uint32_t>(nlo >> 32),
-                                      static_cast<uint32_t>(nhi), static_cast<uint32_t>(nhi >> 32));
-}
-
-// The warp's exact sum as 67 chunk values (row[0..66], |row[i]| < 2^38):
-// normalise each lane, then lane j sums slot j's two low words over all lanes.
-__device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, const Lane &a, int lane,
-                                            long long *row) {
-  normalize(a);
-  __syncwarp();
-  const uint4 *base = reinterpret_cast<const uint4 *>(warp_smem);
-  unsigned long long s0 = 0, s1 = 0;
-#pragma unroll 8
-  for (int i = 0; i < 32; ++i) {
-    const int col = (i + lane) & 31;
-    const uint2 v = *reinterpret_cast<const uint2 *>(&base[lane * 32 + col]);
-    s0 += v.x;
-    s1 += v.y;
-  }
-  row[2 * lane] = static_cast<long long>(s0);
-  row[2 * lane + 1] = static_cast<long long>(s1);
-  const uint4 t = base[(kSlots - 1) * 32 + lane];
-  unsigned long long c64 = t.x, c65 = t.y;
-  long long c66 = static_cast<long long>((static_cast<unsigned long long>(t.w) << 32) | t.z);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    c64 += __shfl_xor_sync(0xffffffffu, c64, o);
-    c65 += __shfl_xor_sync(0xffffffffu, c65, o);
-    c66 += __shfl_xor_sync(0xffffffffu, c66, o);
-  }
-  if (lane == 0) {
-    row[64] = static_cast<long long>(c64);
-    row[65] = static_cast<long long>(c65);
-    row[66] = c66;
-  }
-}
-
-}  // namespace slot128
-
-// ============================================================ slot layout: 96
-namespace slot96 {
+// ------------------------------------------------------ lane accumulators
 
 constexpr int kWarps = 8;
-constexpr int kSlots = 66;       // slots 0..63 take terms (e' >> 5), 64..65 only carries
+constexpr int kThreads = kWarps * 32;
+constexpr int kSlots = 66;  // slots 0..63 take terms (e' >> 5), 64..65 only carries
 constexpr int kLPlane = kSlots * 32 * 4;
 constexpr int kHPlane = kSlots * 32 * 8;
-constexpr int kWarpSmem = kLPlane + kHPlane;  // 25,344 B
-constexpr int kDefaultVec = 8;
+constexpr int kWarpSmem = kLPlane + kHPlane;            // 25,344 B
+constexpr int kScratch = kWarps * kChunks * 8;          // per-warp chunk rows
+constexpr int kSmem = kWarps * kWarpSmem + kScratch;    // 207,040 B
+constexpr int kPrefetchBatches = EXSUM_PREFETCH_BATCHES;
+constexpr int kUniformBackoff = EXSUM_UNIFORM_BACKOFF;
+static_assert(kSmem <= 227 * 1024, "shared memory budget");
 
-// Slot k's low word is at sl + 128 k and its high word at 2 * (sl + 128 k) + hoff.
+// One lane's view of its accumulator.  Generic pointers serve the cold paths;
+// the hot path uses 32-bit shared addresses: slot k's low word at sl + 128 k,
+// its high word at 2 (sl + 128 k) + hoff.
 struct Lane {
   uint32_t *L;            // &Lplane[0][lane]; slot k at L[32 k]
   unsigned long long *H;  // &Hplane[0][lane]; slot k at H[32 k]
@@ -229,15 +126,20 @@ __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
   return v;
 }
 
-// Same scheme as slot128 with a 96-bit window: m << (e' & 31) at slot e' >> 5.
-#if EXSUM_DECODE == 2
-// Pipe-balanced form (the B200 integer ALU pipe and the FMA pipe each retire 16
-// lanes/clk/SMSP; SHF/LOP3/IADD3/VIMNMX/ISETP go to the ALU, IMAD/VIADD to the
-// FMA pipe).  Per term: 11 ALU + 9 FMA + 4 LSU.  e (exponent field) and s (sign
-// mask) come precomputed from the batch decode.
+// Zero one warp's accumulator cooperatively with 16-byte stores.
+__device__ __forceinline__ void zero_warp(unsigned char *warp_smem, int lane) {
+  uint4 *p = reinterpret_cast<uint4 *>(warp_smem);
+  constexpr int n16 = kWarpSmem / 16;
+#pragma unroll 4
+  for (int i = lane; i < n16; i += 32) p[i] = make_uint4(0, 0, 0, 0);
+}
+
 // The term as three 32-bit words of its complemented, shifted significand
-// (u2:u1:u0 = s ? ~(m << sh) : m << sh; the +1 of a negative term is the carry-in
-// s + s), plus e' = max(e, 1).
+// (u2:u1:u0 = s ? ~(m << sh) : m << sh; a negative term's +1 is the carry-in
+// s + s) and e' = max(e, 1).  Pipe-balanced: the B200 integer ALU pipe and the
+// FMA pipe each retire 16 lanes/clk/SMSP (measured, profiles/r01_pipe_probe_*):
+// SHF/LOP3/IADD3/VIMNMX on the ALU pipe, IMAD (x ^ s = x (2s + 1) + s for
+// s in {0,-1}) on the FMA pipe.
 __device__ __forceinline__ void decode96(uint32_t lo, uint32_t hi, uint32_t e, uint32_t &s,
                                          uint32_t &u0, uint32_t &u1, uint32_t &u2,
                                          uint32_t &ep) {
@@ -245,14 +147,14 @@ __device__ __forceinline__ void decode96(uint32_t lo, uint32_t hi, uint32_t e, u
   asm("shr.s32 %0, %1, 31;" : "=r"(s) : "r"(hi));                         // ALU: sign mask
   asm("max.u32 %0, %1, 1;" : "=r"(ep) : "r"(e));                         // ALU
   asm("mad.lo.u32 %0, %1, -1, %2;" : "=r"(d) : "r"(e), "r"(ep));          // FMA: 1 iff e == 0
-  asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x100000u));  // ALU: (a&b)|c
+  asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x100000u));  // (a&b)|c
   asm("mad.lo.u32 %0, %1, -1048576, %2;" : "=r"(mh) : "r"(d), "r"(mhi));  // FMA: drop implicit 1
   asm("mad.lo.u32 %0, %1, 2, 1;" : "=r"(m1) : "r"(s));                    // FMA: +-1
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(lx) : "r"(lo), "r"(m1), "r"(s));  // FMA: lo ^ s
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(mx) : "r"(mh), "r"(m1), "r"(s));  // FMA: mh ^ s
-  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(s), "r"(lx), "r"(ep));   // ALU
-  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lx), "r"(mx), "r"(ep));  // ALU
-  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mx), "r"(s), "r"(ep));   // ALU
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(s), "r"(lx), "r"(ep));   // shift mod 32
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lx), "r"(mx), "r"(ep));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mx), "r"(s), "r"(ep));
 }
 
 // Read-modify-write of slot k with a 96-bit two's-complement value (no carry-in).
@@ -275,33 +177,14 @@ __device__ __forceinline__ void slot_add96(const Lane &a, uint32_t k, uint32_t v
       : "memory");
 }
 
+// Add one term (exponent field e != 2047, or 2047 for the blind add of an
+// Inf/NaN that the batch fix-up cancels) to the lane's slots.
 __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
   uint32_t s, ep, k, la, ha, u0, u1, u2;
   decode96(lo, hi, e, s, u0, u1, u2, ep);
-  asm("shr.u32 %0, %1, 5;" : "=r"(k) : "r"(ep));                          // ALU
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(k), "r"(a.c128), "r"(a.sl));  // FMA
-#if EXSUM_HSPLIT
-  // three 32-bit planes: every access is a conflict-free 32-bit LDS/STS at
-  // la + {0, kPlane, 2 kPlane} (immediate offsets, no second address)
-  (void)ha;
-  asm volatile(
-      "{\n\t.reg .u32 l, h0, h1, cf;\n\t"
-      "ld.shared.u32 l, [%0];\n\t"
-      "ld.shared.u32 h0, [%0+8448];\n\t"
-      "ld.shared.u32 h1, [%0+16896];\n\t"
-      "add.cc.u32 cf, %1, %1;\n\t"
-      "addc.cc.u32 l, l, %2;\n\t"
-      "addc.cc.u32 h0, h0, %3;\n\t"
-      "addc.u32 h1, h1, %4;\n\t"
-      "st.shared.u32 [%0], l;\n\t"
-      "st.shared.u32 [%0+8448], h0;\n\t"
-      "st.shared.u32 [%0+16896], h1;\n\t}"
-      :
-      : "r"(la), "r"(s), "r"(u0), "r"(u1), "r"(u2)
-      : "memory");
-  return;
-#endif
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));  // FMA
+  asm("shr.u32 %0, %1, 5;" : "=r"(k) : "r"(ep));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(k), "r"(a.c128), "r"(a.sl));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));
   asm volatile(
       "{\n\t.reg .u32 l, h0, h1, cf;\n\t"
       "ld.shared.u32 l, [%0];\n\t"
@@ -316,71 +199,9 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
       : "r"(la), "r"(ha), "r"(s), "r"(u0), "r"(u1), "r"(u2)
       : "memory");
 }
-#else
-__device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
-#if EXSUM_DECODE == 1
-  // Decode on the FMA pipe (IMAD / IMAD.HI) to unload the integer ALU pipe:
-  // t = hi >> 20, s = sign mask, low 20 mantissa bits = hi - t 2^20, implicit
-  // one = (e + 2047) >> 11, x ^ s = x (2s + 1) + s for s in {0, -1}.
-  const uint32_t t = __umulhi(hi, 4096u);
-  const uint32_t s = static_cast<uint32_t>(__mulhi(static_cast<int>(hi), 1));
-  const uint32_t ib = __umulhi(e + 2047u, 2097152u);
-  const uint32_t mh = hi - t * 1048576u + ib * 1048576u;
-  const uint32_t ep = max(e, 1u);
-  const uint32_t m1 = s * 2u + 1u;
-  const uint32_t lx = lo * m1 + s;
-  const uint32_t mx = mh * m1 + s;
-#else
-  const uint32_t ep = max(e, 1u);
-  const uint32_t imp = e ? 0x100000u : 0u;
-  const uint32_t s = static_cast<uint32_t>(static_cast<int32_t>(hi) >> 31);
-  const uint32_t mx = ((hi & 0xFFFFFu) | imp) ^ s;
-  const uint32_t lx = lo ^ s;
-#endif
-  const uint32_t u0 = __funnelshift_l(s, lx, ep);
-  const uint32_t u1 = __funnelshift_l(lx, mx, ep);
-  const uint32_t u2 = __funnelshift_l(mx, s, ep);
-  const uint32_t la = a.sl + ((ep >> 5) << 7);
-  const uint32_t ha = 2u * la + a.hoff;
-  asm volatile(
-      "{\n\t.reg .u32 l, h0, h1, cf;\n\t"
-      "ld.shared.u32 l, [%0];\n\t"
-      "ld.shared.v2.u32 {h0, h1}, [%1];\n\t"
-      "add.cc.u32 cf, %2, %2;\n\t"
-      "addc.cc.u32 l, l, %3;\n\t"
-      "addc.cc.u32 h0, h0, %4;\n\t"
-      "addc.u32 h1, h1, %5;\n\t"
-      "st.shared.u32 [%0], l;\n\t"
-      "st.shared.v2.u32 [%1], {h0, h1};\n\t}"
-      :
-      : "r"(la), "r"(ha), "r"(s), "r"(u0), "r"(u1), "r"(u2)
-      : "memory");
-}
-#endif
 
 // Carry upward: L_k in [0, 2^32), H_k = 0 for k < 65; slot 65 keeps the rest.
-#if EXSUM_HSPLIT
-__device__ __forceinline__ void normalize(const Lane &a) {
-  uint32_t *H0 = a.L + kSlots * 32, *H1 = a.L + 2 * kSlots * 32;
-  long long c = 0;
-#pragma unroll 6
-  for (int k = 0; k < kSlots - 1; ++k) {
-    const long long u = static_cast<long long>(a.L[32 * k]) + c;
-    const long long h = static_cast<long long>((static_cast<unsigned long long>(H1[32 * k]) << 32) | H0[32 * k]);
-    a.L[32 * k] = static_cast<uint32_t>(u);
-    H0[32 * k] = 0u;
-    H1[32 * k] = 0u;
-    c = h + (u >> 32);
-  }
-  const int k = kSlots - 1;
-  const long long u = static_cast<long long>(a.L[32 * k]) + c;
-  const long long h = static_cast<long long>((static_cast<unsigned long long>(H1[32 * k]) << 32) | H0[32 * k]);
-  const unsigned long long nh = static_cast<unsigned long long>(h + (u >> 32));
-  a.L[32 * k] = static_cast<uint32_t>(u);
-  H0[32 * k] = static_cast<uint32_t>(nh);
-  H1[32 * k] = static_cast<uint32_t>(nh >> 32);
-}
-#else
+// Safe whenever every slot has absorbed <= 2047 terms (|H_k| < 2^63 - 2^52).
 __device__ __forceinline__ void normalize(const Lane &a) {
   long long c = 0;
 #pragma unroll 6
@@ -396,235 +217,61 @@ __device__ __forceinline__ void normalize(const Lane &a) {
   a.L[32 * k] = static_cast<uint32_t>(u);
   a.H[32 * k] = static_cast<unsigned long long>(static_cast<long long>(a.H[32 * k]) + (u >> 32));
 }
-#endif
-
-// ---- pipelined term streams (EXSUM_PIPE) ------------------------------------
-//
-// add_term above is a strict read-modify-write chain per lane: the next term's
-// LDS cannot issue before this term's STS.  The pipes break that chain.
-//
-// Forward (EXSUM_PIPE 1): term j's LDS is issued before term j-1's STS; if both
-// hit the same slot, j-1's fresh value is forwarded from registers.
-// Merge (EXSUM_PIPE 2): a "pending" slot accumulates consecutive terms that hit
-// it in registers; only when the slot changes is the pending value committed
-// (predicated STS) and the new slot loaded (predicated LDS, issued before the
-// commit).  Narrow exponent ranges then touch shared memory rarely.
-
-struct Pipe {
-  uint32_t pla;         // L-plane address of the pending slot
-  uint32_t v0, v1, v2;  // forward: its new value; merge: its loaded base value
-  uint32_t a0, a1, a2;  // merge: pending addend
-};
-
-__device__ __forceinline__ void term_words(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e,
-                                           uint32_t &s, uint32_t &u0, uint32_t &u1,
-                                           uint32_t &u2, uint32_t &la) {
-  const uint32_t ep = max(e, 1u);
-  const uint32_t imp = e ? 0x100000u : 0u;
-  s = static_cast<uint32_t>(static_cast<int32_t>(hi) >> 31);
-  const uint32_t mx = ((hi & 0xFFFFFu) | imp) ^ s;
-  const uint32_t lx = lo ^ s;
-  u0 = __funnelshift_l(s, lx, ep);
-  u1 = __funnelshift_l(lx, mx, ep);
-  u2 = __funnelshift_l(mx, s, ep);
-  la = a.sl + ((ep >> 5) << 7);
-}
-
-__device__ __forceinline__ void pipe_init(const Lane &a, Pipe &p) {
-  p.pla = a.sl;  // slot 0
-  const uint32_t ha = 2u * p.pla + a.hoff;
-  asm volatile("ld.shared.u32 %0, [%3];\n\tld.shared.v2.u32 {%1, %2}, [%4];"
-               : "=r"(p.v0), "=r"(p.v1), "=r"(p.v2)
-               : "r"(p.pla), "r"(ha)
-               : "memory");
-  p.a0 = p.a1 = p.a2 = 0u;
-}
-
-__device__ __forceinline__ void pipe_flush(const Lane &a, Pipe &p) {
-  uint32_t c0 = p.v0, c1 = p.v1, c2 = p.v2;
-#if EXSUM_PIPE == 2
-  asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
-      : "+r"(c0), "+r"(c1), "+r"(c2)
-      : "r"(p.a0), "r"(p.a1), "r"(p.a2));
-#endif
-  const uint32_t ha = 2u * p.pla + a.hoff;
-  asm volatile("st.shared.u32 [%0], %2;\n\tst.shared.v2.u32 [%1], {%3, %4};" ::"r"(p.pla),
-               "r"(ha), "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-
-__device__ __forceinline__ void pipe_step(const Lane &a, Pipe &p, uint32_t lo, uint32_t hi,
-                                          uint32_t e) {
-  uint32_t s, u0, u1, u2, la;
-  term_words(a, lo, hi, e, s, u0, u1, u2, la);
-  const uint32_t ha = 2u * la + a.hoff;
-  const uint32_t pha = 2u * p.pla + a.hoff;
-#if EXSUM_PIPE == 1
-  uint32_t l0, l1, l2;
-  asm volatile(
-      "ld.shared.u32 %0, [%3];\n\t"
-      "ld.shared.v2.u32 {%1, %2}, [%4];\n\t"
-      "st.shared.u32 [%5], %7;\n\t"
-      "st.shared.v2.u32 [%6], {%8, %9};"
-      : "=r"(l0), "=r"(l1), "=r"(l2)
-      : "r"(la), "r"(ha), "r"(p.pla), "r"(pha), "r"(p.v0), "r"(p.v1), "r"(p.v2)
-      : "memory");
-  const bool same = la == p.pla;
-  uint32_t n0 = same ? p.v0 : l0, n1 = same ? p.v1 : l1, n2 = same ? p.v2 : l2;
-  asm("{\n\t.reg .u32 cf;\n\tadd.cc.u32 cf, %3, %3;\n\taddc.cc.u32 %0, %0, %4;\n\t"
-      "addc.cc.u32 %1, %1, %5;\n\taddc.u32 %2, %2, %6;\n\t}"
-      : "+r"(n0), "+r"(n1), "+r"(n2)
-      : "r"(s), "r"(u0), "r"(u1), "r"(u2));
-  p.v0 = n0;
-  p.v1 = n1;
-  p.v2 = n2;
-  p.pla = la;
-#else
-  // commit value of the pending slot (used only if the slot changes)
-  uint32_t c0 = p.v0, c1 = p.v1, c2 = p.v2;
-  asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
-      : "+r"(c0), "+r"(c1), "+r"(c2)
-      : "r"(p.a0), "r"(p.a1), "r"(p.a2));
-  asm volatile(
-      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, %5;\n\t"
-      "@q ld.shared.u32 %0, [%3];\n\t"
-      "@q ld.shared.v2.u32 {%1, %2}, [%4];\n\t"
-      "@q st.shared.u32 [%5], %7;\n\t"
-      "@q st.shared.v2.u32 [%6], {%8, %9};\n\t}"
-      : "+r"(p.v0), "+r"(p.v1), "+r"(p.v2)
-      : "r"(la), "r"(ha), "r"(p.pla), "r"(pha), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-  const bool same = la == p.pla;
-  uint32_t n0 = same ? p.a0 : 0u, n1 = same ? p.a1 : 0u, n2 = same ? p.a2 : 0u;
-  asm("{\n\t.reg .u32 cf;\n\tadd.cc.u32 cf, %3, %3;\n\taddc.cc.u32 %0, %0, %4;\n\t"
-      "addc.cc.u32 %1, %1, %5;\n\taddc.u32 %2, %2, %6;\n\t}"
-      : "+r"(n0), "+r"(n1), "+r"(n2)
-      : "r"(s), "r"(u0), "r"(u1), "r"(u2));
-  p.a0 = n0;
-  p.a1 = n1;
-  p.a2 = n2;
-  p.pla = la;
-#endif
-}
 
 // The warp's exact sum as 67 chunk values, straight from the (unnormalised)
 // slots: slot k = L_k + 2^32 H_k feeds chunk k (L_k), chunk k+1 (low word of H_k)
 // and chunk k+2 (signed high word of H_k); every addend is < 2^32 in magnitude,
 // so 32-lane sums stay below 2^38.  The high word of the carry-only slot 65
-// belongs to chunk 67 and is folded into chunk 66.  Reads are bank-skewed.
-__device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, const Lane &a, int lane,
-                                            long long *row) {
-  (void)a;
+// belongs to chunk 67 and is folded into chunk 66.
+// Lane j sums the rows of slots j, j+32, j+64 with bank-skewed 128-bit reads
+// (8 lanes per wavefront hit 8 distinct 16-byte bank groups), then the chunk
+// values are assembled with shuffles: 24 LDS.128 per lane per round.
+__device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, int lane, long long *row) {
   __syncwarp();
   const uint32_t *Lp = reinterpret_cast<const uint32_t *>(warp_smem);
-#if EXSUM_HSPLIT
-  const uint32_t *H0 = Lp + kSlots * 32, *H1 = Lp + 2 * kSlots * 32;
-#define EXSUM_HLO(k, col) H0[(k) * 32 + (col)]
-#define EXSUM_HHI(k, col) H1[(k) * 32 + (col)]
-#else
-  const uint32_t *Hw = reinterpret_cast<const uint32_t *>(warp_smem + kLPlane);  // H as 2 words
-#define EXSUM_HLO(k, col) Hw[2 * ((k) * 32 + (col))]
-#define EXSUM_HHI(k, col) Hw[2 * ((k) * 32 + (col)) + 1]
-#endif
+  const uint32_t *Hw = reinterpret_cast<const uint32_t *>(warp_smem + kLPlane);
+  long long sl[3], shl[3], shh[3];
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
-    const int c = 32 * r + lane;  // chunk index this lane sums
-    if (c >= kChunks) break;
-    long long acc = 0;
-#pragma unroll 8
-    for (int i = 0; i < 32; ++i) {
-      const int col = (i + lane) & 31;
-      if (c < kSlots) acc += Lp[c * 32 + col];
-      if (c >= 1) acc += EXSUM_HLO(c - 1, col);  // low word of H_{c-1}
-      if (c >= 2 && c - 2 < kSlots - 1)
-        acc += static_cast<int32_t>(EXSUM_HHI(c - 2, col));  // high word of H_{c-2}
-      if (c == kChunks - 1)
-        acc += static_cast<long long>(static_cast<int32_t>(EXSUM_HHI(kSlots - 1, col)))
-               << 32;  // high word of H_65 (chunk 67) folded into chunk 66
+    const int k = 32 * r + lane;
+    sl[r] = shl[r] = shh[r] = 0;
+    if (k < kSlots) {
+      long long a = 0, bl = 0, bh = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(Lp + k * 32 + 4 * ((i + lane) & 7));
+        a += static_cast<long long>(v.x) + v.y + static_cast<long long>(v.z) + v.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(Hw + k * 64 + 4 * ((i + lane) & 15));
+        bl += static_cast<long long>(v.x) + v.z;
+        bh += static_cast<long long>(static_cast<int32_t>(v.y)) + static_cast<int32_t>(v.w);
+      }
+      sl[r] = a;
+      shl[r] = bl;
+      shh[r] = bh;
     }
-#undef EXSUM_HLO
-#undef EXSUM_HHI
-    row[c] = acc;
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int c = 32 * r + lane;
+    long long lo1 = __shfl_up_sync(0xffffffffu, shl[r], 1);   // low word sums of slot c-1
+    long long hi2 = __shfl_up_sync(0xffffffffu, shh[r], 2);   // high word sums of slot c-2
+    const long long wl = __shfl_sync(0xffffffffu, r ? shl[r > 0 ? r - 1 : 0] : 0ll, 31);
+    const long long wh = __shfl_sync(0xffffffffu, r ? shh[r > 0 ? r - 1 : 0] : 0ll, 30 + (lane & 1));
+    if (lane == 0) lo1 = wl;
+    if (lane < 2) hi2 = wh;
+    long long v = sl[r] + lo1 + hi2;
+    if (r == 2) {
+      const long long top = __shfl_sync(0xffffffffu, shh[2], 1);  // high words of slot 65
+      if (c == kChunks - 1) v += top * 4294967296ll;
+    }
+    if (c < kChunks) row[c] = v;
   }
 }
 
-}  // namespace slot96
-
-#if EXSUM_SLOT_BITS == 96
-namespace acc = slot96;
-#elif EXSUM_SLOT_BITS == 128
-namespace acc = slot128;
-#else
-#error "EXSUM_SLOT_BITS must be 96 or 128"
-#endif
-
-// ------------------------------------------------------------ common machinery
-
-constexpr int kWarps = acc::kWarps;
-constexpr int kThreads = kWarps * 32;
-constexpr int kWarpSmem = acc::kWarpSmem;
-#ifndef EXSUM_VEC_PER_LANE
-#define EXSUM_VEC_PER_LANE acc::kDefaultVec
-#endif
-constexpr int kVecPerLane = EXSUM_VEC_PER_LANE;   // 256-bit vectors per lane per batch
-constexpr int kBatchTerms = kVecPerLane * 4;
-constexpr int kNormEvery = 2016 / kBatchTerms;    // batches between renormalisations
-#ifndef EXSUM_PREFETCH_BATCHES
-#define EXSUM_PREFETCH_BATCHES 1
-#endif
-constexpr int kPrefetchBatches = EXSUM_PREFETCH_BATCHES;  // L2 prefetch distance
-#ifndef EXSUM_UNIFORM_FAST
-#define EXSUM_UNIFORM_FAST 1  // register fast path when a warp's batch hits one slot per lane
-#endif
-#ifndef EXSUM_UNIFORM_BACKOFF
-#define EXSUM_UNIFORM_BACKOFF 7
-#endif
-constexpr int kUniformBackoff = EXSUM_UNIFORM_BACKOFF;
-#ifndef EXSUM_ROLL
-#define EXSUM_ROLL 1  // rolling single-buffer loads with batch-end Inf/NaN fix-up
-#endif
-#ifndef EXSUM_CHECK_GROUP
-#define EXSUM_CHECK_GROUP 0  // vectors per Inf/NaN-check group (0: whole batch)
-#endif
-#ifndef EXSUM_PREFETCH_LANES
-#define EXSUM_PREFETCH_LANES 0
-#endif
-#ifndef EXSUM_BUFFERS
-#define EXSUM_BUFFERS 1  // register batch buffers (1: rely on the L2 prefetch)
-#endif
-constexpr int kScratch = kWarps * kChunks * 8;              // per-warp chunk rows
-constexpr int kSmem = kWarps * kWarpSmem + kScratch;
-static_assert(kSmem <= 227 * 1024, "shared memory budget");
-static_assert(kNormEvery >= 1, "batch too large for the carry budget");
-
-using acc::Lane;
-
-// Term stream over a lane accumulator: pipelined (EXSUM_PIPE) or plain RMW.
-#if EXSUM_PIPE != 0 && EXSUM_SLOT_BITS == 96
-using acc::Pipe;
-__device__ __forceinline__ void stream_begin(const Lane &a, Pipe &p) { acc::pipe_init(a, p); }
-__device__ __forceinline__ void stream_end(const Lane &a, Pipe &p) { acc::pipe_flush(a, p); }
-__device__ __forceinline__ void stream_term(const Lane &a, Pipe &p, uint32_t lo, uint32_t hi,
-                                            uint32_t e) {
-  acc::pipe_step(a, p, lo, hi, e);
-}
-#else
-struct Pipe {};
-__device__ __forceinline__ void stream_begin(const Lane &, Pipe &) {}
-__device__ __forceinline__ void stream_end(const Lane &, Pipe &) {}
-__device__ __forceinline__ void stream_term(const Lane &a, Pipe &, uint32_t lo, uint32_t hi,
-                                            uint32_t e) {
-  acc::add_term(a, lo, hi, e);
-}
-#endif
-
-// Zero one warp's accumulator cooperatively with 16-byte stores.
-__device__ __forceinline__ void zero_warp(unsigned char *warp_smem, int lane) {
-  uint4 *p = reinterpret_cast<uint4 *>(warp_smem);
-  constexpr int n16 = kWarpSmem / 16;
-#pragma unroll 4
-  for (int i = lane; i < n16; i += 32) p[i] = make_uint4(0, 0, 0, 0);
-}
+// ------------------------------------------------------------- term streams
 
 __device__ __forceinline__ void record_special(Specials &sp, uint32_t lo, uint32_t hi,
                                                unsigned long long index) {
@@ -644,7 +291,7 @@ __device__ __forceinline__ void add_term_checked(const Lane &a, Specials &sp, ui
   if (e == 0x7FFu) {
     record_special(sp, lo, hi, index);
   } else {
-    acc::add_term(a, lo, hi, e);
+    add_term(a, lo, hi, e);
   }
 }
 
@@ -657,170 +304,176 @@ __device__ __forceinline__ void ldg256(const double *p, uint32_t (&w)[8]) {
       : "l"(p));
 }
 
+template <int V>
 struct Batch {
-  uint32_t w[kVecPerLane][8];
+  uint32_t w[V][8];
 };
 
-// Load one batch: vectors v0 + u*32 + lane (u < kVecPerLane) of the 32-byte
-// vector array starting at X4; vectors at or beyond vend read as zero terms.
-__device__ __forceinline__ void load_batch(Batch &b, const double *X4, long long v0,
+// Load vector v0 + u*32 + lane (u < V) of the 32-byte vector array X4; vectors at
+// or beyond vend read as zero terms (which add nothing).
+template <int V>
+__device__ __forceinline__ void load_batch(Batch<V> &b, const double *X4, long long v0,
                                            long long vend, int lane) {
-  if (v0 + kVecPerLane * 32 <= vend) {
 #pragma unroll
-    for (int u = 0; u < kVecPerLane; ++u) ldg256(X4 + 4 * (v0 + u * 32 + lane), b.w[u]);
-  } else {
+  for (int u = 0; u < V; ++u) {
+    const long long v = v0 + u * 32 + lane;
 #pragma unroll
-    for (int u = 0; u < kVecPerLane; ++u) {
-      const long long v = v0 + u * 32 + lane;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) b.w[u][q] = 0u;
-      if (v < vend) ldg256(X4 + 4 * v, b.w[u]);
-    }
+    for (int q = 0; q < 8; ++q) b.w[u][q] = 0u;
+    if (v < vend) ldg256(X4 + 4 * v, b.w[u]);
   }
 }
 
-// Bulk L2 prefetch (cp.async.bulk.prefetch.L2) of one batch-sized stretch of
-// 32-byte vectors starting at vector v0, clipped to vend.  Issued by one lane a
-// few batches ahead of the register loads; costs no registers, no shared memory.
+// Bulk L2 prefetch (cp.async.bulk.prefetch.L2) of the batch-sized stretch of
+// 32-byte vectors starting at vector v0, clipped to vend.  One lane issues it a
+// batch ahead of the register loads; it costs no registers and no shared memory.
+template <int V>
 __device__ __forceinline__ void prefetch_l2(const double *X4, long long v0, long long vend) {
-#if EXSUM_PREFETCH_LANES
-  // per-lane variant: every lane prefetches the 256 B of its own vectors
-  (void)vend;
-  return;
-#endif
   if (v0 >= vend) return;
   long long nv = vend - v0;
-  if (nv > kVecPerLane * 32) nv = kVecPerLane * 32;
+  if (nv > V * 32) nv = V * 32;
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(X4 + 4 * v0),
                "r"(static_cast<uint32_t>(nv * 32))
                : "memory");
 }
 
-// Process one batch (kBatchTerms terms per lane).  index_of_vec0 is the
-// special-value index of term 0 of the batch's first vector.
-#if EXSUM_CHECK_GROUP > 0 && EXSUM_EXPERIMENT == 0
-// Grouped form: the Inf/NaN test and the adds run per group of G vectors, so the
-// first group is processed while the batch's later loads are still in flight.
-__device__ __forceinline__ void process_batch(const Lane &a, Pipe &pp, Specials &sp, Batch &b,
-                                              int lane, unsigned long long index_of_vec0) {
-  constexpr int G = EXSUM_CHECK_GROUP;
-  static_assert(kVecPerLane % G == 0, "group must divide the batch");
+// Inf/NaN fix-up of one batch (rare): the batch's terms were added blindly;
+// re-read the lane's terms, record each Inf/NaN by index and cancel its
+// (garbage) contribution with its sign-flipped twin — exact in the modular slot
+// arithmetic, and always before the next renormalisation.  Kept inline (an
+// out-of-line call forces the lane's Specials into local memory).
+//   kScan = false: compact loop, one L2 round trip per term (cold data only).
+//   kScan = true:  all high words loaded at once into a bitmask, then only the
+//                  flagged terms are re-read (data with frequent specials).
+template <int V, bool kScan>
+__device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, const double *X4,
+                                               long long v, long long nvec, int lane,
+                                               unsigned long long ib) {
+  const unsigned long long *xb = reinterpret_cast<const unsigned long long *>(X4);
+  if (kScan) {
+    static_assert(4 * V <= 32, "scan mask holds one batch");
+    const uint32_t *xh = reinterpret_cast<const uint32_t *>(X4);
+    uint32_t mask = 0u;
 #pragma unroll
-  for (int g = 0; g < kVecPerLane; g += G) {
-    uint32_t e[G][4];
-    uint32_t emax = 0;
-#pragma unroll
-    for (int u = 0; u < G; ++u)
+    for (int u = 0; u < V; ++u) {
+      const long long vec = v + u * 32 + lane;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        e[u][q] = exponent_field(b.w[g + u][2 * q + 1]);
-        emax = max(emax, e[u][q]);
+        const uint32_t hi = vec < nvec ? __ldcg(xh + 2 * (4 * vec + q) + 1) : 0u;
+        mask |= static_cast<uint32_t>(exponent_field(hi) == 0x7FFu) << (4 * u + q);
       }
-    if (emax == 0x7FFu) {  // rare: record Inf/NaN and turn them into zero terms
-#pragma unroll
-      for (int u = 0; u < G; ++u)
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (e[u][q] == 0x7FFu) {
-            record_special(sp, b.w[g + u][2 * q], b.w[g + u][2 * q + 1],
-                           index_of_vec0 + 4ull * static_cast<unsigned long long>((g + u) * 32 + lane) + q);
-            b.w[g + u][2 * q] = 0u;
-            b.w[g + u][2 * q + 1] = 0u;
-            e[u][q] = 0u;
-          }
     }
-#pragma unroll
-    for (int u = 0; u < G; ++u)
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        stream_term(a, pp, b.w[g + u][2 * q], b.w[g + u][2 * q + 1], e[u][q]);
+    while (mask) {
+      const int i = __ffs(mask) - 1;
+      mask &= mask - 1u;
+      const long long vec = v + (i >> 2) * 32 + lane;
+      const int q = i & 3;
+      const unsigned long long bits = __ldcg(xb + 4 * vec + q);
+      const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
+      record_special(sp, lo, hi, ib + 4ull * static_cast<unsigned long long>(vec) + q);
+      add_term(a, lo, hi ^ 0x80000000u, 0x7FFu);  // cancel the garbage add
+    }
+    return;
+  }
+#pragma unroll 1
+  for (int u = 0; u < V; ++u) {
+    const long long vec = v + u * 32 + lane;
+    if (vec >= nvec) break;
+#pragma unroll 1
+    for (int q = 0; q < 4; ++q) {
+      const unsigned long long bits = __ldcg(xb + 4 * vec + q);
+      const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
+      if (exponent_field(hi) == 0x7FFu) {
+        record_special(sp, lo, hi, ib + 4ull * static_cast<unsigned long long>(vec) + q);
+        add_term(a, lo, hi ^ 0x80000000u, 0x7FFu);  // cancel the garbage add
+      }
+    }
   }
 }
-#else
-__device__ __forceinline__ void process_batch(const Lane &a, Pipe &pp, Specials &sp, Batch &b,
-                                              int lane, unsigned long long index_of_vec0) {
-  uint32_t e[kVecPerLane][4];
-  bool special = false;
-#if EXSUM_DECODE == 2
-  // exponent fields; "any Inf/NaN" = (max exponent == 2047), 3-input max chains
+
+// Add one batch (registers b) with rolling refill from vector nv onward.  kGuard:
+// bounds-checked refills (only the last batches need it).  Returns the batch's
+// maximum exponent field (2047 iff it contained an Inf/NaN).
+template <int V, bool kGuard>
+__device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V> &b, const double *X4,
+                                                  long long nv, long long nvec, int lane) {
   uint32_t emax = 0;
+  const double *pn = X4 + 4 * (nv + lane);
 #pragma unroll
-  for (int u = 0; u < kVecPerLane; ++u)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      e[u][q] = exponent_field(b.w[u][2 * q + 1]);
-      emax = max(emax, e[u][q]);
-    }
-  special = emax == 0x7FFu;
-#else
-#pragma unroll
-  for (int u = 0; u < kVecPerLane; ++u)
+  for (int u = 0; u < V; ++u) {
+    uint32_t e[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-#if EXSUM_DECODE == 1
-      {
-        const uint32_t hw = b.w[u][2 * q + 1];
-        e[u][q] = __umulhi(hw, 4096u) + static_cast<uint32_t>(__mulhi(static_cast<int>(hw), 1)) * 2048u;
-      }
-#else
-      e[u][q] = exponent_field(b.w[u][2 * q + 1]);
-#endif
-      special |= e[u][q] == 0x7FFu;
+      e[q] = exponent_field(b.w[u][2 * q + 1]);
+      emax = max(emax, e[q]);
     }
-#endif
-  if (special) {  // rare: record Inf/NaN and turn them into zero terms
 #pragma unroll
-    for (int u = 0; u < kVecPerLane; ++u)
+    for (int q = 0; q < 4; ++q) add_term(a, b.w[u][2 * q], b.w[u][2 * q + 1], e[q]);
+    if (!kGuard || nv + u * 32 + lane < nvec) {
+      ldg256(pn + 4 * 32 * u, b.w[u]);
+    } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (e[u][q] == 0x7FFu) {
-          record_special(sp, b.w[u][2 * q], b.w[u][2 * q + 1],
-                         index_of_vec0 + 4ull * static_cast<unsigned long long>(u * 32 + lane) + q);
-          b.w[u][2 * q] = 0u;
-          b.w[u][2 * q + 1] = 0u;
-          e[u][q] = 0u;
-        }
+      for (int q = 0; q < 8; ++q) b.w[u][q] = 0u;
+    }
   }
-#if EXSUM_EXPERIMENT == 0
+  return emax;
+}
+
+// Register fast path: every lane's batch lies in slot k (|sum| < 2^89 per lane):
+// sum it in registers, then one read-modify-write.  Refills are unguarded.
+template <int V>
+__device__ __forceinline__ void batch_uniform(const Lane &a, Batch<V> &b, const double *X4,
+                                              long long nv, int lane, uint32_t k) {
+  const double *pn = X4 + 4 * (nv + lane);
+  uint32_t r0 = 0, r1 = 0, r2 = 0;
 #pragma unroll
-  for (int u = 0; u < kVecPerLane; ++u)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) stream_term(a, pp, b.w[u][2 * q], b.w[u][2 * q + 1], e[u][q]);
-#else
-  // Tuning experiments only (wrong sums): 1 = same per-term ALU work, register
-  // accumulation, one shared RMW per batch; 2 = loads only.
-  uint32_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-#pragma unroll
-  for (int u = 0; u < kVecPerLane; ++u)
+  for (int u = 0; u < V; ++u) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const uint32_t lo = b.w[u][2 * q], hi = b.w[u][2 * q + 1];
-#if EXSUM_EXPERIMENT == 1
-      const uint32_t ep = max(e[u][q], 1u);
-      const uint32_t imp = e[u][q] ? 0x100000u : 0u;
-      const uint32_t s = static_cast<uint32_t>(static_cast<int32_t>(hi) >> 31);
-      const uint32_t mx = ((hi & 0xFFFFFu) | imp) ^ s;
-      const uint32_t lx = lo ^ s;
-      const uint32_t w0 = __funnelshift_l(s, lx, ep), w1 = __funnelshift_l(lx, mx, ep);
-      const uint32_t w2 = __funnelshift_l(mx, s, ep);
-      asm("add.cc.u32 %0, %0, %4;\n\taddc.cc.u32 %1, %1, %5;\n\taddc.cc.u32 %2, %2, %6;\n\taddc.u32 %3, %3, %7;"
-          : "+r"(r0), "+r"(r1), "+r"(r2), "+r"(r3) : "r"(w0), "r"(w1), "r"(w2), "r"(ep));
-#else
-      r0 ^= lo;
-      r1 ^= hi;
-#endif
+      uint32_t sg, u0, u1, u2, ep;
+      decode96(b.w[u][2 * q], b.w[u][2 * q + 1], exponent_field(b.w[u][2 * q + 1]), sg, u0, u1,
+               u2, ep);
+      asm("{\n\t.reg .u32 cf;\n\tadd.cc.u32 cf, %3, %3;\n\taddc.cc.u32 %0, %0, %4;\n\t"
+          "addc.cc.u32 %1, %1, %5;\n\taddc.u32 %2, %2, %6;\n\t}"
+          : "+r"(r0), "+r"(r1), "+r"(r2)
+          : "r"(sg), "r"(u0), "r"(u1), "r"(u2));
     }
-  acc::add_term(a, r0 ^ r2, r1 ^ r3, 5u);
-#endif
+    ldg256(pn + 4 * 32 * u, b.w[u]);
+  }
+  slot_add96(a, k, r0, r1, r2);
 }
-#endif
+
+// One-slot test for a batch: the slot of a term is its top six exponent bits
+// (hi bits 25..30; e = 0 maps to slot 0 like e' = 1).  All terms share a slot
+// iff the AND and the OR of their high words agree on those bits; slot 63 may
+// hold Inf/NaN and never counts as uniform.  Returns the slot bits or ~0u.
+template <int V>
+__device__ __forceinline__ uint32_t uniform_slot(const Batch<V> &b) {
+  uint32_t hor = 0u, hand = 0xFFFFFFFFu;
+#pragma unroll
+  for (int u = 0; u < V; ++u)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      hor |= b.w[u][2 * q + 1];
+      hand &= b.w[u][2 * q + 1];
+    }
+  const uint32_t kbits = hor & 0x7E000000u;
+  return (kbits == (hand & 0x7E000000u) && kbits != 0x7E000000u) ? (kbits >> 25) : ~0u;
+}
 
 // Accumulate x[begin, end) into the calling warp's lane accumulators.
 // index_base is added to positions to form special-value indices; norm_count
 // counts batches since the last renormalisation (warp-uniform).
-__device__ void warp_accumulate(const double *__restrict__ x, unsigned long long begin,
-                                unsigned long long end, unsigned long long index_base,
-                                const Lane &a, Specials &sp, int &norm_count, int lane) {
+//   V:        vectors (4 terms) per lane per batch
+//   kUniform: register fast path for one-slot batches (larger code)
+//   kSplit:   separate unguarded steady-state body (larger code, fewer instrs)
+//   kScan:    scanning Inf/NaN fix-up (for data with frequent specials)
+template <int V, bool kUniform, bool kSplit, bool kScan>
+__device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
+                                                unsigned long long begin, unsigned long long end,
+                                                unsigned long long index_base, const Lane &a,
+                                                Specials &sp, int &norm_count, int lane) {
+  constexpr int kNormEvery = 2016 / (4 * V);  // batches between renormalisations
+  static_assert(kNormEvery >= 1, "batch too large for the carry budget");
   if (begin >= end) return;
   // Scalar head up to 32-byte alignment of &x[pos], scalar tail after the vectors.
   const uintptr_t addr = reinterpret_cast<uintptr_t>(x + begin);
@@ -842,214 +495,45 @@ __device__ void warp_accumulate(const double *__restrict__ x, unsigned long long
                      index_base + tail_t + lane);
   }
   if (nvec <= 0) return;
-  constexpr long long kStep = kVecPerLane * 32;
-#if EXSUM_ROLL
-  // Rolling single buffer: after a vector's four terms are added, its registers
-  // are immediately refilled with the same vector of the next batch, so every
-  // load is in flight for almost a whole batch without a second register set.
-  // Inf/NaN: terms are added unconditionally; if the batch's maximum exponent
-  // field is 2047 the batch is re-read and each Inf/NaN term is recorded and
-  // its (garbage) contribution cancelled by adding its sign-flipped twin — exact
-  // in the modular slot arithmetic, and before any renormalisation.
-  Batch b0;
+  constexpr long long kStep = V * 32;
   const unsigned long long ib = index_base + vbeg_t;
   if (lane == 0) {
-    for (int d = 0; d <= kPrefetchBatches; ++d) prefetch_l2(X4, d * kStep, nvec);
+    for (int d = 0; d <= kPrefetchBatches; ++d) prefetch_l2<V>(X4, d * kStep, nvec);
   }
-  load_batch(b0, X4, 0, nvec, lane);
+  Batch<V> b;
+  load_batch<V>(b, X4, 0, nvec, lane);
   int backoff = 0;
   for (long long v = 0; v < nvec; v += kStep) {
     const long long nv = v + kStep;
-    if (lane == 0) prefetch_l2(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
+    if (lane == 0) prefetch_l2<V>(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
     uint32_t emax = 0;
-    if (nv + kStep <= nvec) {
-      // steady state: the next batch is complete, unguarded loads at immediate
-      // offsets from one pointer
-      const double *pn = X4 + 4 * (nv + lane);
-#if EXSUM_UNIFORM_FAST
-      // Slot of a term = top six exponent bits (hi bits 25..30; e = 0 maps to
-      // slot 0 like e' = 1).  All terms of the batch share a slot iff the AND and
-      // the OR of their high words agree on those bits: 3-input LOP3 chains, no
-      // per-term exponent kept live.  Slot 63 may hold Inf/NaN: never "uniform".
-      // Wide data rarely turns uniform: after a non-uniform batch the test is
-      // skipped for the next kUniformBackoff batches (warp-uniform counter).
-      bool fast = false;
-      uint32_t kbits = 0u;
+    const bool steady = nv + kStep <= nvec;  // next batch complete: unguarded refills
+    uint32_t k = ~0u;
+    if (kUniform && steady) {
       if (backoff > 0) {
         --backoff;
       } else {
-        uint32_t hor = 0u, hand = 0xFFFFFFFFu;
-#pragma unroll
-        for (int u = 0; u < kVecPerLane; ++u)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            hor |= b0.w[u][2 * q + 1];
-            hand &= b0.w[u][2 * q + 1];
-          }
-        kbits = hor & 0x7E000000u;
-        const bool uniform = kbits == (hand & 0x7E000000u) && kbits != 0x7E000000u;
-        fast = __all_sync(0xffffffffu, uniform);
-        if (!fast) backoff = kUniformBackoff;
-      }
-      if (fast) {
-        // every lane's batch lies in one slot: sum it in registers (|sum| < 2^89),
-        // then one read-modify-write of that slot
-        uint32_t r0 = 0, r1 = 0, r2 = 0;
-#pragma unroll
-        for (int u = 0; u < kVecPerLane; ++u) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint32_t sg, u0, u1, u2, ep;
-            acc::decode96(b0.w[u][2 * q], b0.w[u][2 * q + 1], exponent_field(b0.w[u][2 * q + 1]),
-                          sg, u0, u1, u2, ep);
-            asm("{\n\t.reg .u32 cf;\n\tadd.cc.u32 cf, %3, %3;\n\taddc.cc.u32 %0, %0, %4;\n\t"
-                "addc.cc.u32 %1, %1, %5;\n\taddc.u32 %2, %2, %6;\n\t}"
-                : "+r"(r0), "+r"(r1), "+r"(r2)
-                : "r"(sg), "r"(u0), "r"(u1), "r"(u2));
-          }
-          ldg256(pn + 4 * 32 * u, b0.w[u]);
-        }
-        acc::slot_add96(a, kbits >> 25, r0, r1, r2);
-      } else {
-#pragma unroll
-        for (int u = 0; u < kVecPerLane; ++u) {
-          uint32_t e[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            e[q] = exponent_field(b0.w[u][2 * q + 1]);
-            emax = max(emax, e[q]);
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc::add_term(a, b0.w[u][2 * q], b0.w[u][2 * q + 1], e[q]);
-          ldg256(pn + 4 * 32 * u, b0.w[u]);
+        k = uniform_slot<V>(b);
+        if (!__all_sync(0xffffffffu, k != ~0u)) {
+          k = ~0u;
+          backoff = kUniformBackoff;  // wide data rarely turns uniform
         }
       }
-#else
-#pragma unroll
-      for (int u = 0; u < kVecPerLane; ++u) {
-        uint32_t e[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          e[q] = exponent_field(b0.w[u][2 * q + 1]);
-          emax = max(emax, e[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc::add_term(a, b0.w[u][2 * q], b0.w[u][2 * q + 1], e[q]);
-        ldg256(pn + 4 * 32 * u, b0.w[u]);
-      }
-#endif
+    }
+    if (k != ~0u) {
+      batch_uniform<V>(a, b, X4, nv, lane, k);
+    } else if (kSplit && steady) {
+      emax = batch_rolling<V, false>(a, b, X4, nv, nvec, lane);
     } else {
-#pragma unroll
-      for (int u = 0; u < kVecPerLane; ++u) {
-        uint32_t e[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          e[q] = exponent_field(b0.w[u][2 * q + 1]);
-          emax = max(emax, e[q]);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) acc::add_term(a, b0.w[u][2 * q], b0.w[u][2 * q + 1], e[q]);
-        const long long vv = nv + u * 32 + lane;
-        if (vv < nvec) {
-          ldg256(X4 + 4 * vv, b0.w[u]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 8; ++q) b0.w[u][q] = 0u;
-        }
-      }
+      emax = batch_rolling<V, true>(a, b, X4, nv, nvec, lane);
     }
-    if (__builtin_expect(emax == 0x7FFu, 0)) {
-      const unsigned long long *xb = reinterpret_cast<const unsigned long long *>(X4);
-      for (int u = 0; u < kVecPerLane; ++u) {
-        const long long vec = v + u * 32 + lane;
-        if (vec >= nvec) break;
-        for (int q = 0; q < 4; ++q) {
-          const unsigned long long bits = __ldcg(xb + 4 * vec + q);
-          const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
-          if (exponent_field(hi) == 0x7FFu) {
-            record_special(sp, lo, hi, ib + 4ull * static_cast<unsigned long long>(vec) + q);
-            acc::add_term(a, lo, hi ^ 0x80000000u, 0x7FFu);  // cancel the garbage add
-          }
-        }
-      }
-    }
+    if (__builtin_expect(emax == 0x7FFu, 0))
+      fixup_specials<V, kScan>(a, sp, X4, v, nvec, lane, ib);
     if (++norm_count >= kNormEvery) {
-      acc::normalize(a);
+      normalize(a);
       norm_count = 0;
     }
   }
-#elif EXSUM_BUFFERS == 1
-  // Single register buffer: the L2 bulk prefetch (kPrefetchBatches ahead) hides
-  // DRAM latency, the register load only waits for L2; frees 32-64 registers
-  // for instruction-level parallelism.
-  Batch b0;
-  const unsigned long long ib = index_base + vbeg_t;
-  if (lane == 0) {
-    for (int d = 0; d <= kPrefetchBatches; ++d) prefetch_l2(X4, d * kStep, nvec);
-  }
-  Pipe pp;
-  stream_begin(a, pp);
-  for (long long v = 0; v < nvec; v += kStep) {
-    load_batch(b0, X4, v, nvec, lane);
-#if EXSUM_PREFETCH_LANES
-    {
-      const long long pv = v + (kPrefetchBatches + 1) * kStep;
-#pragma unroll
-      for (int u = 0; u < kVecPerLane; u += 4) {
-        const long long q = pv + u * 32 + lane * 4;  // 4 consecutive vectors = 128 B
-        if (q < nvec) asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(X4 + 4 * q));
-      }
-    }
-#else
-    if (lane == 0) prefetch_l2(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
-#endif
-    process_batch(a, pp, sp, b0, lane, ib + 4ull * static_cast<unsigned long long>(v));
-    if (++norm_count >= kNormEvery) {
-      stream_end(a, pp);
-      acc::normalize(a);
-      stream_begin(a, pp);
-      norm_count = 0;
-    }
-  }
-  stream_end(a, pp);
-#else
-  Batch b0, b1;
-  long long v = 0;
-  if (kPrefetchBatches > 0 && lane == 0) {
-    for (int d = 1; d <= kPrefetchBatches; ++d) prefetch_l2(X4, d * kStep, nvec);
-  }
-  load_batch(b0, X4, 0, nvec, lane);
-  const unsigned long long ib = index_base + vbeg_t;
-  Pipe pp;
-  stream_begin(a, pp);
-  while (true) {
-    long long nx = v + kStep;
-    if (kPrefetchBatches > 0 && lane == 0) prefetch_l2(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
-    if (nx < nvec) load_batch(b1, X4, nx, nvec, lane);
-    process_batch(a, pp, sp, b0, lane, ib + 4ull * static_cast<unsigned long long>(v));
-    if (++norm_count >= kNormEvery) {
-      stream_end(a, pp);
-      acc::normalize(a);
-      stream_begin(a, pp);
-      norm_count = 0;
-    }
-    v = nx;
-    if (v >= nvec) break;
-    nx = v + kStep;
-    if (kPrefetchBatches > 0 && lane == 0) prefetch_l2(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
-    if (nx < nvec) load_batch(b0, X4, nx, nvec, lane);
-    process_batch(a, pp, sp, b1, lane, ib + 4ull * static_cast<unsigned long long>(v));
-    if (++norm_count >= kNormEvery) {
-      stream_end(a, pp);
-      acc::normalize(a);
-      stream_begin(a, pp);
-      norm_count = 0;
-    }
-    v = nx;
-    if (v >= nvec) break;
-  }
-  stream_end(a, pp);
-#endif
 }
 
 __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
@@ -1061,8 +545,9 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
   return v;
 }
 
-// Warp-parallel finalisation (all 32 lanes of one warp): the same canonical form
-// and rounding as emit_record / exsum_core.h, without a 67-step serial chain.
+// Warp-parallel finalisation (all 32 lanes of one warp): the canonical form and
+// rounding of exsum_core.h (SmallAccumulator::carry_propagate + round,
+// small_accumulator.cpp:244-348) without a 67-step serial chain:
 //   1. carry propagation by repeated shuffle passes until no lane holds a carry
 //      (two or three passes for accumulated chunk sums);
 //   2. canonical top / fold of a -1 top chunk via ballots;
@@ -1245,19 +730,20 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
   const unsigned long long tb = qb * 4, te = min(qe * 4, n);
   if (lane == 0 && te > tb) {  // start the first batches' DRAM reads before zeroing smem
     const uintptr_t p0 = reinterpret_cast<uintptr_t>(x + tb) & ~uintptr_t{15};
-    const uintptr_t p1 = reinterpret_cast<uintptr_t>(x + min(te, tb + 2ull * kBatchTerms * 32));
+    const uintptr_t p1 = reinterpret_cast<uintptr_t>(x + min(te, tb + 2ull * 4 * EXSUM_VEC_PER_LANE * 32));
     const uint32_t bytes = static_cast<uint32_t>((p1 - p0 + 15) & ~uintptr_t{15});
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"(bytes) : "memory");
   }
   zero_warp(wsm, lane);
   __syncwarp();
-  const Lane a = acc::lane_view(wsm, lane);
+  const Lane a = lane_view(wsm, lane);
   Specials sp{~0ull, ~0ull, ~0ull};
   int norm_count = 0;
-  warp_accumulate(x, tb, te, base_index, a, sp, norm_count, lane);
+  warp_accumulate<EXSUM_VEC_PER_LANE, EXSUM_UNIFORM_FAST != 0, true, false>(
+      x, tb, te, base_index, a, sp, norm_count, lane);
 
   // K2: the warp's 67 chunk sums.
-  acc::warp_chunks(wsm, a, lane, scratch + warp * kChunks);
+  warp_chunks(wsm, lane, scratch + warp * kChunks);
   const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                            N = warp_min_u64(sp.N);
   // The workspace is shared with the previous sum in the stream: wait for that
@@ -1336,7 +822,7 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
   const int warp = threadIdx.x >> 5;
   unsigned char *wsm = smem + warp * kWarpSmem;
   long long *row = reinterpret_cast<long long *>(smem + kWarps * kWarpSmem) + warp * kChunks;
-  const Lane a = acc::lane_view(wsm, lane);
+  const Lane a = lane_view(wsm, lane);
   while (true) {
     unsigned int s = 0;
     if (lane == 0) s = atomicAdd(&ws->seg_next, 1u);
@@ -1348,8 +834,8 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
     Specials sp{~0ull, ~0ull, ~0ull};
     int norm_count = 0;
     // indices local to the segment: position - b
-    warp_accumulate(x, b, e, 0ull - b, a, sp, norm_count, lane);
-    acc::warp_chunks(wsm, a, lane, row);
+    warp_accumulate<EXSUM_SEG_VEC, false, EXSUM_SEG_SPLIT != 0, true>(x, b, e, 0ull - b, a, sp, norm_count, lane);
+    warp_chunks(wsm, lane, row);
     const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                              N = warp_min_u64(sp.N);
     __syncwarp();

@@ -164,10 +164,11 @@ __global__ void gen_kernel(int config, uint64_t seed, uint64_t n_total, uint64_t
 __constant__ double c_pow10[601];
 bool g_pow10_ready = false;
 
-__global__ void gen5_kernel(uint64_t seed, uint64_t count, double *out) {
+__global__ void gen5_kernel(uint64_t seed, uint64_t first, uint64_t count, double *out) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
-       i += stride) {
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < count;
+       t += stride) {
+    const uint64_t i = first + t;
     const uint64_t h = draw(seed, 51, i);
     double v;
     if ((h >> 11) < 900719925474ull) {  // 1e-4 * 2^53
@@ -181,7 +182,7 @@ __global__ void gen5_kernel(uint64_t seed, uint64_t count, double *out) {
       const int k = static_cast<int>(draw(seed, 55, i) % 601);
       v = z * c_pow10[k];
     }
-    out[i] = v;
+    out[t] = v;
   }
 }
 
@@ -230,8 +231,9 @@ int exsum_host_gen_offsets(uint64_t seed, size_t nseg, uint64_t lo, uint64_t hi,
   return EXSUM_OK;
 }
 
-int exsum_cuda_gen_segmented(uint64_t seed, uint64_t n_total, double *d_out, void *stream) {
-  if (n_total && !d_out) return EXSUM_EINVAL;
+int exsum_cuda_gen_segmented(uint64_t seed, uint64_t first, size_t count, double *d_out,
+                             void *stream) {
+  if (count && !d_out) return EXSUM_EINVAL;
   if (!g_pow10_ready) {
     double p[601];
     char buf[16];
@@ -242,9 +244,9 @@ int exsum_cuda_gen_segmented(uint64_t seed, uint64_t n_total, double *d_out, voi
     if (cudaMemcpyToSymbol(c_pow10, p, sizeof p) != cudaSuccess) return EXSUM_ECUDA;
     g_pow10_ready = true;
   }
-  if (n_total == 0) return EXSUM_OK;
-  gen5_kernel<<<gen_grid(n_total), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, n_total,
-                                                                               d_out);
+  if (count == 0) return EXSUM_OK;
+  gen5_kernel<<<gen_grid(count), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, first, count,
+                                                                             d_out);
   return cudaGetLastError() == cudaSuccess ? EXSUM_OK : EXSUM_ECUDA;
 }
 

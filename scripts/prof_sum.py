@@ -24,7 +24,7 @@ if config == 5:
     _lib.call("exsum_host_gen_offsets", 1, nseg, 1000, 100000, offs.ctypes.data)
     total = int(offs[-1])
     x = torch.empty(total, dtype=torch.float64, device=dev)
-    _lib.call("exsum_cuda_gen_segmented", 1, total, x.data_ptr(), stream)
+    _lib.call("exsum_cuda_gen_segmented", 1, 0, total, x.data_ptr(), stream)
     o = torch.from_numpy(offs.astype(np.int64)).to(dev)
     for _ in range(reps):
         out = ops.exact_sum_segmented(x, o)

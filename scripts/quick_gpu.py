@@ -70,7 +70,7 @@ offs = np.zeros(1001, dtype=np.uint64)
 offs[1:] = np.cumsum(rng.integers(0, 5000, size=1000))
 N = int(offs[-1])
 xs = torch.empty(N, dtype=torch.float64, device=dev)
-_lib.call("exsum_cuda_gen_segmented", 3, N, xs.data_ptr(), torch.cuda.current_stream().cuda_stream)
+_lib.call("exsum_cuda_gen_segmented", 3, 0, N, xs.data_ptr(), torch.cuda.current_stream().cuda_stream)
 out = ops.exact_sum_segmented(xs, torch.from_numpy(offs.astype(np.int64)).to(dev))
 want = ref.segmented_sum(xs.cpu().numpy(), offs)
 segbad = int((out.cpu().numpy().view(np.uint64) != want.view(np.uint64)).sum())

@@ -17,6 +17,27 @@ from paper_1505_05571_b200 import _lib, ops
 dev = torch.device("cuda", 0)
 out = {}
 for config, n, K in %s:
+    if config == 5:
+        offs = np.zeros(n + 1, dtype=np.uint64)
+        _lib.call("exsum_host_gen_offsets", 1, n, 1000, 100000, offs.ctypes.data)
+        tot = int(offs[-1])
+        x = torch.empty(tot, dtype=torch.float64, device=dev)
+        _lib.call("exsum_cuda_gen_segmented", 1, 0, tot, x.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        o = torch.from_numpy(offs.astype(np.int64)).to(dev)
+        ws = ops.Workspace(dev)
+        for _ in range(3):
+            r = ops.exact_sum_segmented(x, o, workspace=ws)
+        torch.cuda.synchronize()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        for _ in range(K):
+            r = ops.exact_sum_segmented(x, o, workspace=ws)
+        en.record(); torch.cuda.synchronize()
+        ms = st.elapsed_time(en) / K
+        h = int(np.bitwise_xor.reduce(r.cpu().numpy().view(np.uint64)))
+        out[config] = (ms, 8 * tot / ms / 1e6, h)
+        del x; torch.cuda.empty_cache()
+        continue
     x = torch.empty(n, dtype=torch.float64, device=dev)
     _lib.call("exsum_cuda_gen", config, 1, n, 0, n, x.data_ptr(), torch.cuda.current_stream().cuda_stream)
     res = torch.empty(1, dtype=torch.float64, device=dev)
@@ -36,7 +57,10 @@ for config, n, K in %s:
 print("RESULT", json.dumps(out))
 '''
 
-cases = [(2, 100_000_000, 20), (3, 100_000_000, 20), (4, 1_000_000_000, 5)]
+cases = [(2, 100_000_000, 20), (3, 100_000_000, 20), (4, 1_000_000_000, 5), (5, 65_536, 5)]
+if os.environ.get("TV_CONFIGS"):
+    keep = {int(c) for c in os.environ["TV_CONFIGS"].split(",")}
+    cases = [c for c in cases if c[0] in keep]
 variants = sys.argv[1:] or sorted(p.stem for p in (ROOT / "paper_1505_05571_b200/lib/variants").glob("*.so"))
 variants = ["default"] + [v for v in variants if v != "default"]
 for v in variants:

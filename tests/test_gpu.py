@@ -204,7 +204,7 @@ def test_config5_segmented(cuda, checker):
         _lib.call("exsum_host_gen_offsets", seed, nseg, 1000, 100_000, offs.ctypes.data)
         total = int(offs[-1])
         x = torch.empty(total, dtype=torch.float64, device="cuda")
-        _lib.call("exsum_cuda_gen_segmented", seed, total, x.data_ptr(), stream())
+        _lib.call("exsum_cuda_gen_segmented", seed, 0, total, x.data_ptr(), stream())
         out = ops.exact_sum_segmented(x, torch.from_numpy(offs.astype(np.int64)).cuda())
         got = out.cpu().numpy().view(np.uint64)
         want = checker.segmented_sum(x.cpu().numpy(), offs).view(np.uint64)
