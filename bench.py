@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--nccl", action="store_true",
+                   help="use the exsum_nccl_sum step even at N=1 (1-rank communicator)")
     return p.parse_args()
 
 
@@ -375,7 +377,7 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1505_05571_b200 import _lib, ops
-    from paper_1505_05571_b200.distributed import exchange_partials, shard_bounds
+    from paper_1505_05571_b200.distributed import NcclCommunicator, nccl_exact_sum, shard_bounds
 
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -393,16 +395,19 @@ def main():
     res = torch.empty(1, dtype=torch.float64, device=dev)
     part = torch.empty(ops.PARTIAL_BYTES, dtype=torch.uint8, device=dev)
 
-    # Back-to-back steps launch with programmatic dependent launch (EXSUM_SUM_OVERLAP):
-    # step i+1's CTAs start streaming on SMs released by step i while step i's last
-    # CTA rounds.  Every step is still one complete exact sum of the whole array.
-    overlap = world == 1
+    # N = 1: back-to-back steps launch with programmatic dependent launch
+    # (EXSUM_SUM_OVERLAP): step i+1's CTAs start streaming on SMs released by step i
+    # while step i's last CTA rounds.  Every step is still one complete exact sum.
+    # N > 1: one exsum_nccl_sum per step — shard sum kernel, ncclAllGather of the
+    # 592-byte records, merge kernel — inside the C library (the C-ABI form of
+    # parallel_exact_sum); every rank ends with the full array's exact sum.
+    comm = NcclCommunicator(dev) if (world > 1 or args.nccl) else None
 
     def step():
+        if comm is not None:
+            return nccl_exact_sum(x, comm, base_index=begin, result=res)
         ops.exact_sum_tensor(x, base_index=begin, result=res, partial=part, workspace=ws,
-                             overlap=overlap)
-        if world > 1:
-            return ops.merge_partials(exchange_partials(part))[0]
+                             overlap=True)
         return res
 
     for _ in range(max(args.warmup, 3)):
@@ -432,7 +437,7 @@ def main():
     # dominant kernel: average duration per launch over the timed region (for N = 1
     # the step IS the sum kernel; launches overlap their epilogues, so per-launch
     # events would serialise them).  For N > 1 the kernel is timed in its own loop.
-    if world == 1:
+    if comm is None:
         k_ms = ms / steps
     else:
         ks, ke = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -512,7 +517,7 @@ def main():
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded counter-based generator, BASELINE.json shapes)",
             "config": {"workload": wl["desc"], "n_total": n_total, "n_per_gpu": n_local,
-                       "parallelism": f"shard{world}" + (" + NCCL all-gather of 592 B records" if world > 1 else ""),
+                       "parallelism": f"shard{world}" + (" + exsum_nccl_sum (ncclAllGather of 592 B records + merge kernel)" if comm is not None else ""),
                        "l2": "inputs >= 800 MB per GPU > 126 MB L2; no flush needed"},
             "terms_per_s": round(value * 1e9 / 8, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
@@ -522,12 +527,14 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": steps * (2 if world > 1 else 1),
+            "gpu_launches": steps * (2 if comm is not None else 1),
             "clocks": clocks.report(),
             "result_bits": hex(result_bits),
             "bit_exact_vs_oracle": parity,
         }
         print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 

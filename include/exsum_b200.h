@@ -32,6 +32,7 @@ extern "C" {
 #define EXSUM_EINVAL 1 /* bad argument (mean with n == 0, null pointer, length mismatch) */
 #define EXSUM_ECUDA 2  /* a CUDA runtime call failed (no device, launch failure, ...) */
 #define EXSUM_ENOMEM 3 /* allocation failed / workspace too small */
+#define EXSUM_ENCCL 4  /* NCCL unavailable or an NCCL call failed */
 
 /* -------------------------------------------------------------- geometry */
 /* small_accumulator.hpp:27-35 and large_accumulator.hpp:27-29 */
@@ -172,6 +173,35 @@ exsum_context *exsum_context_create(int device, size_t staging_bytes);
 void exsum_context_free(exsum_context *ctx);
 int exsum_context_sum(exsum_context *ctx, const double *h_x, size_t n, double *h_result,
                       exsum_partial *h_partial);
+
+/* ------------------------------------------ multi-GPU (NCCL over NVLink) */
+/* parallel_exact_sum (vector_ops.cpp:172-186) with one shard per GPU (one
+ * process per GPU).  split (vector_ops.cpp:37-49) gives each rank a contiguous
+ * shard; the rank reduces it to one exsum_partial record, the records are
+ * exchanged with ONE ncclAllGather (nranks x 592 B) and every rank merges them
+ * (merge_partials, vector_ops.cpp:64-70, with index-ordered Inf/NaN), so every
+ * rank holds the serial exact_sum bits.  NCCL is loaded on first use
+ * (libnccl.so.2 already in the process, else EXSUM_NCCL_LIB, else the system
+ * one); `comm` is an ncclComm_t passed as void*, e.g. one the caller already
+ * owns or one from exsum_nccl_comm_init. */
+#define EXSUM_NCCL_UNIQUE_ID_BYTES 128 /* sizeof(ncclUniqueId) */
+/* split(n, parts)[rank] — vector_ops.cpp:37-49 (remainder to the first shards). */
+int exsum_shard_bounds(uint64_t n, int nranks, int rank, uint64_t *begin, uint64_t *end);
+/* 1 if NCCL can be loaded (and its version in *version if non-NULL), else 0. */
+int exsum_nccl_available(int *version);
+int exsum_nccl_get_unique_id(void *id /* EXSUM_NCCL_UNIQUE_ID_BYTES */);
+/* ncclCommInitRank on the current CUDA device. */
+int exsum_nccl_comm_init(void **comm, int nranks, const void *id, int rank);
+int exsum_nccl_comm_destroy(void *comm);
+/* Workspace of exsum_nccl_sum for a communicator of nranks ranks (device memory;
+ * zero it once with exsum_cuda_workspace_init, every call leaves it zeroed). */
+size_t exsum_nccl_workspace_bytes(int nranks);
+/* This rank's shard d_shard[0..n) = logical indices [base_index, base_index + n):
+ * sum kernel -> ncclAllGather of the records -> merge kernel, stream-ordered and
+ * graph-capturable.  Outputs (either may be NULL) are identical on every rank. */
+int exsum_nccl_sum(const double *d_shard, size_t n, uint64_t base_index, void *comm,
+                   double *d_result, exsum_partial *d_partial, void *d_ws, size_t ws_bytes,
+                   void *stream);
 
 /* --------------------------------------------------- synthetic data (bench) */
 /* Seeded counter-based generators for the BASELINE.json configs (SURVEY.md

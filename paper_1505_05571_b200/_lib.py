@@ -13,12 +13,13 @@ from pathlib import Path
 LIB_PATH = Path(os.environ.get("EXSUM_LIB") or
                 Path(__file__).resolve().parent / "lib" / "libexsum_b200.so")
 
-EXSUM_OK, EXSUM_EINVAL, EXSUM_ECUDA, EXSUM_ENOMEM = 0, 1, 2, 3
+EXSUM_OK, EXSUM_EINVAL, EXSUM_ECUDA, EXSUM_ENOMEM, EXSUM_ENCCL = 0, 1, 2, 3, 4
+NCCL_UNIQUE_ID_BYTES = 128
 SMALL_CHUNKS = 67
 NO_INDEX = (1 << 64) - 1
 
 _STATUS_NAMES = {EXSUM_EINVAL: "EXSUM_EINVAL", EXSUM_ECUDA: "EXSUM_ECUDA",
-                 EXSUM_ENOMEM: "EXSUM_ENOMEM"}
+                 EXSUM_ENOMEM: "EXSUM_ENOMEM", EXSUM_ENCCL: "EXSUM_ENCCL"}
 
 
 class ExsumSmall(C.Structure):
@@ -92,6 +93,13 @@ _SIGNATURES = {
     "exsum_cuda_finalize": (_i32, [_vp, _vp, _vp, _sz, _vp]),
     "exsum_cuda_sum_segmented": (_i32, [_vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp]),
     "exsum_cuda_merge": (_i32, [_vp, _sz, _vp, _vp, _vp]),
+    "exsum_shard_bounds": (_i32, [_u64, _i32, _i32, C.POINTER(_u64), C.POINTER(_u64)]),
+    "exsum_nccl_available": (_i32, [C.POINTER(_i32)]),
+    "exsum_nccl_get_unique_id": (_i32, [_vp]),
+    "exsum_nccl_comm_init": (_i32, [C.POINTER(_vp), _i32, _vp, _i32]),
+    "exsum_nccl_comm_destroy": (_i32, [_vp]),
+    "exsum_nccl_workspace_bytes": (_sz, [_i32]),
+    "exsum_nccl_sum": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "exsum_context_create": (_vp, [_i32, _sz]),
     "exsum_context_free": (None, [_vp]),
     "exsum_context_sum": (_i32, [_vp, _vp, _sz, _dp, _pp]),

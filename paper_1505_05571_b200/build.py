@@ -23,7 +23,7 @@ LIB = PKG / "lib" / "libexsum_b200.so"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = "/usr/bin/g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["sum_kernels.cu", "synth.cu", "context.cu"]
+CU_SOURCES = ["sum_kernels.cu", "synth.cu", "context.cu", "nccl_sum.cu"]
 CXX_SOURCES = ["host_accumulators.cpp"]
 HEADERS = [CSRC / "exsum_core.h", INCLUDE / "exsum_b200.h"]
 
@@ -66,7 +66,7 @@ def build(verbose: bool = False, force: bool = False, defines: tuple[str, ...] =
                   "-c", str(CSRC / src), "-o", str(obj)], verbose)
     if force or _stale(lib, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs),
-              "-Xcompiler", "-fopenmp", "-lgomp"], verbose)
+              "-Xcompiler", "-fopenmp", "-lgomp", "-ldl"], verbose)
     return lib
 
 

@@ -349,7 +349,7 @@ __device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, cons
                                                long long v, long long nvec, int lane,
                                                unsigned long long ib) {
   const unsigned long long *xb = reinterpret_cast<const unsigned long long *>(X4);
-  if (kScan) {
+  if constexpr (kScan) {
     static_assert(4 * V <= 32, "scan mask holds one batch");
     const uint32_t *xh = reinterpret_cast<const uint32_t *>(X4);
     uint32_t mask = 0u;
@@ -372,19 +372,19 @@ __device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, cons
       record_special(sp, lo, hi, ib + 4ull * static_cast<unsigned long long>(vec) + q);
       add_term(a, lo, hi ^ 0x80000000u, 0x7FFu);  // cancel the garbage add
     }
-    return;
-  }
+  } else {
 #pragma unroll 1
-  for (int u = 0; u < V; ++u) {
-    const long long vec = v + u * 32 + lane;
-    if (vec >= nvec) break;
+    for (int u = 0; u < V; ++u) {
+      const long long vec = v + u * 32 + lane;
+      if (vec >= nvec) break;
 #pragma unroll 1
-    for (int q = 0; q < 4; ++q) {
-      const unsigned long long bits = __ldcg(xb + 4 * vec + q);
-      const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
-      if (exponent_field(hi) == 0x7FFu) {
-        record_special(sp, lo, hi, ib + 4ull * static_cast<unsigned long long>(vec) + q);
-        add_term(a, lo, hi ^ 0x80000000u, 0x7FFu);  // cancel the garbage add
+      for (int q = 0; q < 4; ++q) {
+        const unsigned long long bits = __ldcg(xb + 4 * vec + q);
+        const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
+        if (exponent_field(hi) == 0x7FFu) {
+          record_special(sp, lo, hi, ib + 4ull * static_cast<unsigned long long>(vec) + q);
+          add_term(a, lo, hi ^ 0x80000000u, 0x7FFu);  // cancel the garbage add
+        }
       }
     }
   }

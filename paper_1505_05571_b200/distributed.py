@@ -26,7 +26,8 @@ from . import _lib
 from ._lib import ExsumPartial
 from .ops import PARTIAL_BYTES, exact_sum_tensor, merge_partials, partial_from_tensor
 
-__all__ = ["shard_bounds", "exchange_partials", "merge_records", "parallel_exact_sum"]
+__all__ = ["shard_bounds", "exchange_partials", "merge_records", "parallel_exact_sum",
+           "NcclCommunicator", "nccl_exact_sum"]
 
 
 def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -76,3 +77,68 @@ def parallel_exact_sum(shard: torch.Tensor, *, base_index: int, group=None) -> t
 
 def record_to_partial(rec: torch.Tensor) -> ExsumPartial:
     return partial_from_tensor(rec)
+
+
+class NcclCommunicator:
+    """The library's own NCCL communicator (exsum_nccl_comm_init) for the ranks
+    of a torch.distributed group (any backend: gloo suffices to ship the unique
+    id).  One per process/device; ``workspace`` is the exsum_nccl_sum scratch.
+
+    exsum_nccl_sum runs sum kernel -> ncclAllGather of the 592-byte records ->
+    merge kernel inside the C library: the C-ABI form of parallel_exact_sum
+    (vector_ops.cpp:172-186) that a non-Python caller would use."""
+
+    def __init__(self, device: torch.device, group=None):
+        single = not dist.is_initialized()  # one process, no group: a 1-rank communicator
+        self.rank = 0 if single else dist.get_rank(group)
+        self.world = 1 if single else dist.get_world_size(group)
+        self.device = torch.device(device)
+        uid = bytearray(_lib.NCCL_UNIQUE_ID_BYTES)
+        if self.rank == 0:
+            buf = (C.c_char * _lib.NCCL_UNIQUE_ID_BYTES)()
+            _lib.call("exsum_nccl_get_unique_id", buf)
+            uid = bytearray(buf.raw)
+        box = [bytes(uid)]
+        if not single:
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0,
+                                       group=group)
+        idbuf = (C.c_char * _lib.NCCL_UNIQUE_ID_BYTES).from_buffer_copy(box[0])
+        comm = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.call("exsum_nccl_comm_init", C.byref(comm), self.world, idbuf, self.rank)
+        self.comm = comm
+        nbytes = int(_lib.lib.exsum_nccl_workspace_bytes(self.world))
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.call("exsum_cuda_workspace_init", self.workspace.data_ptr(), nbytes,
+                      torch.cuda.current_stream(self.device).cuda_stream)
+
+    def close(self) -> None:
+        if self.comm:
+            _lib.call("exsum_nccl_comm_destroy", self.comm)
+            self.comm = C.c_void_p()
+
+    def __del__(self):  # best effort; explicit close() preferred
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_exact_sum(shard: torch.Tensor, comm: NcclCommunicator, *, base_index: int,
+                   result: torch.Tensor | None = None,
+                   record: torch.Tensor | None = None) -> torch.Tensor:
+    """exsum_nccl_sum: exact sum of the logical array of which ``shard`` holds
+    [base_index, base_index + len).  Returns the 1-element float64 result
+    (identical bits on every rank); ``record`` (592 B uint8) receives the merged
+    canonical record if given."""
+    if not shard.is_cuda or shard.dtype != torch.float64:
+        raise ValueError("nccl_exact_sum: shard must be a CUDA float64 tensor")
+    x = shard.contiguous()
+    if result is None:
+        result = torch.empty(1, dtype=torch.float64, device=x.device)
+    stream = torch.cuda.current_stream(x.device).cuda_stream
+    _lib.call("exsum_nccl_sum", x.data_ptr() if x.numel() else None, x.numel(), base_index,
+              comm.comm, result.data_ptr(), record.data_ptr() if record is not None else None,
+              comm.workspace.data_ptr(), comm.workspace.numel(), stream)
+    return result

@@ -83,3 +83,34 @@ def test_gloo_world2_exchange_and_merge(golden):
         assert p.exitcode == 0
     for r in range(world):
         assert results[r] == want
+
+
+def test_c_shard_bounds_matches_split():
+    """exsum_shard_bounds (C ABI) == split (vector_ops.cpp:37-49) == shard_bounds."""
+    b, e = C.c_uint64(), C.c_uint64()
+    for n in (0, 1, 2, 7, 10, 1000, 10**9 + 7, 2**63 + 5):
+        for w in range(1, 10):
+            for r in range(w):
+                _lib.call("exsum_shard_bounds", n, w, r, C.byref(b), C.byref(e))
+                assert (b.value, e.value) == shard_bounds(n, w, r), (n, w, r)
+    for bad in ((10, 0, 0), (10, 2, 2), (10, 2, -1)):
+        assert _lib.lib.exsum_shard_bounds(*bad, C.byref(b), C.byref(e)) == _lib.EXSUM_EINVAL
+
+
+def test_nccl_entry_points_without_gpu():
+    """NCCL loads lazily (dlopen); argument errors are status codes, not crashes."""
+    ver = C.c_int(0)
+    if not _lib.lib.exsum_nccl_available(C.byref(ver)):
+        pytest.skip("libnccl.so.2 not loadable here")
+    assert ver.value >= 21900  # NCCL 2.19+
+    uid = (C.c_char * _lib.NCCL_UNIQUE_ID_BYTES)()
+    assert _lib.lib.exsum_nccl_get_unique_id(None) == _lib.EXSUM_EINVAL
+    comm = C.c_void_p()
+    assert _lib.lib.exsum_nccl_comm_init(C.byref(comm), 0, uid, 0) == _lib.EXSUM_EINVAL
+    assert _lib.lib.exsum_nccl_comm_init(C.byref(comm), 2, uid, 2) == _lib.EXSUM_EINVAL
+    assert _lib.lib.exsum_nccl_sum(None, 0, 0, None, None, None, None, 0, None) == _lib.EXSUM_EINVAL
+    assert _lib.lib.exsum_nccl_comm_destroy(None) == _lib.EXSUM_EINVAL
+    sizes = [_lib.lib.exsum_nccl_workspace_bytes(w) for w in (1, 2, 8)]
+    assert _lib.lib.exsum_nccl_workspace_bytes(0) == 0
+    assert sizes[0] >= _lib.lib.exsum_cuda_workspace_bytes() + 2 * 592
+    assert sizes[2] - sizes[1] == 6 * 592

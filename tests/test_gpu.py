@@ -222,3 +222,54 @@ def test_workspace_reuse_and_streams(cuda):
         b = dev_sum(x)[0]
     torch.cuda.synchronize()
     assert a == b == dev_sum(x)[0]
+
+
+# ------------------------------------------------------------- NCCL C ABI
+
+def test_nccl_sum_world1_and_graph(cuda, checker):
+    """exsum_nccl_sum (sum -> ncclAllGather -> merge in the C library) on a
+    1-rank communicator: bits and record equal the serial reference, with a
+    nonzero base_index, specials, and under CUDA-graph capture."""
+    import socket
+    import torch.distributed as dist
+    from paper_1505_05571_b200.distributed import NcclCommunicator, nccl_exact_sum
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        comm = NcclCommunicator(torch.device("cuda", 0))
+        rng = np.random.default_rng(11)
+        for n in (0, 1, 1000, 1_000_003):
+            b = rng.integers(0, 2**64 - 1, size=n, dtype=np.uint64)
+            e = rng.integers(0, 2047, size=n, dtype=np.uint64)
+            if n:
+                e[rng.random(n) < 0.001] = 2047
+            h = ((b & np.uint64(0x800FFFFFFFFFFFFF)) | (e << np.uint64(52))).view(np.float64)
+            x = to_dev(h, 1)
+            rec = torch.empty(ops.PARTIAL_BYTES, dtype=torch.uint8, device="cuda")
+            got = bits_of(nccl_exact_sum(x, comm, base_index=12345, record=rec).item())
+            assert got == bits_of(checker.exact_sum(h)), n
+            want_r, want_p = dev_sum(x, base_index=12345)
+            assert got == want_r
+            assert bytes(rec.cpu().numpy()) == bytes(want_p), n
+        # graph capture of the whole step
+        x = gen(4, 10_000_000, 3)
+        want, _ = dev_sum(x)
+        res = torch.empty(1, dtype=torch.float64, device="cuda")
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            nccl_exact_sum(x, comm, base_index=0, result=res)  # warm-up outside capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            nccl_exact_sum(x, comm, base_index=0, result=res)
+        res.zero_()
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        assert bits_of(res.item()) == want
+        comm.close()
+    finally:
+        dist.destroy_process_group()
