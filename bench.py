@@ -349,7 +349,7 @@ def run_segmented(args, wl):
                        "l2": "11.3 GB input > 126 MB L2"},
             "terms_per_s": round(int(offs[-1]) * steps / (ms / 1e3), 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": None,
+                         "frac": round(achieved / peak, 4), "traffic": ncu_traffic(5),
                          "kernel": "exsum_segmented_kernel", "kernel_ms": round(ms / steps, 4)},
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": steps, "clocks": clocks.report(),
             "bit_exact_vs_oracle_first4096": parity,
@@ -360,6 +360,16 @@ def run_segmented(args, wl):
 
 
 # ---------------------------------------------------------------- GPU arm
+
+def ncu_traffic(config: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel, from the committed `ncu --set full` capture (profiles/ncu_summary.json)."""
+    prof = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        return json.loads(prof.read_text()).get(f"config{config}", {}).get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        return None
+
 
 def main():
     args = parse()
@@ -458,13 +468,7 @@ def main():
     achieved = 8.0 * n_local / (k_ms / 1e3) / 1e9              # dominant kernel, per GPU
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    prof = ROOT / "profiles" / "ncu_summary.json"
-    traffic = None
-    if prof.exists():
-        try:
-            traffic = json.loads(prof.read_text()).get(f"config{args.config}", {}).get("dram_bytes_per_launch")
-        except Exception:  # noqa: BLE001
-            traffic = None
+    traffic = ncu_traffic(args.config)
 
     # e2e through the C ABI with host buffers (pinned), copies inside the timed region
     e2e = None

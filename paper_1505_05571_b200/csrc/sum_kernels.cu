@@ -61,6 +61,9 @@
 #ifndef EXSUM_UNIFORM_FAST
 #define EXSUM_UNIFORM_FAST 1  // single-sum kernel: register fast path for one-slot batches
 #endif
+#ifndef EXSUM_TIMELINE
+#define EXSUM_TIMELINE 0  // diagnostics build: per-warp %globaltimer stamps (scripts/timeline.py)
+#endif
 #ifndef EXSUM_UNIFORM_BACKOFF
 #define EXSUM_UNIFORM_BACKOFF 7  // batches to skip the one-slot test after a miss
 #endif
@@ -101,6 +104,25 @@ constexpr int kScratch = kWarps * kChunks * 8;          // per-warp chunk rows
 constexpr int kSmem = kWarps * kWarpSmem + kScratch;    // 207,040 B
 constexpr int kPrefetchBatches = EXSUM_PREFETCH_BATCHES;
 constexpr int kUniformBackoff = EXSUM_UNIFORM_BACKOFF;
+
+#if EXSUM_TIMELINE
+// [warp][0..3]: start, loop end, flush end (after the CTA's REDs), last-CTA end
+__device__ unsigned long long g_timeline[148 * 8 * 4 + 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define EXSUM_STAMP(slot)                                                                  \
+  do {                                                                                     \
+    if (lane == 0 && blockIdx.x < 148)                                                     \
+      g_timeline[(blockIdx.x * kWarps + warp) * 4 + (slot)] = gtimer();                    \
+  } while (0)
+#else
+#define EXSUM_STAMP(slot) \
+  do {                    \
+  } while (0)
+#endif
 static_assert(kSmem <= 227 * 1024, "shared memory budget");
 
 // One lane's view of its accumulator.  Generic pointers serve the cold paths;
@@ -722,6 +744,7 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
   // Programmatic dependent launch: let the next sum in the stream start its CTAs
   // on SMs this grid releases (no-op unless launched with EXSUM_SUM_OVERLAP).
   asm volatile("griddepcontrol.launch_dependents;");
+  EXSUM_STAMP(0);
   // K1: contiguous per-warp ranges, boundaries on 4-term multiples.
   const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * kWarps + warp;
   const unsigned long long nw = static_cast<unsigned long long>(gridDim.x) * kWarps;
@@ -743,6 +766,7 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
       x, tb, te, base_index, a, sp, norm_count, lane);
 
   // K2: the warp's 67 chunk sums.
+  EXSUM_STAMP(1);
   warp_chunks(wsm, lane, scratch + warp * kChunks);
   const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                            N = warp_min_u64(sp.N);
@@ -764,6 +788,7 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
   }
   __threadfence();
   __syncthreads();
+  EXSUM_STAMP(2);
   if (threadIdx.x == 0) s_last = atomicAdd(&ws->done, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!s_last) return;
@@ -789,6 +814,7 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
   if (lane == 0) ws->done = 0;
   if (!finalize) return;
   warp_emit(scratch, ~s_spec[0], ~s_spec[1], Nf, payload, result, partial, lane);
+  EXSUM_STAMP(3);
 }
 
 // Finalise a workspace filled by exsum_cuda_accumulate launches.
@@ -1023,5 +1049,12 @@ int exsum_cuda_merge(const exsum_partial *d_parts, size_t k, double *d_result,
                                                                       d_out);
   return launch_status();
 }
+
+#if EXSUM_TIMELINE
+int exsum_debug_timeline(unsigned long long *out, size_t count) {
+  if (!out || count > sizeof(g_timeline) / 8) return EXSUM_EINVAL;
+  return cudaMemcpyFromSymbol(out, g_timeline, count * 8) == cudaSuccess ? EXSUM_OK : EXSUM_ECUDA;
+}
+#endif
 
 }  // extern "C"

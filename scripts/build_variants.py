@@ -9,9 +9,9 @@ VARIANTS = {
     "nofast": ("EXSUM_UNIFORM_FAST=0",),
     "backoff0": ("EXSUM_UNIFORM_BACKOFF=0",),
     "backoff15": ("EXSUM_UNIFORM_BACKOFF=15",),
+    "timeline": ("EXSUM_TIMELINE=1",),
     "seg4": ("EXSUM_SEG_VEC=4",),
     "segsplit": ("EXSUM_SEG_SPLIT=1",),
-    "segsplit4": ("EXSUM_SEG_SPLIT=1", "EXSUM_SEG_VEC=4"),
 }
 names = sys.argv[1:] or list(VARIANTS)
 verbose = "-v" in names

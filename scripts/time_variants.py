@@ -1,6 +1,8 @@
 """Time kernel variants (lib/variants/*.so) on configs 2/3 (1e8) and 4 (1e9).
 
-Each variant runs in its own process (EXSUM_LIB selects the .so).  Prints one
+Each variant runs in its own process (EXSUM_LIB selects the .so).
+TV_OVERLAP=1 launches back-to-back sums with programmatic dependent launch
+(the bench's mode); TV_CONFIGS=2,3 restricts the configs.  Prints one
 line per (variant, config): ms per sum, GB/s, result bits (must agree).
 """
 import json
@@ -11,7 +13,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 CHILD = r'''
-import sys, json, torch, numpy as np
+import os, sys, json, torch, numpy as np
 sys.path.insert(0, %r)
 from paper_1505_05571_b200 import _lib, ops
 dev = torch.device("cuda", 0)
@@ -43,13 +45,14 @@ for config, n, K in %s:
     res = torch.empty(1, dtype=torch.float64, device=dev)
     part = torch.empty(ops.PARTIAL_BYTES, dtype=torch.uint8, device=dev)
     ws = ops.Workspace(dev)
+    ov = bool(int(os.environ.get("TV_OVERLAP", "0")))
     for _ in range(3):
-        ops.exact_sum_tensor(x, result=res, partial=part, workspace=ws)
+        ops.exact_sum_tensor(x, result=res, partial=part, workspace=ws, overlap=ov)
     torch.cuda.synchronize()
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st.record()
     for _ in range(K):
-        ops.exact_sum_tensor(x, result=res, partial=part, workspace=ws)
+        ops.exact_sum_tensor(x, result=res, partial=part, workspace=ws, overlap=ov)
     en.record(); torch.cuda.synchronize()
     ms = st.elapsed_time(en) / K
     out[config] = (ms, 8 * n / ms / 1e6, int(np.float64(res.item()).view(np.uint64)))
