@@ -103,6 +103,15 @@ int exsum_large_small(const exsum_large *acc, exsum_small *out);
 /* LargeAccumulator::chunks_in_use — large_accumulator.cpp:143-149 */
 int exsum_large_chunks_in_use(const exsum_large *acc);
 
+/* --------------------------------------------------- sqnorm / dot (host) */
+/* sqnorm(values, SumMethod::large) — vector_ops.cpp:143-146 via sum_products
+ * (:72-97): the exact, correctly rounded sum of the rounded squares x[i]*x[i]. */
+int exsum_sqnorm(const double *x, size_t n, double *out);
+/* dot(a, b, SumMethod::large) — vector_ops.cpp:147-155: exact sum of the
+ * rounded products a[i]*b[i]; EXSUM_EINVAL on length mismatch (the reference
+ * throws std::invalid_argument, :150-152). */
+int exsum_dot(const double *a, size_t na, const double *b, size_t nb, double *out);
+
 /* ---------------------------------------------------- partial records (host) */
 /* Exact sum of x[0..n) into a partial record (host code; the record format the
  * device path and the multi-GPU exchange use).  base_index is the global index
@@ -143,6 +152,18 @@ int exsum_cuda_sum(const double *d_x, size_t n, uint64_t base_index, double *d_r
 int exsum_cuda_sum_ex(const double *d_x, size_t n, uint64_t base_index, double *d_result,
                       exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
                       unsigned flags);
+
+/* sqnorm / dot on the device (vector_ops.cpp:143-155): the exact sum of the
+ * products rounded as the reference's x86 multiply rounds them (IEEE nearest
+ * even; a NaN operand propagates quieted, x first; 0 * Inf is the x86 default
+ * NaN 0xFFF8000000000000), one launch like exsum_cuda_sum.  dot reads both
+ * arrays with 256-bit loads when they are co-aligned mod 32 bytes; na != nb is
+ * EXSUM_EINVAL. */
+int exsum_cuda_sqnorm(const double *d_x, size_t n, uint64_t base_index, double *d_result,
+                      exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream);
+int exsum_cuda_dot(const double *d_a, size_t na, const double *d_b, size_t nb,
+                   uint64_t base_index, double *d_result, exsum_partial *d_partial, void *d_ws,
+                   size_t ws_bytes, void *stream);
 
 /* Incremental form (LargeAccumulator::add(span) across calls, large_accumulator.hpp:61):
  * accumulate d_x into the workspace without rounding; then finalize. */

@@ -35,6 +35,8 @@ class Port:
             ("port_canonical", i32, [vp, sz, vp, C.POINTER(u64), C.POINTER(u64)]),
             ("port_segmented_sum", None, [vp, vp, sz, vp, i32]),
             ("port_max_threads", i32, []),
+            ("port_sqnorm", dbl, [vp, sz]),
+            ("port_dot", i32, [vp, sz, vp, sz, C.POINTER(dbl)]),
         ]:
             f = getattr(L, name)
             f.restype, f.argtypes = res, args
@@ -68,6 +70,17 @@ class Port:
         self.lib.port_segmented_sum(a.ctypes.data, o.ctypes.data, o.size - 1, out.ctypes.data,
                                     threads or self._threads)
         return out
+
+    def sqnorm(self, x) -> float:
+        a = self._arr(x)
+        return self.lib.port_sqnorm(a.ctypes.data, a.size)
+
+    def dot(self, x, y) -> float:
+        a, b = self._arr(x), self._arr(y)
+        out = C.c_double()
+        if self.lib.port_dot(a.ctypes.data, a.size, b.ctypes.data, b.size, C.byref(out)):
+            raise ValueError("dot: length mismatch")
+        return out.value
 
     def set_threads(self, n: int) -> None:
         self._threads = n

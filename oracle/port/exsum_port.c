@@ -305,6 +305,38 @@ double port_exact_sum(const double *x, size_t n, int method) {
   return port_small_round(&s);
 }
 
+/* sum_products (vector_ops.cpp:72-97) with SumMethod::large; sqnorm / dot
+ * (vector_ops.cpp:143-155).  Products rounded by the host multiply (x86: NaN
+ * operands propagate quieted, 0 * Inf = default NaN), as in the reference. */
+double port_sqnorm(const double *x, size_t n) {
+  port_large *L = (port_large *)malloc(sizeof *L);
+  large_init(L);
+  for (size_t i = 0; i < n; ++i) {
+    const double p = x[i] * x[i];
+    large_add(L, bits_of(p));
+  }
+  large_drain(L);
+  port_small s = L->s;
+  free(L);
+  return port_small_round(&s);
+}
+
+/* returns 1 (and leaves *out) on length mismatch, as dot throws (:150-152) */
+int port_dot(const double *a, size_t na, const double *b, size_t nb, double *out) {
+  if (na != nb) return 1;
+  port_large *L = (port_large *)malloc(sizeof *L);
+  large_init(L);
+  for (size_t i = 0; i < na; ++i) {
+    const double p = a[i] * b[i];
+    large_add(L, bits_of(p));
+  }
+  large_drain(L);
+  port_small s = L->s;
+  free(L);
+  *out = port_small_round(&s);
+  return 0;
+}
+
 /* vector_ops.cpp:37-70,172-186 */
 double port_parallel_exact_sum(const double *x, size_t n, int parts, size_t thr, int threads) {
   if (parts < 1) parts = 1;

@@ -18,6 +18,8 @@ int port_small_propagate(port_small *a);
 void port_small_merge(port_small *dst, const port_small *src);
 double port_small_round(port_small *a);
 double port_exact_sum(const double *x, size_t n, int method);
+double port_sqnorm(const double *x, size_t n);
+int port_dot(const double *a, size_t na, const double *b, size_t nb, double *out);
 double port_parallel_exact_sum(const double *x, size_t n, int parts, size_t thr, int threads);
 int port_canonical(const double *x, size_t n, int64_t *chunks67, uint64_t *inf_bits,
                    uint64_t *nan_bits);

@@ -102,6 +102,18 @@ class Ref:
                                    threads)
         return out
 
+    def sqnorm(self, x, method: str = "large") -> float:
+        a = self._arr(x)
+        return self.lib.ref_sqnorm(a.ctypes.data, a.size, 0 if method == "small" else 1)
+
+    def dot(self, x, y, method: str = "large") -> float:
+        a, b = self._arr(x), self._arr(y)
+        out = C.c_double()
+        if self.lib.ref_dot(a.ctypes.data, b.ctypes.data, a.size, b.size,
+                            0 if method == "small" else 1, C.byref(out)):
+            raise ValueError("dot: length mismatch")
+        return out.value
+
     def set_threads(self, n: int) -> None:
         self.lib.ref_set_threads(n)
 

@@ -82,6 +82,8 @@ _SIGNATURES = {
     "exsum_large_mean": (_i32, [_vp, _u64, _dp]),
     "exsum_large_small": (_i32, [_vp, _sp]),
     "exsum_large_chunks_in_use": (_i32, [_vp]),
+    "exsum_sqnorm": (_i32, [_vp, _sz, _dp]),
+    "exsum_dot": (_i32, [_vp, _sz, _vp, _sz, _dp]),
     "exsum_partial_from_array": (_i32, [_vp, _sz, _u64, _pp]),
     "exsum_partial_merge": (_i32, [_pp, _sz, _pp, _dp]),
     "exsum_partial_round": (_i32, [_pp, _dp]),
@@ -89,6 +91,8 @@ _SIGNATURES = {
     "exsum_cuda_workspace_init": (_i32, [_vp, _sz, _vp]),
     "exsum_cuda_sum": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _sz, _vp]),
     "exsum_cuda_sum_ex": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _sz, _vp, C.c_uint]),
+    "exsum_cuda_sqnorm": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _sz, _vp]),
+    "exsum_cuda_dot": (_i32, [_vp, _sz, _vp, _sz, _u64, _vp, _vp, _vp, _sz, _vp]),
     "exsum_cuda_accumulate": (_i32, [_vp, _sz, _u64, _vp, _sz, _vp]),
     "exsum_cuda_finalize": (_i32, [_vp, _vp, _vp, _sz, _vp]),
     "exsum_cuda_sum_segmented": (_i32, [_vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp]),

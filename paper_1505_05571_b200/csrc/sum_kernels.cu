@@ -49,6 +49,9 @@
 #ifndef EXSUM_VEC_PER_LANE
 #define EXSUM_VEC_PER_LANE 8  // single-sum kernel: 256-bit vectors per lane per batch
 #endif
+#ifndef EXSUM_DOT_VEC
+#define EXSUM_DOT_VEC 4  // dot kernel: vectors per lane per batch (x and y each)
+#endif
 #ifndef EXSUM_SEG_VEC
 #define EXSUM_SEG_VEC 8  // segmented kernel: vectors per lane per batch
 #endif
@@ -306,12 +309,67 @@ __device__ __forceinline__ void record_special(Specials &sp, uint32_t lo, uint32
   }
 }
 
-// One term of a scalar head/tail: Inf/NaN recorded, everything else added.
-__device__ __forceinline__ void add_term_checked(const Lane &a, Specials &sp, uint32_t lo,
-                                                 uint32_t hi, unsigned long long index) {
+// ------------------------------------------------------------- term sources
+//
+// The stream kernels sum terms produced from their input arrays by one of:
+//   kSum       x[i]                        exact_sum  (vector_ops.cpp:121-130)
+//   kSqnorm    fl(x[i] * x[i])              sqnorm     (vector_ops.cpp:143-146)
+//   kDot       fl(x[i] * y[i]), x, y co-aligned        dot (vector_ops.cpp:147-155)
+//   kDotScalarB  the same, y read with 8-byte loads (x, y not co-aligned mod 32 B)
+// Products are __dmul_rn (IEEE, round to nearest even, denormals kept: what the
+// reference's SSE2 multiply computes for every non-NaN result).  A NaN product
+// follows the x86 rules the reference inherits (probed on the compiled
+// reference): a NaN operand propagates quieted with its payload, x first;
+// 0 * Inf gives the x86 default NaN 0xFFF8000000000000.  The device product of
+// those cases is a canonical NaN instead, so batches with an Inf/NaN product go
+// through the fix-up, which cancels the device bits and records the x86 ones.
+enum Op : int { kSum = 0, kSqnorm = 1, kDot = 2, kDotScalarB = 3 };
+
+template <int kOp>
+__device__ __forceinline__ void term_bits(uint32_t xl, uint32_t xh, uint32_t yl, uint32_t yh,
+                                          uint32_t &lo, uint32_t &hi) {
+  if constexpr (kOp == kSum) {
+    lo = xl;
+    hi = xh;
+  } else {
+    const double a = __hiloint2double(static_cast<int>(xh), static_cast<int>(xl));
+    const double b = kOp == kSqnorm ? a : __hiloint2double(static_cast<int>(yh), static_cast<int>(yl));
+    const double p = __dmul_rn(a, b);
+    lo = static_cast<uint32_t>(__double2loint(p));
+    hi = static_cast<uint32_t>(__double2hiint(p));
+  }
+}
+
+// The bits the reference's x86 multiply produces for a*b (differs from the
+// device product only when the product is a NaN).
+__device__ __forceinline__ unsigned long long x86_product(unsigned long long a,
+                                                          unsigned long long b) {
+  const unsigned long long kAbs = 0x7FFFFFFFFFFFFFFFull, kInf = 0x7FF0000000000000ull;
+  const unsigned long long kQuiet = 0x0008000000000000ull;
+  if ((a & kAbs) > kInf) return a | kQuiet;
+  if ((b & kAbs) > kInf) return b | kQuiet;
+  const double p = __dmul_rn(__longlong_as_double(static_cast<long long>(a)),
+                             __longlong_as_double(static_cast<long long>(b)));
+  const unsigned long long pb = static_cast<unsigned long long>(__double_as_longlong(p));
+  return (pb & kAbs) > kInf ? 0xFFF8000000000000ull : pb;  // 0 * Inf: x86 default NaN
+}
+
+// One term of a scalar head/tail (element i): Inf/NaN recorded, others added.
+template <int kOp>
+__device__ __forceinline__ void add_elem_checked(const Lane &a, Specials &sp, const double *x,
+                                                 const double *y, unsigned long long i,
+                                                 unsigned long long index) {
+  const unsigned long long xb = __ldg(reinterpret_cast<const unsigned long long *>(x) + i);
+  const unsigned long long yb =
+      kOp >= kDot ? __ldg(reinterpret_cast<const unsigned long long *>(y) + i) : xb;
+  uint32_t lo, hi;
+  term_bits<kOp>(static_cast<uint32_t>(xb), static_cast<uint32_t>(xb >> 32),
+                 static_cast<uint32_t>(yb), static_cast<uint32_t>(yb >> 32), lo, hi);
   const uint32_t e = exponent_field(hi);
   if (e == 0x7FFu) {
-    record_special(sp, lo, hi, index);
+    const unsigned long long t =
+        kOp == kSum ? xb : x86_product(xb, yb);
+    record_special(sp, static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32), index);
   } else {
     add_term(a, lo, hi, e);
   }
@@ -326,22 +384,53 @@ __device__ __forceinline__ void ldg256(const double *p, uint32_t (&w)[8]) {
       : "l"(p));
 }
 
-template <int V>
+// Four 8-byte loads of a 32-byte group that is only 8-byte aligned (kDotScalarB's
+// y); L1-allocating so a warp's four instructions share the lines.
+__device__ __forceinline__ void ldg4x64(const double *p, uint32_t (&w)[8]) {
+  const unsigned long long *q = reinterpret_cast<const unsigned long long *>(p);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned long long v = __ldg(q + i);
+    w[2 * i] = static_cast<uint32_t>(v);
+    w[2 * i + 1] = static_cast<uint32_t>(v >> 32);
+  }
+}
+
+template <int V, int kOp = kSum>
 struct Batch {
-  uint32_t w[V][8];
+  uint32_t w[V][8];                       // x
+  uint32_t y[kOp >= kDot ? V : 1][8];     // y (dot only)
 };
 
-// Load vector v0 + u*32 + lane (u < V) of the 32-byte vector array X4; vectors at
-// or beyond vend read as zero terms (which add nothing).
-template <int V>
-__device__ __forceinline__ void load_batch(Batch<V> &b, const double *X4, long long v0,
-                                           long long vend, int lane) {
+// Vector u of a batch: x (and y) of the 32-byte group `vec`.
+template <int V, int kOp>
+__device__ __forceinline__ void load_vec(Batch<V, kOp> &b, int u, const double *X4,
+                                         const double *Y4, long long vec) {
+  ldg256(X4 + 4 * vec, b.w[u]);
+  if constexpr (kOp == kDot) ldg256(Y4 + 4 * vec, b.y[u]);
+  if constexpr (kOp == kDotScalarB) ldg4x64(Y4 + 4 * vec, b.y[u]);
+}
+
+template <int V, int kOp>
+__device__ __forceinline__ void zero_vec(Batch<V, kOp> &b, int u) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q) b.w[u][q] = 0u;
+  if constexpr (kOp >= kDot) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) b.y[u][q] = 0u;
+  }
+}
+
+// Load vector v0 + u*32 + lane (u < V) of the 32-byte vector arrays; vectors at
+// or beyond vend read as zero terms (which add nothing; 0 * 0 = +0 for products).
+template <int V, int kOp>
+__device__ __forceinline__ void load_batch(Batch<V, kOp> &b, const double *X4, const double *Y4,
+                                           long long v0, long long vend, int lane) {
 #pragma unroll
   for (int u = 0; u < V; ++u) {
     const long long v = v0 + u * 32 + lane;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) b.w[u][q] = 0u;
-    if (v < vend) ldg256(X4 + 4 * v, b.w[u]);
+    zero_vec<V, kOp>(b, u);
+    if (v < vend) load_vec<V, kOp>(b, u, X4, Y4, v);
   }
 }
 
@@ -353,9 +442,19 @@ __device__ __forceinline__ void prefetch_l2(const double *X4, long long v0, long
   if (v0 >= vend) return;
   long long nv = vend - v0;
   if (nv > V * 32) nv = V * 32;
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(X4 + 4 * v0),
-               "r"(static_cast<uint32_t>(nv * 32))
+  const uintptr_t p0 = reinterpret_cast<uintptr_t>(X4 + 4 * v0);
+  const uintptr_t p1 = p0 + static_cast<uintptr_t>(nv * 32);
+  const uintptr_t a0 = p0 & ~uintptr_t{15};  // kDotScalarB's y is only 8-byte aligned
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0),
+               "r"(static_cast<uint32_t>((p1 - a0 + 15) & ~uintptr_t{15}))
                : "memory");
+}
+
+template <int V, int kOp>
+__device__ __forceinline__ void prefetch_batch(const double *X4, const double *Y4, long long v0,
+                                               long long vend) {
+  prefetch_l2<V>(X4, v0, vend);
+  if constexpr (kOp >= kDot) prefetch_l2<V>(Y4, v0, vend);
 }
 
 // Inf/NaN fix-up of one batch (rare): the batch's terms were added blindly;
@@ -366,12 +465,14 @@ __device__ __forceinline__ void prefetch_l2(const double *X4, long long v0, long
 //   kScan = false: compact loop, one L2 round trip per term (cold data only).
 //   kScan = true:  all high words loaded at once into a bitmask, then only the
 //                  flagged terms are re-read (data with frequent specials).
-template <int V, bool kScan>
+template <int V, bool kScan, int kOp>
 __device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, const double *X4,
-                                               long long v, long long nvec, int lane,
-                                               unsigned long long ib) {
+                                               const double *Y4, long long v, long long nvec,
+                                               int lane, unsigned long long ib) {
   const unsigned long long *xb = reinterpret_cast<const unsigned long long *>(X4);
+  const unsigned long long *yb = reinterpret_cast<const unsigned long long *>(Y4);
   if constexpr (kScan) {
+    static_assert(kOp == kSum, "scanning fix-up: plain sums only");
     static_assert(4 * V <= 32, "scan mask holds one batch");
     const uint32_t *xh = reinterpret_cast<const uint32_t *>(X4);
     uint32_t mask = 0u;
@@ -401,10 +502,15 @@ __device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, cons
       if (vec >= nvec) break;
 #pragma unroll 1
       for (int q = 0; q < 4; ++q) {
-        const unsigned long long bits = __ldcg(xb + 4 * vec + q);
-        const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
+        const unsigned long long xv = __ldcg(xb + 4 * vec + q);
+        const unsigned long long yv = kOp >= kDot ? __ldcg(yb + 4 * vec + q) : xv;
+        uint32_t lo, hi;  // the bits that were added blindly
+        term_bits<kOp>(static_cast<uint32_t>(xv), static_cast<uint32_t>(xv >> 32),
+                       static_cast<uint32_t>(yv), static_cast<uint32_t>(yv >> 32), lo, hi);
         if (exponent_field(hi) == 0x7FFu) {
-          record_special(sp, lo, hi, ib + 4ull * static_cast<unsigned long long>(vec) + q);
+          const unsigned long long t = kOp == kSum ? xv : x86_product(xv, yv);
+          record_special(sp, static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32),
+                         ib + 4ull * static_cast<unsigned long long>(vec) + q);
           add_term(a, lo, hi ^ 0x80000000u, 0x7FFu);  // cancel the garbage add
         }
       }
@@ -414,27 +520,29 @@ __device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, cons
 
 // Add one batch (registers b) with rolling refill from vector nv onward.  kGuard:
 // bounds-checked refills (only the last batches need it).  Returns the batch's
-// maximum exponent field (2047 iff it contained an Inf/NaN).
-template <int V, bool kGuard>
-__device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V> &b, const double *X4,
+// maximum exponent field (2047 iff it contained an Inf/NaN term).
+template <int V, bool kGuard, int kOp>
+__device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &b,
+                                                  const double *X4, const double *Y4,
                                                   long long nv, long long nvec, int lane) {
   uint32_t emax = 0;
-  const double *pn = X4 + 4 * (nv + lane);
 #pragma unroll
   for (int u = 0; u < V; ++u) {
-    uint32_t e[4];
+    uint32_t lo[4], hi[4], e[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      e[q] = exponent_field(b.w[u][2 * q + 1]);
+      term_bits<kOp>(b.w[u][2 * q], b.w[u][2 * q + 1], b.y[kOp >= kDot ? u : 0][2 * q],
+                     b.y[kOp >= kDot ? u : 0][2 * q + 1], lo[q], hi[q]);
+      e[q] = exponent_field(hi[q]);
       emax = max(emax, e[q]);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) add_term(a, b.w[u][2 * q], b.w[u][2 * q + 1], e[q]);
-    if (!kGuard || nv + u * 32 + lane < nvec) {
-      ldg256(pn + 4 * 32 * u, b.w[u]);
+    for (int q = 0; q < 4; ++q) add_term(a, lo[q], hi[q], e[q]);
+    const long long vec = nv + u * 32 + lane;
+    if (!kGuard || vec < nvec) {
+      load_vec<V, kOp>(b, u, X4, Y4, vec);
     } else {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) b.w[u][q] = 0u;
+      zero_vec<V, kOp>(b, u);
     }
   }
   return emax;
@@ -482,75 +590,76 @@ __device__ __forceinline__ uint32_t uniform_slot(const Batch<V> &b) {
   return (kbits == (hand & 0x7E000000u) && kbits != 0x7E000000u) ? (kbits >> 25) : ~0u;
 }
 
-// Accumulate x[begin, end) into the calling warp's lane accumulators.
-// index_base is added to positions to form special-value indices; norm_count
-// counts batches since the last renormalisation (warp-uniform).
+// Accumulate the terms of elements [begin, end) into the calling warp's lane
+// accumulators.  index_base is added to positions to form special-value
+// indices; norm_count counts batches since the last renormalisation
+// (warp-uniform).
 //   V:        vectors (4 terms) per lane per batch
-//   kUniform: register fast path for one-slot batches (larger code)
+//   kUniform: register fast path for one-slot batches (plain sums; larger code)
 //   kSplit:   separate unguarded steady-state body (larger code, fewer instrs)
 //   kScan:    scanning Inf/NaN fix-up (for data with frequent specials)
-template <int V, bool kUniform, bool kSplit, bool kScan>
+//   kOp:      term source (kSum, kSqnorm, kDot, kDotScalarB); y used by dots
+template <int V, bool kUniform, bool kSplit, bool kScan, int kOp = kSum>
 __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
+                                                const double *__restrict__ y,
                                                 unsigned long long begin, unsigned long long end,
                                                 unsigned long long index_base, const Lane &a,
                                                 Specials &sp, int &norm_count, int lane) {
   constexpr int kNormEvery = 2016 / (4 * V);  // batches between renormalisations
   static_assert(kNormEvery >= 1, "batch too large for the carry budget");
+  static_assert(kOp == kSum || !kUniform, "one-slot fast path: plain sums only");
   if (begin >= end) return;
   // Scalar head up to 32-byte alignment of &x[pos], scalar tail after the vectors.
   const uintptr_t addr = reinterpret_cast<uintptr_t>(x + begin);
   unsigned long long head = ((32u - (addr & 31u)) & 31u) >> 3;
   if (head > end - begin) head = end - begin;
-  const unsigned long long *xb = reinterpret_cast<const unsigned long long *>(x);
-  if (lane < static_cast<int>(head)) {
-    const unsigned long long bits = __ldg(xb + begin + lane);
-    add_term_checked(a, sp, static_cast<uint32_t>(bits), static_cast<uint32_t>(bits >> 32),
-                     index_base + begin + lane);
-  }
+  if (lane < static_cast<int>(head))
+    add_elem_checked<kOp>(a, sp, x, y, begin + lane, index_base + begin + lane);
   const unsigned long long vbeg_t = begin + head;  // first vector's term position
   const long long nvec = static_cast<long long>((end - vbeg_t) >> 2);
   const double *X4 = x + vbeg_t;                   // 32-byte aligned
+  const double *Y4 = kOp >= kDot ? y + vbeg_t : X4;
   const unsigned long long tail_t = vbeg_t + 4ull * static_cast<unsigned long long>(nvec);
-  if (lane < static_cast<int>(end - tail_t)) {
-    const unsigned long long bits = __ldg(xb + tail_t + lane);
-    add_term_checked(a, sp, static_cast<uint32_t>(bits), static_cast<uint32_t>(bits >> 32),
-                     index_base + tail_t + lane);
-  }
+  if (lane < static_cast<int>(end - tail_t))
+    add_elem_checked<kOp>(a, sp, x, y, tail_t + lane, index_base + tail_t + lane);
   if (nvec <= 0) return;
   constexpr long long kStep = V * 32;
   const unsigned long long ib = index_base + vbeg_t;
   if (lane == 0) {
-    for (int d = 0; d <= kPrefetchBatches; ++d) prefetch_l2<V>(X4, d * kStep, nvec);
+    for (int d = 0; d <= kPrefetchBatches; ++d) prefetch_batch<V, kOp>(X4, Y4, d * kStep, nvec);
   }
-  Batch<V> b;
-  load_batch<V>(b, X4, 0, nvec, lane);
+  Batch<V, kOp> b;
+  load_batch<V, kOp>(b, X4, Y4, 0, nvec, lane);
   int backoff = 0;
   for (long long v = 0; v < nvec; v += kStep) {
     const long long nv = v + kStep;
-    if (lane == 0) prefetch_l2<V>(X4, v + (kPrefetchBatches + 1) * kStep, nvec);
+    if (lane == 0) prefetch_batch<V, kOp>(X4, Y4, v + (kPrefetchBatches + 1) * kStep, nvec);
     uint32_t emax = 0;
     const bool steady = nv + kStep <= nvec;  // next batch complete: unguarded refills
     uint32_t k = ~0u;
-    if (kUniform && steady) {
-      if (backoff > 0) {
-        --backoff;
-      } else {
-        k = uniform_slot<V>(b);
-        if (!__all_sync(0xffffffffu, k != ~0u)) {
-          k = ~0u;
-          backoff = kUniformBackoff;  // wide data rarely turns uniform
+    if constexpr (kUniform) {
+      if (steady) {
+        if (backoff > 0) {
+          --backoff;
+        } else {
+          k = uniform_slot<V>(b);
+          if (!__all_sync(0xffffffffu, k != ~0u)) {
+            k = ~0u;
+            backoff = kUniformBackoff;  // wide data rarely turns uniform
+          }
         }
       }
+      if (k != ~0u) batch_uniform<V>(a, b, X4, nv, lane, k);
     }
-    if (k != ~0u) {
-      batch_uniform<V>(a, b, X4, nv, lane, k);
-    } else if (kSplit && steady) {
-      emax = batch_rolling<V, false>(a, b, X4, nv, nvec, lane);
-    } else {
-      emax = batch_rolling<V, true>(a, b, X4, nv, nvec, lane);
+    if (k == ~0u) {
+      if (kSplit && steady) {
+        emax = batch_rolling<V, false, kOp>(a, b, X4, Y4, nv, nvec, lane);
+      } else {
+        emax = batch_rolling<V, true, kOp>(a, b, X4, Y4, nv, nvec, lane);
+      }
     }
     if (__builtin_expect(emax == 0x7FFu, 0))
-      fixup_specials<V, kScan>(a, sp, X4, v, nvec, lane, ib);
+      fixup_specials<V, kScan, kOp>(a, sp, X4, Y4, v, nvec, lane, ib);
     if (++norm_count >= kNormEvery) {
       normalize(a);
       norm_count = 0;
@@ -730,10 +839,13 @@ __device__ void warp_emit(const long long *row, unsigned long long P, unsigned l
 
 // --------------------------------------------------------------- K1 + K2 + K3
 
+template <int kOp>
 __global__ void __launch_bounds__(kThreads, 1)
-exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
+exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, unsigned long long n,
                  unsigned long long base_index, Workspace *__restrict__ ws, int finalize,
                  double *result, exsum_partial *partial) {
+  // vectors per lane per batch: a dot keeps two arrays' vectors in registers
+  constexpr int V = kOp >= kDot ? EXSUM_DOT_VEC : EXSUM_VEC_PER_LANE;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_last;
   __shared__ unsigned long long s_spec[4];
@@ -752,18 +864,23 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
   const unsigned long long qb = quads * gw / nw, qe = quads * (gw + 1) / nw;
   const unsigned long long tb = qb * 4, te = min(qe * 4, n);
   if (lane == 0 && te > tb) {  // start the first batches' DRAM reads before zeroing smem
-    const uintptr_t p0 = reinterpret_cast<uintptr_t>(x + tb) & ~uintptr_t{15};
-    const uintptr_t p1 = reinterpret_cast<uintptr_t>(x + min(te, tb + 2ull * 4 * EXSUM_VEC_PER_LANE * 32));
-    const uint32_t bytes = static_cast<uint32_t>((p1 - p0 + 15) & ~uintptr_t{15});
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"(bytes) : "memory");
+    const unsigned long long tp = min(te, tb + 2ull * 4 * V * 32);
+#pragma unroll
+    for (int arr = 0; arr < (kOp >= kDot ? 2 : 1); ++arr) {
+      const double *base = arr ? y : x;
+      const uintptr_t p0 = reinterpret_cast<uintptr_t>(base + tb) & ~uintptr_t{15};
+      const uintptr_t p1 = reinterpret_cast<uintptr_t>(base + tp);
+      const uint32_t bytes = static_cast<uint32_t>((p1 - p0 + 15) & ~uintptr_t{15});
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"(bytes) : "memory");
+    }
   }
   zero_warp(wsm, lane);
   __syncwarp();
   const Lane a = lane_view(wsm, lane);
   Specials sp{~0ull, ~0ull, ~0ull};
   int norm_count = 0;
-  warp_accumulate<EXSUM_VEC_PER_LANE, EXSUM_UNIFORM_FAST != 0, true, false>(
-      x, tb, te, base_index, a, sp, norm_count, lane);
+  warp_accumulate<V, kOp == kSum && EXSUM_UNIFORM_FAST != 0, true, false, kOp>(
+      x, y, tb, te, base_index, a, sp, norm_count, lane);
 
   // K2: the warp's 67 chunk sums.
   EXSUM_STAMP(1);
@@ -808,7 +925,11 @@ exsum_sum_kernel(const double *__restrict__ x, unsigned long long n,
   const unsigned long long Nf = ~s_spec[2];
   unsigned long long payload = s_spec[3];
   if (Nf != ~0ull && Nf >= base_index && Nf - base_index < n) {
-    payload = __ldcg(reinterpret_cast<const unsigned long long *>(x) + (Nf - base_index));
+    const unsigned long long i = Nf - base_index;
+    payload = __ldcg(reinterpret_cast<const unsigned long long *>(x) + i);
+    if constexpr (kOp == kSqnorm) payload = x86_product(payload, payload);
+    if constexpr (kOp >= kDot)
+      payload = x86_product(payload, __ldcg(reinterpret_cast<const unsigned long long *>(y) + i));
     if (!finalize && lane == 0) ws->nan_payload = payload;  // first NaN so far is in this launch
   }
   if (lane == 0) ws->done = 0;
@@ -860,7 +981,8 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
     Specials sp{~0ull, ~0ull, ~0ull};
     int norm_count = 0;
     // indices local to the segment: position - b
-    warp_accumulate<EXSUM_SEG_VEC, false, EXSUM_SEG_SPLIT != 0, true>(x, b, e, 0ull - b, a, sp, norm_count, lane);
+    warp_accumulate<EXSUM_SEG_VEC, false, EXSUM_SEG_SPLIT != 0, true>(x, x, b, e, 0ull - b, a, sp,
+                                                                      norm_count, lane);
     warp_chunks(wsm, lane, row);
     const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                              N = warp_min_u64(sp.N);
@@ -933,8 +1055,14 @@ int prepare_device(int *sms) {
     int n = 0;
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
       return EXSUM_ECUDA;
-    if (cudaFuncSetAttribute(exsum_sum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(exsum_sum_kernel<kSum>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(exsum_sum_kernel<kSqnorm>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(exsum_sum_kernel<kDot>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(exsum_sum_kernel<kDotScalarB>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess ||
         cudaFuncSetAttribute(exsum_segmented_kernel,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess)
       return EXSUM_ECUDA;
@@ -959,8 +1087,9 @@ unsigned grid_for(unsigned long long n, int sms) {
 
 int sum_launch(const double *d_x, size_t n, uint64_t base_index, void *d_ws, size_t ws_bytes,
                void *stream, int finalize, double *d_result, exsum_partial *d_partial,
-               unsigned flags = 0) {
-  if (!d_ws || ws_bytes < sizeof(Workspace) || (n && !d_x)) return EXSUM_EINVAL;
+               unsigned flags = 0, int op = kSum, const double *d_y = nullptr) {
+  if (!d_ws || ws_bytes < sizeof(Workspace) || (n && !d_x) || (op >= kDot && n && !d_y))
+    return EXSUM_EINVAL;
   int sms = 0;
   const int st = prepare_device(&sms);
   if (st) return st;
@@ -976,12 +1105,34 @@ int sum_launch(const double *d_x, size_t n, uint64_t base_index, void *d_ws, siz
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
-  if (cudaLaunchKernelEx(&cfg, exsum_sum_kernel, d_x, static_cast<unsigned long long>(n),
-                         static_cast<unsigned long long>(base_index),
-                         static_cast<Workspace *>(d_ws), finalize, d_result, d_partial) !=
-      cudaSuccess)
-    return EXSUM_ECUDA;
+  const unsigned long long nn = n, bi = base_index;
+  Workspace *ws = static_cast<Workspace *>(d_ws);
+  cudaError_t e;
+  switch (op) {
+    case kSqnorm:
+      e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kSqnorm>, d_x, d_x, nn, bi, ws, finalize,
+                             d_result, d_partial);
+      break;
+    case kDot:
+      e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kDot>, d_x, d_y, nn, bi, ws, finalize,
+                             d_result, d_partial);
+      break;
+    case kDotScalarB:
+      e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kDotScalarB>, d_x, d_y, nn, bi, ws, finalize,
+                             d_result, d_partial);
+      break;
+    default:
+      e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kSum>, d_x, d_x, nn, bi, ws, finalize,
+                             d_result, d_partial);
+  }
+  if (e != cudaSuccess) return EXSUM_ECUDA;
   return launch_status();
+}
+
+int dot_op(const double *d_a, const double *d_b) {
+  return ((reinterpret_cast<uintptr_t>(d_a) ^ reinterpret_cast<uintptr_t>(d_b)) & 31u) == 0
+             ? kDot
+             : kDotScalarB;
 }
 
 }  // namespace
@@ -1007,6 +1158,20 @@ int exsum_cuda_sum_ex(const double *d_x, size_t n, uint64_t base_index, double *
                       exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
                       unsigned flags) {
   return sum_launch(d_x, n, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial, flags);
+}
+
+int exsum_cuda_sqnorm(const double *d_x, size_t n, uint64_t base_index, double *d_result,
+                      exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream) {
+  return sum_launch(d_x, n, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial, 0,
+                    kSqnorm);
+}
+
+int exsum_cuda_dot(const double *d_a, size_t na, const double *d_b, size_t nb,
+                   uint64_t base_index, double *d_result, exsum_partial *d_partial, void *d_ws,
+                   size_t ws_bytes, void *stream) {
+  if (na != nb) return EXSUM_EINVAL;  // dot: length mismatch (vector_ops.cpp:150-152)
+  return sum_launch(d_a, na, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial, 0,
+                    dot_op(d_a, d_b), d_b);
 }
 
 int exsum_cuda_accumulate(const double *d_x, size_t n, uint64_t base_index, void *d_ws,

@@ -25,7 +25,8 @@ from . import _lib
 from ._lib import ExsumPartial, lib
 from .accumulators import SmallAccumulator, bits_double
 
-__all__ = ["exact_sum", "exact_mean", "exact_sum_tensor", "exact_sum_segmented",
+__all__ = ["exact_sum", "exact_mean", "exact_sum_tensor", "exact_sum_segmented", "sqnorm", "dot",
+           "exact_sqnorm_tensor", "exact_dot_tensor",
            "merge_partials", "partial_from_tensor", "Workspace", "HostContext",
            "PARTIAL_BYTES", "WORKSPACE_BYTES"]
 
@@ -106,6 +107,68 @@ def exact_sum_tensor(x: torch.Tensor, *, base_index: int = 0, result: torch.Tens
               partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev),
               1 if overlap else 0)
     return result, partial
+
+
+def exact_sqnorm_tensor(x: torch.Tensor, *, base_index: int = 0,
+                       result: torch.Tensor | None = None, partial: torch.Tensor | None = None,
+                       workspace: Workspace | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """sqnorm(values, SumMethod::large) (vector_ops.cpp:143-146) of a CUDA float64
+    tensor: the exact sum of the rounded squares.  Returns (result, partial)."""
+    if not x.is_cuda:
+        raise ValueError("exact_sqnorm_tensor needs a CUDA tensor")
+    x = _device_tensor(x)
+    dev = x.device
+    ws = workspace or _workspace(dev)
+    result = torch.empty(1, dtype=torch.float64, device=dev) if result is None else result
+    partial = torch.empty(PARTIAL_BYTES, dtype=torch.uint8, device=dev) if partial is None else partial
+    _lib.call("exsum_cuda_sqnorm", x.data_ptr(), x.numel(), base_index, result.data_ptr(),
+              partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev))
+    return result, partial
+
+
+def exact_dot_tensor(a: torch.Tensor, b: torch.Tensor, *, base_index: int = 0,
+                     result: torch.Tensor | None = None, partial: torch.Tensor | None = None,
+                     workspace: Workspace | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """dot(a, b, SumMethod::large) (vector_ops.cpp:147-155) of two CUDA float64
+    tensors: the exact sum of the rounded products.  Raises on length mismatch
+    like the reference (std::invalid_argument there, EXSUM_EINVAL here)."""
+    if not (a.is_cuda and b.is_cuda):
+        raise ValueError("exact_dot_tensor needs CUDA tensors")
+    if a.device != b.device:
+        raise ValueError("exact_dot_tensor: tensors on different devices")
+    a, b = _device_tensor(a), _device_tensor(b)
+    dev = a.device
+    ws = workspace or _workspace(dev)
+    result = torch.empty(1, dtype=torch.float64, device=dev) if result is None else result
+    partial = torch.empty(PARTIAL_BYTES, dtype=torch.uint8, device=dev) if partial is None else partial
+    _lib.call("exsum_cuda_dot", a.data_ptr(), a.numel(), b.data_ptr(), b.numel(), base_index,
+              result.data_ptr(), partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev))
+    return result, partial
+
+
+def sqnorm(values, method: str = "large") -> float:
+    """exsum::sqnorm with an exact method: CUDA tensors on the device, host
+    arrays through the host library (exsum_sqnorm)."""
+    _check_method(method)
+    if isinstance(values, torch.Tensor) and values.is_cuda:
+        return exact_sqnorm_tensor(values)[0].item()
+    a = np.ascontiguousarray(values.numpy() if isinstance(values, torch.Tensor) else values,
+                             dtype=np.float64).reshape(-1)
+    out = C.c_double()
+    _lib.call("exsum_sqnorm", a.ctypes.data, a.size, C.byref(out))
+    return out.value
+
+
+def dot(a, b, method: str = "large") -> float:
+    """exsum::dot with an exact method (see sqnorm)."""
+    _check_method(method)
+    if isinstance(a, torch.Tensor) and a.is_cuda:
+        return exact_dot_tensor(a, b)[0].item()
+    x = np.ascontiguousarray(a.numpy() if isinstance(a, torch.Tensor) else a, dtype=np.float64).reshape(-1)
+    y = np.ascontiguousarray(b.numpy() if isinstance(b, torch.Tensor) else b, dtype=np.float64).reshape(-1)
+    out = C.c_double()
+    _lib.call("exsum_dot", x.ctypes.data, x.size, y.ctypes.data, y.size, C.byref(out))
+    return out.value
 
 
 class HostContext:
