@@ -33,6 +33,8 @@ extern "C" {
 #define EXSUM_ECUDA 2  /* a CUDA runtime call failed (no device, launch failure, ...) */
 #define EXSUM_ENOMEM 3 /* allocation failed / workspace too small */
 #define EXSUM_ENCCL 4  /* NCCL unavailable or an NCCL call failed */
+#define EXSUM_EIO 5    /* file I/O or parse failure (the reference throws std::runtime_error);
+                          exsum_io_error() has the reference's message */
 
 /* -------------------------------------------------------------- geometry */
 /* small_accumulator.hpp:27-35 and large_accumulator.hpp:27-29 */
@@ -194,6 +196,12 @@ exsum_context *exsum_context_create(int device, size_t staging_bytes);
 void exsum_context_free(exsum_context *ctx);
 int exsum_context_sum(exsum_context *ctx, const double *h_x, size_t n, double *h_result,
                       exsum_partial *h_partial);
+/* exact_sum(read_values(path, format)) without materialising the array: a bin
+ * file is read chunk by chunk into pinned host buffers that feed the staging
+ * ring (disk read, host->device copy and accumulate overlap); a text file is
+ * parsed on the host first.  *n_out (optional) receives the value count. */
+int exsum_context_sum_file(exsum_context *ctx, const char *path, int format, double *h_result,
+                           exsum_partial *h_partial, uint64_t *n_out);
 
 /* ------------------------------------------ multi-GPU (NCCL over NVLink) */
 /* parallel_exact_sum (vector_ops.cpp:172-186) with one shard per GPU (one
@@ -223,6 +231,23 @@ size_t exsum_nccl_workspace_bytes(int nranks);
 int exsum_nccl_sum(const double *d_shard, size_t n, uint64_t base_index, void *comm,
                    double *d_result, exsum_partial *d_partial, void *d_ws, size_t ws_bytes,
                    void *stream);
+
+/* ------------------------------------------------------------ value files */
+/* exsum::FileFormat (io.hpp:23-29): bin = raw little-endian doubles; text =
+ * one value per line, decimal or a 0x-prefixed 16-hex-digit bit pattern. */
+#define EXSUM_FORMAT_BIN 0
+#define EXSUM_FORMAT_TEXT 1
+/* parse_format (io.cpp:71-79): "bin" | "text" -> EXSUM_FORMAT_*, -1 otherwise. */
+int exsum_parse_format(const char *name);
+/* read_values (io.cpp:83-131): *values is malloc'ed (free with
+ * exsum_free_values), *n its length.  EXSUM_EIO on open/read/parse errors. */
+int exsum_read_values(const char *path, int format, double **values, size_t *n);
+void exsum_free_values(double *values);
+/* write_values (io.cpp:133-159): %.17g for finite values, 0x%016llx for Inf/NaN. */
+int exsum_write_values(const char *path, const double *values, size_t n, int format);
+/* Message of the last EXSUM_EIO on this thread ("<path>: <what>", as the
+ * reference's exception text). */
+const char *exsum_io_error(void);
 
 /* --------------------------------------------------- synthetic data (bench) */
 /* Seeded counter-based generators for the BASELINE.json configs (SURVEY.md

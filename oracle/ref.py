@@ -50,6 +50,10 @@ class Ref:
             "ref_segmented_sum": (None, [vp, vp, sz, vp, i32]),
             "ref_set_threads": (None, [i32]), "ref_max_threads": (i32, []),
             "ref_sqnorm": (dbl, [vp, sz, i32]),
+            "ref_read_values": (i32, [C.c_char_p, i32, C.POINTER(C.POINTER(dbl)), C.POINTER(sz),
+                                      C.c_char_p, sz]),
+            "ref_write_values": (i32, [C.c_char_p, vp, sz, i32]),
+            "ref_free": (None, [vp]),
             "ref_dot": (i32, [vp, vp, sz, sz, i32, C.POINTER(dbl)]),
             "ref_sum_ordered": (dbl, [vp, sz]), "ref_sum_unordered": (dbl, [vp, sz]),
             "ref_sum_kahan": (dbl, [vp, sz]),
@@ -113,6 +117,22 @@ class Ref:
                             0 if method == "small" else 1, C.byref(out)):
             raise ValueError("dot: length mismatch")
         return out.value
+
+    def read_values(self, path, fmt: str):
+        """(values, None) or (None, message) — io.cpp:83-131."""
+        out, n = C.POINTER(C.c_double)(), C.c_size_t()
+        msg = C.create_string_buffer(512)
+        if self.lib.ref_read_values(str(path).encode(), 1 if fmt == "text" else 0, C.byref(out),
+                                    C.byref(n), msg, 512):
+            return None, msg.value.decode()
+        vals = np.ctypeslib.as_array(out, shape=(n.value,)).copy() if n.value else np.zeros(0)
+        self.lib.ref_free(out)
+        return vals, None
+
+    def write_values(self, path, x, fmt: str) -> bool:
+        a = self._arr(x)
+        return self.lib.ref_write_values(str(path).encode(), a.ctypes.data, a.size,
+                                         1 if fmt == "text" else 0) == 0
 
     def set_threads(self, n: int) -> None:
         self.lib.ref_set_threads(n)

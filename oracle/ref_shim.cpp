@@ -13,6 +13,7 @@
 //                            vector_ops.hpp:35-75
 //   exsum::sum_ordered / sum_unordered / sum_kahan   baselines.hpp:21-35
 //   exsum::generate          generator.hpp:25-60
+//   exsum::read_values / write_values   io.hpp:31-37
 //
 // The SmallAccumulator is standard-layout and trivially copyable (560 B),
 // so it crosses this boundary as raw bytes.
@@ -29,7 +30,11 @@
 #include <omp.h>
 #endif
 
+#include <cstdlib>
+#include <string>
+
 #include "exsum/baselines.hpp"
+#include "exsum/io.hpp"
 #include "exsum/generator.hpp"
 #include "exsum/large_accumulator.hpp"
 #include "exsum/small_accumulator.hpp"
@@ -220,6 +225,36 @@ int ref_max_threads(void) {
   return 1;
 #endif
 }
+
+// read_values / write_values: 0 on success, 1 when the reference throws; the
+// message is copied to msg (msg_len bytes).  *out is malloc'ed (free with
+// ref_free).
+int ref_read_values(const char *path, int format, double **out, std::size_t *n, char *msg,
+                    std::size_t msg_len) {
+  try {
+    const std::vector<double> v =
+        exsum::read_values(path, format ? exsum::FileFormat::text : exsum::FileFormat::bin);
+    *n = v.size();
+    *out = static_cast<double *>(std::malloc(v.empty() ? 8 : v.size() * 8));
+    if (!v.empty()) std::memcpy(*out, v.data(), v.size() * 8);
+    return 0;
+  } catch (const std::exception &e) {
+    std::snprintf(msg, msg_len, "%s", e.what());
+    return 1;
+  }
+}
+
+int ref_write_values(const char *path, const double *x, std::size_t n, int format) {
+  try {
+    exsum::write_values(path, span_of(x, n),
+                        format ? exsum::FileFormat::text : exsum::FileFormat::bin);
+    return 0;
+  } catch (const std::exception &) {
+    return 1;
+  }
+}
+
+void ref_free(void *p) { std::free(p); }
 
 double ref_sqnorm(const double *x, std::size_t n, int method) {
   return exsum::sqnorm(span_of(x, n), static_cast<exsum::SumMethod>(method));

@@ -13,13 +13,14 @@ from pathlib import Path
 LIB_PATH = Path(os.environ.get("EXSUM_LIB") or
                 Path(__file__).resolve().parent / "lib" / "libexsum_b200.so")
 
-EXSUM_OK, EXSUM_EINVAL, EXSUM_ECUDA, EXSUM_ENOMEM, EXSUM_ENCCL = 0, 1, 2, 3, 4
+EXSUM_OK, EXSUM_EINVAL, EXSUM_ECUDA, EXSUM_ENOMEM, EXSUM_ENCCL, EXSUM_EIO = 0, 1, 2, 3, 4, 5
+FORMAT_BIN, FORMAT_TEXT = 0, 1
 NCCL_UNIQUE_ID_BYTES = 128
 SMALL_CHUNKS = 67
 NO_INDEX = (1 << 64) - 1
 
 _STATUS_NAMES = {EXSUM_EINVAL: "EXSUM_EINVAL", EXSUM_ECUDA: "EXSUM_ECUDA",
-                 EXSUM_ENOMEM: "EXSUM_ENOMEM", EXSUM_ENCCL: "EXSUM_ENCCL"}
+                 EXSUM_ENOMEM: "EXSUM_ENOMEM", EXSUM_ENCCL: "EXSUM_ENCCL", EXSUM_EIO: "EXSUM_EIO"}
 
 
 class ExsumSmall(C.Structure):
@@ -44,7 +45,10 @@ assert C.sizeof(ExsumPartial) == 592
 
 class ExsumError(RuntimeError):
     def __init__(self, fn: str, status: int):
-        super().__init__(f"{fn} failed: {_STATUS_NAMES.get(status, status)}")
+        msg = f"{fn} failed: {_STATUS_NAMES.get(status, status)}"
+        if status == EXSUM_EIO:
+            msg += f" ({lib.exsum_io_error().decode()})"
+        super().__init__(msg)
         self.status = status
 
 
@@ -104,6 +108,12 @@ _SIGNATURES = {
     "exsum_nccl_comm_destroy": (_i32, [_vp]),
     "exsum_nccl_workspace_bytes": (_sz, [_i32]),
     "exsum_nccl_sum": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "exsum_parse_format": (_i32, [C.c_char_p]),
+    "exsum_read_values": (_i32, [C.c_char_p, _i32, C.POINTER(_dp), C.POINTER(_sz)]),
+    "exsum_free_values": (None, [_vp]),
+    "exsum_write_values": (_i32, [C.c_char_p, _vp, _sz, _i32]),
+    "exsum_io_error": (C.c_char_p, []),
+    "exsum_context_sum_file": (_i32, [_vp, C.c_char_p, _i32, _dp, _pp, C.POINTER(_u64)]),
     "exsum_context_create": (_vp, [_i32, _sz]),
     "exsum_context_free": (None, [_vp]),
     "exsum_context_sum": (_i32, [_vp, _vp, _sz, _dp, _pp]),

@@ -24,7 +24,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = "/usr/bin/g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["sum_kernels.cu", "synth.cu", "context.cu", "nccl_sum.cu"]
-CXX_SOURCES = ["host_accumulators.cpp"]
+CXX_SOURCES = ["host_accumulators.cpp", "io.cpp"]
 HEADERS = [CSRC / "exsum_core.h", INCLUDE / "exsum_b200.h"]
 
 

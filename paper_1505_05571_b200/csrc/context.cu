@@ -11,10 +11,13 @@
 // pageable memory works but is staged by the driver.
 
 #include <cuda_runtime.h>
+#include <fcntl.h>
 #include <stdint.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <new>
+#include <string>
 
 #include "exsum_b200.h"
 
@@ -28,6 +31,8 @@ struct exsum_context {
   cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
   double *d_result = nullptr;
   exsum_partial *d_partial = nullptr;
+  double *host[2] = {nullptr, nullptr};  // pinned file-read buffers (first file sum)
+  cudaEvent_t h2d[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -38,6 +43,8 @@ void destroy(exsum_context *c) {
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);
   for (int i = 0; i < 2; ++i) {
+    if (c->host[i]) cudaFreeHost(c->host[i]);
+    if (c->h2d[i]) cudaEventDestroy(c->h2d[i]);
     if (c->stage[i]) cudaFree(c->stage[i]);
     if (c->copied[i]) cudaEventDestroy(c->copied[i]);
     if (c->consumed[i]) cudaEventDestroy(c->consumed[i]);
@@ -126,6 +133,97 @@ int exsum_context_sum(exsum_context *c, const double *h_x, size_t n, double *h_r
     st = EXSUM_ECUDA;
   if (cudaStreamSynchronize(c->compute) != cudaSuccess) st = EXSUM_ECUDA;
   cudaSetDevice(prev);
+  return st;
+}
+
+int exsum_context_sum_file(exsum_context *c, const char *path, int format, double *h_result,
+                           exsum_partial *h_partial, uint64_t *n_out) {
+  if (!c || !path || (!h_result && !h_partial)) return EXSUM_EINVAL;
+  if (format == EXSUM_FORMAT_TEXT) {
+    double *v = nullptr;
+    size_t n = 0;
+    int st = exsum_read_values(path, format, &v, &n);
+    if (st == EXSUM_OK) st = exsum_context_sum(c, v, n, h_result, h_partial);
+    exsum_free_values(v);
+    if (st == EXSUM_OK && n_out) *n_out = n;
+    return st;
+  }
+  if (format != EXSUM_FORMAT_BIN) return EXSUM_EINVAL;
+  // bin: validate like read_values (io.cpp:94-99), then stream
+  double *probe = nullptr;
+  size_t dummy = 0;
+  const int fd = open(path, O_RDONLY);
+  if (fd < 0) return exsum_read_values(path, format, &probe, &dummy);  // sets the message
+  const off_t size = lseek(fd, 0, SEEK_END);
+  if (size < 0 || size % 8 != 0) {
+    close(fd);
+    return exsum_read_values(path, format, &probe, &dummy);
+  }
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(c->device) != cudaSuccess) {
+    close(fd);
+    return EXSUM_ECUDA;
+  }
+  int st = EXSUM_OK;
+  for (int i = 0; i < 2 && st == EXSUM_OK; ++i) {
+    if (!c->host[i] &&
+        (cudaMallocHost(&c->host[i], c->stage_elems * sizeof(double)) != cudaSuccess ||
+         cudaEventCreateWithFlags(&c->h2d[i], cudaEventDisableTiming) != cudaSuccess))
+      st = EXSUM_ECUDA;
+  }
+  const size_t n = static_cast<size_t>(size) / 8;
+  size_t off = 0;
+  int i = 0;
+  while (off < n && st == EXSUM_OK) {
+    const size_t len = (n - off < c->stage_elems) ? n - off : c->stage_elems;
+    const int b = i & 1;
+    // the host buffer is free once its previous host->device copy completed
+    if (i >= 2 && cudaEventSynchronize(c->h2d[b]) != cudaSuccess) {
+      st = EXSUM_ECUDA;
+      break;
+    }
+    size_t got = 0;
+    char *dst = reinterpret_cast<char *>(c->host[b]);
+    while (got < len * 8) {
+      const ssize_t r = pread(fd, dst + got, len * 8 - got, static_cast<off_t>(off * 8 + got));
+      if (r <= 0) break;
+      got += static_cast<size_t>(r);
+    }
+    if (got != len * 8) {
+      st = EXSUM_EIO;
+      break;
+    }
+    if (cudaStreamWaitEvent(c->copy, c->consumed[b], 0) != cudaSuccess ||
+        cudaMemcpyAsync(c->stage[b], c->host[b], len * sizeof(double), cudaMemcpyHostToDevice,
+                        c->copy) != cudaSuccess ||
+        cudaEventRecord(c->h2d[b], c->copy) != cudaSuccess ||
+        cudaEventRecord(c->copied[b], c->copy) != cudaSuccess ||
+        cudaStreamWaitEvent(c->compute, c->copied[b], 0) != cudaSuccess) {
+      st = EXSUM_ECUDA;
+      break;
+    }
+    st = exsum_cuda_accumulate(c->stage[b], len, off, c->ws, c->ws_bytes, c->compute);
+    if (st == EXSUM_OK && cudaEventRecord(c->consumed[b], c->compute) != cudaSuccess)
+      st = EXSUM_ECUDA;
+    off += len;
+    ++i;
+  }
+  close(fd);
+  if (st == EXSUM_OK)
+    st = exsum_cuda_finalize(c->d_result, c->d_partial, c->ws, c->ws_bytes, c->compute);
+  if (st == EXSUM_OK && h_result &&
+      cudaMemcpyAsync(h_result, c->d_result, sizeof(double), cudaMemcpyDeviceToHost,
+                      c->compute) != cudaSuccess)
+    st = EXSUM_ECUDA;
+  if (st == EXSUM_OK && h_partial &&
+      cudaMemcpyAsync(h_partial, c->d_partial, sizeof(exsum_partial), cudaMemcpyDeviceToHost,
+                      c->compute) != cudaSuccess)
+    st = EXSUM_ECUDA;
+  if (cudaStreamSynchronize(c->compute) != cudaSuccess && st == EXSUM_OK) st = EXSUM_ECUDA;
+  if (cudaStreamSynchronize(c->copy) != cudaSuccess && st == EXSUM_OK) st = EXSUM_ECUDA;
+  cudaSetDevice(prev);
+  if (st == EXSUM_OK && n_out) *n_out = n;
   return st;
 }
 

@@ -26,7 +26,8 @@ from ._lib import ExsumPartial, lib
 from .accumulators import SmallAccumulator, bits_double
 
 __all__ = ["exact_sum", "exact_mean", "exact_sum_tensor", "exact_sum_segmented", "sqnorm", "dot",
-           "exact_sqnorm_tensor", "exact_dot_tensor",
+           "exact_sqnorm_tensor", "exact_dot_tensor", "read_values", "write_values",
+           "exact_sum_file",
            "merge_partials", "partial_from_tensor", "Workspace", "HostContext",
            "PARTIAL_BYTES", "WORKSPACE_BYTES"]
 
@@ -171,6 +172,35 @@ def dot(a, b, method: str = "large") -> float:
     return out.value
 
 
+def _format(fmt: str) -> int:
+    code = lib.exsum_parse_format(fmt.encode())
+    if code < 0:
+        raise ValueError(f"unknown format: {fmt}")  # io.cpp:71-79
+    return code
+
+
+def read_values(path, fmt: str = "bin") -> np.ndarray:
+    """exsum::read_values (io.cpp:83-131); raises ExsumError (EXSUM_EIO, with the
+    reference's message) where the reference throws std::runtime_error."""
+    ptr, n = C.POINTER(C.c_double)(), C.c_size_t()
+    _lib.call("exsum_read_values", str(path).encode(), _format(fmt), C.byref(ptr), C.byref(n))
+    try:
+        return np.ctypeslib.as_array(ptr, shape=(n.value,)).copy() if n.value else np.zeros(0)
+    finally:
+        lib.exsum_free_values(ptr)
+
+
+def write_values(path, values, fmt: str = "bin") -> None:
+    """exsum::write_values (io.cpp:133-159)."""
+    a = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
+    _lib.call("exsum_write_values", str(path).encode(), a.ctypes.data, a.size, _format(fmt))
+
+
+def exact_sum_file(path, fmt: str = "bin", *, device: int = 0) -> float:
+    """Exact sum of a value file on the device (exsum_context_sum_file)."""
+    return _host_context(device).sum_file(path, fmt)[0]
+
+
 class HostContext:
     """exsum_context: device workspace + staging ring for host-resident arrays."""
 
@@ -199,6 +229,15 @@ class HostContext:
         out = C.c_double()
         _lib.call("exsum_context_sum", self._h, ptr, n, C.byref(out), None)
         return out.value
+
+    def sum_file(self, path, fmt: str = "bin", want_partial: bool = False):
+        """exact_sum(read_values(path, fmt)) — a bin file streams from disk through
+        pinned buffers into the device accumulate.  Returns (result, n[, partial])."""
+        out, n = C.c_double(), C.c_uint64()
+        part = ExsumPartial()
+        _lib.call("exsum_context_sum_file", self._h, str(path).encode(), _format(fmt),
+                  C.byref(out), C.byref(part) if want_partial else None, C.byref(n))
+        return (out.value, n.value, part) if want_partial else (out.value, n.value)
 
 
 _ctx_cache: dict[int, HostContext] = {}
