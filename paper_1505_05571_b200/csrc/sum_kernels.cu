@@ -97,20 +97,27 @@ __device__ __forceinline__ uint32_t exponent_field(uint32_t hi) { return (hi >> 
 
 // ------------------------------------------------------ lane accumulators
 
-constexpr int kWarps = 8;
+#ifndef EXSUM_WARPS
+#define EXSUM_WARPS 8  // warps per CTA (one CTA per SM)
+#endif
+#ifndef EXSUM_SLOTS
+#define EXSUM_SLOTS 66  // 65: one carry-only slot (fits a 9th warp in shared memory)
+#endif
+constexpr int kWarps = EXSUM_WARPS;
 constexpr int kThreads = kWarps * 32;
-constexpr int kSlots = 66;  // slots 0..63 take terms (e' >> 5), 64..65 only carries
+constexpr int kSlots = EXSUM_SLOTS;  // slots 0..63 take terms (e' >> 5), the rest only carries
+static_assert(kSlots == 65 || kSlots == 66, "slot count");
 constexpr int kLPlane = kSlots * 32 * 4;
 constexpr int kHPlane = kSlots * 32 * 8;
 constexpr int kWarpSmem = kLPlane + kHPlane;            // 25,344 B
 constexpr int kScratch = kWarps * kChunks * 8;          // per-warp chunk rows
-constexpr int kSmem = kWarps * kWarpSmem + kScratch;    // 207,040 B
+constexpr int kSmem = kWarps * kWarpSmem + kScratch;    // 207,040 B (8 warps, 66 slots)
 constexpr int kPrefetchBatches = EXSUM_PREFETCH_BATCHES;
 constexpr int kUniformBackoff = EXSUM_UNIFORM_BACKOFF;
 
 #if EXSUM_TIMELINE
 // [warp][0..3]: start, loop end, flush end (after the CTA's REDs), last-CTA end
-__device__ unsigned long long g_timeline[148 * 8 * 4 + 8];
+__device__ unsigned long long g_timeline[148 * 16 * 4 + 8];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -225,7 +232,9 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
       : "memory");
 }
 
-// Carry upward: L_k in [0, 2^32), H_k = 0 for k < 65; slot 65 keeps the rest.
+// Carry upward: L_k in [0, 2^32), H_k = 0 below the top slot, which keeps the
+// rest (with 65 slots: slot 64 holds up to 2^95 units of 2^973 > any finite
+// lane sum, 2^1024 x 2^31 terms).
 // Safe whenever every slot has absorbed <= 2047 terms (|H_k| < 2^63 - 2^52).
 __device__ __forceinline__ void normalize(const Lane &a) {
   long long c = 0;
@@ -288,7 +297,7 @@ __device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, int lane, 
     if (lane == 0) lo1 = wl;
     if (lane < 2) hi2 = wh;
     long long v = sl[r] + lo1 + hi2;
-    if (r == 2) {
+    if (kSlots == 66 && r == 2) {
       const long long top = __shfl_sync(0xffffffffu, shh[2], 1);  // high words of slot 65
       if (c == kChunks - 1) v += top * 4294967296ll;
     }

@@ -273,3 +273,34 @@ def test_nccl_sum_world1_and_graph(cuda, checker):
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ maximum size
+
+def test_more_than_2_pow_32_terms(cuda):
+    """n > 2^32 (34 GB in HBM): the full sum equals the merge of two shards below
+    2^32 terms, and Inf/NaN first indices above 2^32 are not truncated."""
+    n = (1 << 32) + (1 << 20) + 3
+    if torch.cuda.get_device_properties(0).total_memory < 40 * 2**30:
+        pytest.skip("needs > 40 GB of device memory")
+    x = gen(2, n, 5)
+    full, _ = dev_sum(x)
+    cut = (1 << 31) + 12345
+    recs = [ops.exact_sum_tensor(x[:cut], base_index=0)[1],
+            ops.exact_sum_tensor(x[cut:], base_index=cut)[1]]
+    merged, _ = ops.merge_partials(torch.stack(recs))
+    assert bits_of(merged.item()) == full
+    assert 2.0e9 < ops.bits_to_float(full) < 2.4e9
+    # first-NaN rule across the 2^32 boundary: payload B (index 10) must win over
+    # payload A (index 2^32 + 3); a 32-bit index would pick A.
+    xi = x.view(torch.int64)  # write the payloads bit-exactly
+    xi[(1 << 32) + 3] = 0x7FF0000000000AAA
+    xi[10] = 0x7FF0000000000BBB
+    got, part = dev_sum(x)
+    assert got == 0x7FF0000000000BBB
+    assert part.first_nan == 10
+    x[10] = 0.5
+    got, part = dev_sum(x)
+    assert got == 0x7FF0000000000AAA and part.first_nan == (1 << 32) + 3
+    del x
+    torch.cuda.empty_cache()
