@@ -43,6 +43,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
+
 #include "exsum_b200.h"
 #include "exsum_core.h"
 
@@ -1053,14 +1056,21 @@ using namespace exsum_b200::dev;
 namespace {
 
 constexpr int kMaxDevices = 64;
-int g_num_sms[kMaxDevices] = {};
-bool g_configured[kMaxDevices] = {};
+std::atomic<int> g_num_sms[kMaxDevices] = {};  // 0 = not configured yet
+std::mutex g_configure_mutex;
 
 // Per-device one-time setup: SM count and the >48 KB dynamic smem opt-in.
+// Thread-safe: the fast path is one atomic load; first use takes a mutex.
 int prepare_device(int *sms) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return EXSUM_ECUDA;
-  if (!g_configured[dev]) {
+  int ready = g_num_sms[dev].load(std::memory_order_acquire);
+  if (ready > 0) {
+    *sms = ready;
+    return EXSUM_OK;
+  }
+  std::lock_guard<std::mutex> lock(g_configure_mutex);
+  if (g_num_sms[dev].load(std::memory_order_relaxed) == 0) {
     int n = 0;
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
       return EXSUM_ECUDA;
@@ -1075,10 +1085,9 @@ int prepare_device(int *sms) {
         cudaFuncSetAttribute(exsum_segmented_kernel,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess)
       return EXSUM_ECUDA;
-    g_num_sms[dev] = n;
-    g_configured[dev] = true;
+    g_num_sms[dev].store(n, std::memory_order_release);
   }
-  *sms = g_num_sms[dev];
+  *sms = g_num_sms[dev].load(std::memory_order_relaxed);
   return EXSUM_OK;
 }
 

@@ -22,6 +22,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <mutex>
+
 #include "exsum_b200.h"
 
 #if defined(__CUDA_ARCH__)
@@ -162,7 +164,6 @@ __global__ void gen_kernel(int config, uint64_t seed, uint64_t n_total, uint64_t
 }
 
 __constant__ double c_pow10[601];
-bool g_pow10_ready = false;
 
 __global__ void gen5_kernel(uint64_t seed, uint64_t first, uint64_t count, double *out) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -234,15 +235,23 @@ int exsum_host_gen_offsets(uint64_t seed, size_t nseg, uint64_t lo, uint64_t hi,
 int exsum_cuda_gen_segmented(uint64_t seed, uint64_t first, size_t count, double *d_out,
                              void *stream) {
   if (count && !d_out) return EXSUM_EINVAL;
-  if (!g_pow10_ready) {
-    double p[601];
-    char buf[16];
-    for (int k = -300; k <= 300; ++k) {
-      snprintf(buf, sizeof buf, "1e%d", k);
-      p[k + 300] = strtod(buf, nullptr);  // correctly rounded
+  {
+    // 10^k table, once per device (the __constant__ symbol is per device)
+    static std::mutex m;
+    static bool ready[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return EXSUM_ECUDA;
+    std::lock_guard<std::mutex> lock(m);
+    if (!ready[dev]) {
+      double p[601];
+      char buf[16];
+      for (int k = -300; k <= 300; ++k) {
+        snprintf(buf, sizeof buf, "1e%d", k);
+        p[k + 300] = strtod(buf, nullptr);  // correctly rounded
+      }
+      if (cudaMemcpyToSymbol(c_pow10, p, sizeof p) != cudaSuccess) return EXSUM_ECUDA;
+      ready[dev] = true;
     }
-    if (cudaMemcpyToSymbol(c_pow10, p, sizeof p) != cudaSuccess) return EXSUM_ECUDA;
-    g_pow10_ready = true;
   }
   if (count == 0) return EXSUM_OK;
   gen5_kernel<<<gen_grid(count), 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, first, count,
