@@ -530,6 +530,25 @@ __device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, cons
   }
 }
 
+// Products of a freshly loaded batch, in place (x words := product words), so
+// that the one-slot test, the register fast path and the rolling body see
+// plain terms.  Refills still load the raw inputs (load_vec<kOp>).
+template <int V, int kOp>
+__device__ __forceinline__ void products_in_place(Batch<V, kOp> &b) {
+  if constexpr (kOp != kSum) {
+#pragma unroll
+    for (int u = 0; u < V; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t lo, hi;
+        term_bits<kOp>(b.w[u][2 * q], b.w[u][2 * q + 1], b.y[kOp >= kDot ? u : 0][2 * q],
+                       b.y[kOp >= kDot ? u : 0][2 * q + 1], lo, hi);
+        b.w[u][2 * q] = lo;
+        b.w[u][2 * q + 1] = hi;
+      }
+  }
+}
+
 // Add one batch (registers b) with rolling refill from vector nv onward.  kGuard:
 // bounds-checked refills (only the last batches need it).  Returns the batch's
 // maximum exponent field (2047 iff it contained an Inf/NaN term).
@@ -542,9 +561,9 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
   for (int u = 0; u < V; ++u) {
     uint32_t lo[4], hi[4], e[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      term_bits<kOp>(b.w[u][2 * q], b.w[u][2 * q + 1], b.y[kOp >= kDot ? u : 0][2 * q],
-                     b.y[kOp >= kDot ? u : 0][2 * q + 1], lo[q], hi[q]);
+    for (int q = 0; q < 4; ++q) {  // terms: products already in place (products_in_place)
+      lo[q] = b.w[u][2 * q];
+      hi[q] = b.w[u][2 * q + 1];
       e[q] = exponent_field(hi[q]);
       emax = max(emax, e[q]);
     }
@@ -562,10 +581,10 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
 
 // Register fast path: every lane's batch lies in slot k (|sum| < 2^89 per lane):
 // sum it in registers, then one read-modify-write.  Refills are unguarded.
-template <int V>
-__device__ __forceinline__ void batch_uniform(const Lane &a, Batch<V> &b, const double *X4,
-                                              long long nv, int lane, uint32_t k) {
-  const double *pn = X4 + 4 * (nv + lane);
+template <int V, int kOp>
+__device__ __forceinline__ void batch_uniform(const Lane &a, Batch<V, kOp> &b, const double *X4,
+                                              const double *Y4, long long nv, int lane,
+                                              uint32_t k) {
   uint32_t r0 = 0, r1 = 0, r2 = 0;
 #pragma unroll
   for (int u = 0; u < V; ++u) {
@@ -579,7 +598,7 @@ __device__ __forceinline__ void batch_uniform(const Lane &a, Batch<V> &b, const 
           : "+r"(r0), "+r"(r1), "+r"(r2)
           : "r"(sg), "r"(u0), "r"(u1), "r"(u2));
     }
-    ldg256(pn + 4 * 32 * u, b.w[u]);
+    load_vec<V, kOp>(b, u, X4, Y4, nv + u * 32 + lane);
   }
   slot_add96(a, k, r0, r1, r2);
 }
@@ -588,8 +607,8 @@ __device__ __forceinline__ void batch_uniform(const Lane &a, Batch<V> &b, const 
 // (hi bits 25..30; e = 0 maps to slot 0 like e' = 1).  All terms share a slot
 // iff the AND and the OR of their high words agree on those bits; slot 63 may
 // hold Inf/NaN and never counts as uniform.  Returns the slot bits or ~0u.
-template <int V>
-__device__ __forceinline__ uint32_t uniform_slot(const Batch<V> &b) {
+template <int V, int kOp>
+__device__ __forceinline__ uint32_t uniform_slot(const Batch<V, kOp> &b) {
   uint32_t hor = 0u, hand = 0xFFFFFFFFu;
 #pragma unroll
   for (int u = 0; u < V; ++u)
@@ -619,7 +638,6 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
                                                 Specials &sp, int &norm_count, int lane) {
   constexpr int kNormEvery = 2016 / (4 * V);  // batches between renormalisations
   static_assert(kNormEvery >= 1, "batch too large for the carry budget");
-  static_assert(kOp == kSum || !kUniform, "one-slot fast path: plain sums only");
   if (begin >= end) return;
   // Scalar head up to 32-byte alignment of &x[pos], scalar tail after the vectors.
   const uintptr_t addr = reinterpret_cast<uintptr_t>(x + begin);
@@ -646,6 +664,7 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
   for (long long v = 0; v < nvec; v += kStep) {
     const long long nv = v + kStep;
     if (lane == 0) prefetch_batch<V, kOp>(X4, Y4, v + (kPrefetchBatches + 1) * kStep, nvec);
+    products_in_place<V, kOp>(b);
     uint32_t emax = 0;
     const bool steady = nv + kStep <= nvec;  // next batch complete: unguarded refills
     uint32_t k = ~0u;
@@ -654,14 +673,14 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
         if (backoff > 0) {
           --backoff;
         } else {
-          k = uniform_slot<V>(b);
+          k = uniform_slot<V, kOp>(b);
           if (!__all_sync(0xffffffffu, k != ~0u)) {
             k = ~0u;
             backoff = kUniformBackoff;  // wide data rarely turns uniform
           }
         }
       }
-      if (k != ~0u) batch_uniform<V>(a, b, X4, nv, lane, k);
+      if (k != ~0u) batch_uniform<V, kOp>(a, b, X4, Y4, nv, lane, k);
     }
     if (k == ~0u) {
       if (kSplit && steady) {
@@ -891,7 +910,7 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
   const Lane a = lane_view(wsm, lane);
   Specials sp{~0ull, ~0ull, ~0ull};
   int norm_count = 0;
-  warp_accumulate<V, kOp == kSum && EXSUM_UNIFORM_FAST != 0, true, false, kOp>(
+  warp_accumulate<V, EXSUM_UNIFORM_FAST != 0, true, false, kOp>(
       x, y, tb, te, base_index, a, sp, norm_count, lane);
 
   // K2: the warp's 67 chunk sums.
