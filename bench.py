@@ -57,6 +57,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--nccl", action="store_true",
                    help="use the exsum_nccl_sum step even at N=1 (1-rank communicator)")
+    p.add_argument("--p2p", action="store_true",
+                   help="exchange records with exsum_p2p_sum (fused, NVLink peer memory) "
+                        "instead of NCCL; also at N=1 (1-rank group)")
     return p.parse_args()
 
 
@@ -387,7 +390,8 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1505_05571_b200 import _lib, ops
-    from paper_1505_05571_b200.distributed import NcclCommunicator, nccl_exact_sum, shard_bounds
+    from paper_1505_05571_b200.distributed import (NcclCommunicator, P2PGroup, nccl_exact_sum,
+                                                   p2p_exact_sum, shard_bounds)
 
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -411,9 +415,12 @@ def main():
     # N > 1: one exsum_nccl_sum per step — shard sum kernel, ncclAllGather of the
     # 592-byte records, merge kernel — inside the C library (the C-ABI form of
     # parallel_exact_sum); every rank ends with the full array's exact sum.
-    comm = NcclCommunicator(dev) if (world > 1 or args.nccl) else None
+    p2p = P2PGroup(dev) if args.p2p else None
+    comm = NcclCommunicator(dev) if (p2p is None and (world > 1 or args.nccl)) else None
 
     def step():
+        if p2p is not None:
+            return p2p_exact_sum(x, p2p, base_index=begin, result=res, overlap=True)
         if comm is not None:
             return nccl_exact_sum(x, comm, base_index=begin, result=res)
         ops.exact_sum_tensor(x, base_index=begin, result=res, partial=part, workspace=ws,
@@ -447,7 +454,7 @@ def main():
     # dominant kernel: average duration per launch over the timed region (for N = 1
     # the step IS the sum kernel; launches overlap their epilogues, so per-launch
     # events would serialise them).  For N > 1 the kernel is timed in its own loop.
-    if comm is None:
+    if comm is None and p2p is None:
         k_ms = ms / steps
     else:
         ks, ke = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -521,7 +528,11 @@ def main():
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded counter-based generator, BASELINE.json shapes)",
             "config": {"workload": wl["desc"], "n_total": n_total, "n_per_gpu": n_local,
-                       "parallelism": f"shard{world}" + (" + exsum_nccl_sum (ncclAllGather of 592 B records + merge kernel)" if comm is not None else ""),
+                       "parallelism": f"shard{world}" + (
+                           " + exsum_p2p_sum (records over NVLink peer memory, merged in the sum kernel)"
+                           if p2p is not None else
+                           " + exsum_nccl_sum (ncclAllGather of 592 B records + merge kernel)"
+                           if comm is not None else ""),
                        "l2": "inputs >= 800 MB per GPU > 126 MB L2; no flush needed"},
             "terms_per_s": round(value * 1e9 / 8, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
@@ -531,7 +542,7 @@ def main():
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": steps * (2 if comm is not None else 1),
+            "gpu_launches": steps * (2 if comm is not None else 1),  # p2p: 1 per step
             "clocks": clocks.report(),
             "result_bits": hex(result_bits),
             "bit_exact_vs_oracle": parity,
@@ -539,6 +550,10 @@ def main():
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()
+    if p2p is not None:
+        if p2p.error_epoch():
+            print("exsum_p2p_sum: a peer never published (timeout)", file=sys.stderr)
+        p2p.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -249,6 +249,42 @@ int exsum_write_values(const char *path, const double *values, size_t n, int for
  * reference's exception text). */
 const char *exsum_io_error(void);
 
+/* ------------------------------- multi-GPU, fused exchange over peer memory */
+/* parallel_exact_sum as ONE launch per rank: the sum kernel's last CTA writes
+ * the rank's 592 B record into every rank's mailbox over NVLink peer memory,
+ * publishes it with a system-scope release flag carrying `epoch`, waits for
+ * every rank's flag (bounded: 10 s, then the result is NaN 0x7FF80000DEAD0000
+ * and the mailbox error word holds the epoch) and merges the records in place
+ * — the exchange of exsum_nccl_sum without a separate collective.
+ * mailboxes: host array of nranks device pointers, [r] = rank r's mailbox
+ * mapped into this process (its own for r == rank; exsum_ipc_open for peers);
+ * each of exsum_p2p_mailbox_bytes(nranks) bytes, zeroed once.  epoch: 1, 2, 3,
+ * ... per call, the same on every rank.  nranks <= 8.  flags: EXSUM_SUM_OVERLAP
+ * as for exsum_cuda_sum_ex (safe across calls: the mailboxes are double-buffered). */
+size_t exsum_p2p_mailbox_bytes(int nranks);
+/* A zeroed mailbox as its own cudaMalloc allocation (exportable with IPC). */
+int exsum_p2p_mailbox_alloc(int nranks, void **d_mailbox);
+int exsum_p2p_mailbox_free(void *d_mailbox);
+int exsum_p2p_sum(const double *d_shard, size_t n, uint64_t base_index, int rank, int nranks,
+                  void *const *mailboxes, uint64_t epoch, double *d_result,
+                  exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
+                  unsigned flags);
+/* The same protocol with nranks emulated ranks in ONE cooperative launch on one
+ * GPU (rank r sums d_x[bounds[r], bounds[r+1]); d_mailboxes: nranks contiguous
+ * mailboxes; d_ws: nranks contiguous workspaces; outputs: nranks results /
+ * records, all equal).  For testing the exchange where only one GPU exists. */
+int exsum_p2p_emulate_sum(const double *d_x, const uint64_t *bounds, int nranks, uint64_t epoch,
+                          double *d_results, exsum_partial *d_partials, void *d_mailboxes,
+                          void *d_ws, size_t ws_bytes, void *stream);
+/* The mailbox's error word: 0, or the epoch of a call that timed out. */
+int exsum_p2p_error(const void *d_mailbox, int nranks, uint64_t *epoch_out, void *stream);
+/* cudaIpcMemHandle_t (64 bytes) of a cudaMalloc'ed mailbox, and its mapping in
+ * another process (cudaIpcOpenMemHandle, peer access enabled lazily). */
+#define EXSUM_IPC_HANDLE_BYTES 64
+int exsum_ipc_get_handle(const void *d_ptr, void *handle);
+int exsum_ipc_open(const void *handle, void **d_ptr);
+int exsum_ipc_close(void *d_ptr);
+
 /* --------------------------------------------------- synthetic data (bench) */
 /* Seeded counter-based generators for the BASELINE.json configs (SURVEY.md
  * §8(d)); the value at index i depends only on (config, seed, i, n), so shards

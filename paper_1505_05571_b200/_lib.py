@@ -108,6 +108,17 @@ _SIGNATURES = {
     "exsum_nccl_comm_destroy": (_i32, [_vp]),
     "exsum_nccl_workspace_bytes": (_sz, [_i32]),
     "exsum_nccl_sum": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "exsum_p2p_mailbox_bytes": (_sz, [_i32]),
+    "exsum_p2p_mailbox_alloc": (_i32, [_i32, C.POINTER(_vp)]),
+    "exsum_p2p_mailbox_free": (_i32, [_vp]),
+    "exsum_p2p_sum": (_i32, [_vp, _sz, _u64, _i32, _i32, C.POINTER(_vp), _u64, _vp, _vp, _vp, _sz,
+                             _vp, C.c_uint]),
+    "exsum_p2p_emulate_sum": (_i32, [_vp, C.POINTER(_u64), _i32, _u64, _vp, _vp, _vp, _vp, _sz,
+                                     _vp]),
+    "exsum_p2p_error": (_i32, [_vp, _i32, C.POINTER(_u64), _vp]),
+    "exsum_ipc_get_handle": (_i32, [_vp, _vp]),
+    "exsum_ipc_open": (_i32, [_vp, C.POINTER(_vp)]),
+    "exsum_ipc_close": (_i32, [_vp]),
     "exsum_parse_format": (_i32, [C.c_char_p]),
     "exsum_read_values": (_i32, [C.c_char_p, _i32, C.POINTER(_dp), C.POINTER(_sz)]),
     "exsum_free_values": (None, [_vp]),
@@ -124,8 +135,16 @@ _SIGNATURES = {
     "exsum_version": (C.c_char_p, []),
 }
 
+# The product library must export every symbol (a stale build fails loudly).
+# An older build selected with EXSUM_LIB (timing comparisons) may lack newer ones.
+_LENIENT = bool(os.environ.get("EXSUM_LIB"))
 for _name, (_res, _args) in _SIGNATURES.items():
-    _f = getattr(lib, _name)
+    try:
+        _f = getattr(lib, _name)
+    except AttributeError:
+        if _LENIENT:
+            continue
+        raise
     _f.restype = _res
     _f.argtypes = _args
 

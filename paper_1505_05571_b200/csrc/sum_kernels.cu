@@ -43,6 +43,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string.h>
+
 #include <atomic>
 #include <mutex>
 
@@ -870,13 +872,160 @@ __device__ void warp_emit(const long long *row, unsigned long long P, unsigned l
 
 // --------------------------------------------------------------- K1 + K2 + K3
 
+// ------------------------------------------------- multi-GPU exchange (P2P)
+//
+// exsum_p2p_sum fuses parallel_exact_sum's exchange into the sum kernel: the
+// last CTA of each rank writes its canonical 592-byte record into every rank's
+// mailbox over peer memory (NVLink stores), publishes it with a system-scope
+// flag carrying the call's epoch, waits for every rank's flag and merges the
+// records in place (merge_partials, vector_ops.cpp:64-70, with index-ordered
+// specials) — one launch per rank and step, no separate collective.
+// Mailbox of a rank (exsum_p2p_mailbox_bytes): two record sets and two flag
+// sets selected by epoch parity, so a rank that is one step ahead never writes
+// into the set its peers are still reading; then an error word.
+constexpr int kMaxRanks = 8;
+constexpr unsigned long long kP2PTimeoutNs = 10ull * 1000 * 1000 * 1000;  // 10 s
+
+struct GroupArgs {  // grid split into independent sums (emulated ranks); groups = 1 otherwise
+  int groups;
+  unsigned long long off[kMaxRanks + 1];  // groups > 1: group g sums x[off[g], off[g+1])
+};
+
+struct P2PArgs {
+  int nranks;  // 0: no exchange
+  int rank;    // this process's rank; group g of an emulation is rank g
+  unsigned long long epoch;
+  unsigned char *mailbox[kMaxRanks];  // rank r's mailbox, mapped into this process
+};
+
+__host__ __device__ constexpr size_t p2p_flags_offset(int nranks) {
+  return (2 * static_cast<size_t>(nranks) * sizeof(exsum_partial) + 255) & ~size_t{255};
+}
+__host__ __device__ constexpr size_t p2p_error_offset(int nranks) {
+  return p2p_flags_offset(nranks) + 2 * static_cast<size_t>(nranks) * 8;
+}
+__host__ __device__ constexpr size_t p2p_mailbox_bytes(int nranks) {
+  return (p2p_error_offset(nranks) + 8 + 255) & ~size_t{255};
+}
+__device__ __forceinline__ exsum_partial *p2p_record(unsigned char *mb, int nranks, int set,
+                                                     int r) {
+  return reinterpret_cast<exsum_partial *>(mb) + set * nranks + r;
+}
+__device__ __forceinline__ unsigned long long *p2p_flag(unsigned char *mb, int nranks, int set,
+                                                        int r) {
+  return reinterpret_cast<unsigned long long *>(mb + p2p_flags_offset(nranks)) + set * nranks + r;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Warp 0 of a rank's last CTA: publish this rank's record (own = its slot in
+// this rank's own mailbox, already written by warp_emit), wait for all ranks,
+// merge into row/P/M/N/payload for the final warp_emit.  Returns false on a
+// timeout (a peer never published), after flagging the mailbox's error word.
+__device__ bool p2p_exchange(const P2PArgs &p2p, int me, long long *row, unsigned long long &P,
+                             unsigned long long &M, unsigned long long &N,
+                             unsigned long long &payload, int lane) {
+  const int R = p2p.nranks;
+  const int set = static_cast<int>(p2p.epoch & 1);
+  const unsigned long long *own = reinterpret_cast<const unsigned long long *>(
+      p2p_record(p2p.mailbox[me], R, set, me));
+  constexpr int kWords = sizeof(exsum_partial) / 8;  // 74
+  __syncwarp();
+  // 1. the record into every other rank's slot [set][me] (peer stores)
+  for (int r = 0; r < R; ++r) {
+    if (r == me) continue;
+    unsigned long long *dst =
+        reinterpret_cast<unsigned long long *>(p2p_record(p2p.mailbox[r], R, set, me));
+    for (int w = lane; w < kWords; w += 32) dst[w] = __ldcg(own + w);
+  }
+  __threadfence_system();  // each lane's record stores are visible everywhere ...
+  __syncwarp();
+  // 2. ... before this rank's flag in every mailbox
+  if (lane < R) st_release_sys(p2p_flag(p2p.mailbox[lane], R, set, me), p2p.epoch);
+  // 3. wait for every rank's flag in the own mailbox (bounded)
+  bool ok = true;
+  if (lane < R) {
+    const unsigned long long *f = p2p_flag(p2p.mailbox[me], R, set, lane);
+    const unsigned long long t0 = global_ns();
+    while (ld_acquire_sys(f) != p2p.epoch) {
+      if (global_ns() - t0 > kP2PTimeoutNs) {
+        ok = false;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  ok = __all_sync(0xffffffffu, ok);
+  __threadfence_system();  // acquire side for every lane's record reads
+  if (!ok) {
+    if (lane == 0)
+      *reinterpret_cast<unsigned long long *>(p2p.mailbox[me] + p2p_error_offset(R)) = p2p.epoch;
+    return false;
+  }
+  // 4. merge: chunk sums and first indices over the ranks' records
+  for (int c = lane; c < kChunks; c += 32) {
+    long long sum = 0;
+    for (int r = 0; r < R; ++r)
+      sum += static_cast<long long>(
+          __ldcv(reinterpret_cast<const unsigned long long *>(p2p_record(p2p.mailbox[me], R, set, r)) + c));
+    row[c] = sum;
+  }
+  unsigned long long Pm = ~0ull, Mm = ~0ull, Nm = ~0ull, pay = 0;
+  for (int r = 0; r < R; ++r) {
+    const unsigned long long *rec = reinterpret_cast<const unsigned long long *>(
+        p2p_record(p2p.mailbox[me], R, set, r));
+    constexpr int kTail = sizeof(exsum_small) / 8;  // first_pos_inf, first_neg_inf, first_nan, payload
+    const unsigned long long pi = __ldcv(rec + kTail), ni = __ldcv(rec + kTail + 1);
+    const unsigned long long qi = __ldcv(rec + kTail + 2), py = __ldcv(rec + kTail + 3);
+    Pm = min(Pm, pi);
+    Mm = min(Mm, ni);
+    if (qi < Nm) {
+      Nm = qi;
+      pay = py;
+    }
+  }
+  P = Pm;
+  M = Mm;
+  N = Nm;
+  payload = pay;
+  __syncwarp();
+  return true;
+}
+
 template <int kOp>
 __global__ void __launch_bounds__(kThreads, 1)
 exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, unsigned long long n,
                  unsigned long long base_index, Workspace *__restrict__ ws, int finalize,
-                 double *result, exsum_partial *partial) {
+                 double *result, exsum_partial *partial, const __grid_constant__ GroupArgs grp,
+                 const __grid_constant__ P2PArgs p2p) {
   // vectors per lane per batch: a dot keeps two arrays' vectors in registers
   constexpr int V = kOp >= kDot ? EXSUM_DOT_VEC : EXSUM_VEC_PER_LANE;
+  // Independent sums per CTA group (groups > 1 only when emulating ranks in one
+  // cooperative launch): this CTA's group, its index and the group's grid size.
+  const unsigned gctas = gridDim.x / static_cast<unsigned>(grp.groups);
+  const int g = static_cast<int>(blockIdx.x / gctas);
+  const unsigned bid = blockIdx.x - static_cast<unsigned>(g) * gctas;
+  if (grp.groups > 1) {
+    x += grp.off[g];
+    if (kOp >= kDot) y += grp.off[g];
+    n = grp.off[g + 1] - grp.off[g];
+    base_index = grp.off[g];
+    ws += g;
+    result = result ? result + g : nullptr;
+    partial = partial ? partial + g : nullptr;
+  }
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ int s_last;
   __shared__ unsigned long long s_spec[4];
@@ -889,8 +1038,8 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
   asm volatile("griddepcontrol.launch_dependents;");
   EXSUM_STAMP(0);
   // K1: contiguous per-warp ranges, boundaries on 4-term multiples.
-  const unsigned long long gw = static_cast<unsigned long long>(blockIdx.x) * kWarps + warp;
-  const unsigned long long nw = static_cast<unsigned long long>(gridDim.x) * kWarps;
+  const unsigned long long gw = static_cast<unsigned long long>(bid) * kWarps + warp;
+  const unsigned long long nw = static_cast<unsigned long long>(gctas) * kWarps;
   const unsigned long long quads = (n + 3) >> 2;
   const unsigned long long qb = quads * gw / nw, qe = quads * (gw + 1) / nw;
   const unsigned long long tb = qb * 4, te = min(qe * 4, n);
@@ -937,7 +1086,7 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
   __threadfence();
   __syncthreads();
   EXSUM_STAMP(2);
-  if (threadIdx.x == 0) s_last = atomicAdd(&ws->done, 1u) == gridDim.x - 1;
+  if (threadIdx.x == 0) s_last = atomicAdd(&ws->done, 1u) == gctas - 1;
   __syncthreads();
   if (!s_last) return;
   // Last CTA: gather the workspace in parallel, then one thread rounds.
@@ -965,6 +1114,19 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
   }
   if (lane == 0) ws->done = 0;
   if (!finalize) return;
+  if (p2p.nranks > 0) {
+    // this rank's canonical record into its own mailbox slot, then exchange
+    const int me = p2p.rank + g;
+    warp_emit(scratch, ~s_spec[0], ~s_spec[1], Nf, payload, nullptr,
+              p2p_record(p2p.mailbox[me], p2p.nranks, static_cast<int>(p2p.epoch & 1), me), lane);
+    unsigned long long P = 0, M = 0, N = 0, pay = 0;
+    if (!p2p_exchange(p2p, me, scratch, P, M, N, pay, lane)) {
+      if (lane == 0 && result) *result = __longlong_as_double(0x7FF80000DEAD0000ll);
+      return;
+    }
+    warp_emit(scratch, P, M, N, pay, result, partial, lane);
+    return;
+  }
   warp_emit(scratch, ~s_spec[0], ~s_spec[1], Nf, payload, result, partial, lane);
   EXSUM_STAMP(3);
 }
@@ -1124,43 +1286,57 @@ unsigned grid_for(unsigned long long n, int sms) {
 
 int sum_launch(const double *d_x, size_t n, uint64_t base_index, void *d_ws, size_t ws_bytes,
                void *stream, int finalize, double *d_result, exsum_partial *d_partial,
-               unsigned flags = 0, int op = kSum, const double *d_y = nullptr) {
+               unsigned flags = 0, int op = kSum, const double *d_y = nullptr,
+               const P2PArgs *p2p = nullptr, const GroupArgs *grp = nullptr,
+               bool cooperative = false) {
   if (!d_ws || ws_bytes < sizeof(Workspace) || (n && !d_x) || (op >= kDot && n && !d_y))
     return EXSUM_EINVAL;
   int sms = 0;
   const int st = prepare_device(&sms);
   if (st) return st;
+  GroupArgs g1 = {};
+  g1.groups = 1;
+  const GroupArgs G = grp ? *grp : g1;
+  const P2PArgs X = p2p ? *p2p : P2PArgs{};
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid_for(n, sms));
+  // emulated ranks: the whole SM set split into equal co-resident groups
+  cfg.gridDim = dim3(G.groups > 1 ? (sms / G.groups) * G.groups : grid_for(n, sms));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = static_cast<cudaStream_t>(stream);
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  int na = 0;
   if (flags & EXSUM_SUM_OVERLAP) {
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
   }
+  if (cooperative) {  // CTAs wait on one another: all must be resident
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = na ? attr : nullptr;
+  cfg.numAttrs = na;
   const unsigned long long nn = n, bi = base_index;
   Workspace *ws = static_cast<Workspace *>(d_ws);
   cudaError_t e;
   switch (op) {
     case kSqnorm:
       e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kSqnorm>, d_x, d_x, nn, bi, ws, finalize,
-                             d_result, d_partial);
+                             d_result, d_partial, G, X);
       break;
     case kDot:
       e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kDot>, d_x, d_y, nn, bi, ws, finalize,
-                             d_result, d_partial);
+                             d_result, d_partial, G, X);
       break;
     case kDotScalarB:
       e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kDotScalarB>, d_x, d_y, nn, bi, ws, finalize,
-                             d_result, d_partial);
+                             d_result, d_partial, G, X);
       break;
     default:
       e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kSum>, d_x, d_x, nn, bi, ws, finalize,
-                             d_result, d_partial);
+                             d_result, d_partial, G, X);
   }
   if (e != cudaSuccess) return EXSUM_ECUDA;
   return launch_status();
@@ -1209,6 +1385,101 @@ int exsum_cuda_dot(const double *d_a, size_t na, const double *d_b, size_t nb,
   if (na != nb) return EXSUM_EINVAL;  // dot: length mismatch (vector_ops.cpp:150-152)
   return sum_launch(d_a, na, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial, 0,
                     dot_op(d_a, d_b), d_b);
+}
+
+size_t exsum_p2p_mailbox_bytes(int nranks) {
+  return nranks < 1 || nranks > kMaxRanks ? 0 : p2p_mailbox_bytes(nranks);
+}
+
+int exsum_p2p_mailbox_alloc(int nranks, void **d_mailbox) {
+  if (!d_mailbox || nranks < 1 || nranks > kMaxRanks) return EXSUM_EINVAL;
+  *d_mailbox = nullptr;
+  const size_t bytes = p2p_mailbox_bytes(nranks);
+  if (cudaMalloc(d_mailbox, bytes) != cudaSuccess) return EXSUM_ENOMEM;
+  if (cudaMemset(*d_mailbox, 0, bytes) != cudaSuccess) {
+    cudaFree(*d_mailbox);
+    *d_mailbox = nullptr;
+    return EXSUM_ECUDA;
+  }
+  return EXSUM_OK;
+}
+
+int exsum_p2p_mailbox_free(void *d_mailbox) {
+  if (!d_mailbox) return EXSUM_EINVAL;
+  return cudaFree(d_mailbox) == cudaSuccess ? EXSUM_OK : EXSUM_ECUDA;
+}
+
+int exsum_p2p_sum(const double *d_shard, size_t n, uint64_t base_index, int rank, int nranks,
+                  void *const *mailboxes, uint64_t epoch, double *d_result,
+                  exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
+                  unsigned flags) {
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || !mailboxes || epoch == 0)
+    return EXSUM_EINVAL;
+  P2PArgs X = {};
+  X.nranks = nranks;
+  X.rank = rank;
+  X.epoch = epoch;
+  for (int r = 0; r < nranks; ++r) {
+    if (!mailboxes[r]) return EXSUM_EINVAL;
+    X.mailbox[r] = static_cast<unsigned char *>(mailboxes[r]);
+  }
+  return sum_launch(d_shard, n, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial,
+                    flags, kSum, nullptr, &X);
+}
+
+int exsum_p2p_emulate_sum(const double *d_x, const uint64_t *bounds, int nranks, uint64_t epoch,
+                          double *d_results, exsum_partial *d_partials, void *d_mailboxes,
+                          void *d_ws, size_t ws_bytes, void *stream) {
+  if (nranks < 1 || nranks > kMaxRanks || !bounds || !d_mailboxes || !d_ws || epoch == 0 ||
+      ws_bytes < nranks * sizeof(Workspace))
+    return EXSUM_EINVAL;
+  GroupArgs G = {};
+  G.groups = nranks;
+  P2PArgs X = {};
+  X.nranks = nranks;
+  X.rank = 0;
+  X.epoch = epoch;
+  for (int r = 0; r <= nranks; ++r) {
+    if (r && bounds[r] < bounds[r - 1]) return EXSUM_EINVAL;
+    G.off[r] = bounds[r];
+  }
+  for (int r = 0; r < nranks; ++r)
+    X.mailbox[r] = static_cast<unsigned char *>(d_mailboxes) + r * p2p_mailbox_bytes(nranks);
+  return sum_launch(d_x, bounds[nranks] - bounds[0], bounds[0], d_ws, sizeof(Workspace), stream,
+                    1, d_results, d_partials, 0, kSum, nullptr, &X, &G, true);
+}
+
+int exsum_p2p_error(const void *d_mailbox, int nranks, uint64_t *epoch_out, void *stream) {
+  if (!d_mailbox || !epoch_out || nranks < 1 || nranks > kMaxRanks) return EXSUM_EINVAL;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(epoch_out, static_cast<const unsigned char *>(d_mailbox) +
+                                     p2p_error_offset(nranks),
+                      8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return EXSUM_ECUDA;
+  return EXSUM_OK;
+}
+
+int exsum_ipc_get_handle(const void *d_ptr, void *handle) {
+  if (!d_ptr || !handle) return EXSUM_EINVAL;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void *>(d_ptr)) != cudaSuccess) return EXSUM_ECUDA;
+  memcpy(handle, &h, sizeof h);
+  return EXSUM_OK;
+}
+
+int exsum_ipc_open(const void *handle, void **d_ptr) {
+  if (!handle || !d_ptr) return EXSUM_EINVAL;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  return cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess
+             ? EXSUM_OK
+             : EXSUM_ECUDA;
+}
+
+int exsum_ipc_close(void *d_ptr) {
+  if (!d_ptr) return EXSUM_EINVAL;
+  return cudaIpcCloseMemHandle(d_ptr) == cudaSuccess ? EXSUM_OK : EXSUM_ECUDA;
 }
 
 int exsum_cuda_accumulate(const double *d_x, size_t n, uint64_t base_index, void *d_ws,

@@ -27,7 +27,7 @@ from ._lib import ExsumPartial
 from .ops import PARTIAL_BYTES, exact_sum_tensor, merge_partials, partial_from_tensor
 
 __all__ = ["shard_bounds", "exchange_partials", "merge_records", "parallel_exact_sum",
-           "NcclCommunicator", "nccl_exact_sum"]
+           "NcclCommunicator", "nccl_exact_sum", "P2PGroup", "p2p_exact_sum"]
 
 
 def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -141,4 +141,83 @@ def nccl_exact_sum(shard: torch.Tensor, comm: NcclCommunicator, *, base_index: i
     _lib.call("exsum_nccl_sum", x.data_ptr() if x.numel() else None, x.numel(), base_index,
               comm.comm, result.data_ptr(), record.data_ptr() if record is not None else None,
               comm.workspace.data_ptr(), comm.workspace.numel(), stream)
+    return result
+
+
+class P2PGroup:
+    """Mailboxes for exsum_p2p_sum.  Each rank allocates its own mailbox as a
+    whole cudaMalloc allocation (exsum_p2p_mailbox_alloc: IPC exports
+    allocations, not sub-blocks of torch's caching allocator), exports it with
+    exsum_ipc_get_handle, and maps every peer's with exsum_ipc_open; the
+    64-byte handles travel over the torch.distributed group.  World size 1 (or
+    no process group) needs no IPC."""
+
+    def __init__(self, device: torch.device, group=None):
+        single = not dist.is_initialized()
+        self.rank = 0 if single else dist.get_rank(group)
+        self.world = 1 if single else dist.get_world_size(group)
+        if self.world > 8:
+            raise ValueError("exsum_p2p_sum supports up to 8 ranks")
+        self.device = torch.device(device)
+        own = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.call("exsum_p2p_mailbox_alloc", self.world, C.byref(own))
+        self._own = own.value
+        self.ptrs = [0] * self.world
+        self.ptrs[self.rank] = self._own
+        self._opened = []
+        if self.world > 1:
+            h = (C.c_char * 64)()
+            _lib.call("exsum_ipc_get_handle", self._own, h)
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(h.raw), group=group)
+            for r, hb in enumerate(handles):
+                if r == self.rank:
+                    continue
+                p = C.c_void_p()
+                with torch.cuda.device(self.device):
+                    _lib.call("exsum_ipc_open", (C.c_char * 64).from_buffer_copy(hb), C.byref(p))
+                self.ptrs[r] = p.value
+                self._opened.append(p.value)
+            dist.barrier(group=group)  # every mailbox mapped before anyone writes
+        self.epoch = 0
+        nbytes = int(_lib.lib.exsum_cuda_workspace_bytes())
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            _lib.call("exsum_cuda_workspace_init", self.workspace.data_ptr(), nbytes,
+                      torch.cuda.current_stream(self.device).cuda_stream)
+
+    def close(self) -> None:
+        for p in self._opened:
+            _lib.call("exsum_ipc_close", p)
+        self._opened = []
+        if self._own:
+            _lib.call("exsum_p2p_mailbox_free", self._own)
+            self._own = None
+
+    def error_epoch(self) -> int:
+        """0, or the epoch of a call that timed out waiting for a peer."""
+        out = C.c_uint64()
+        _lib.call("exsum_p2p_error", self._own, self.world, C.byref(out),
+                  torch.cuda.current_stream(self.device).cuda_stream)
+        return out.value
+
+
+def p2p_exact_sum(shard: torch.Tensor, grp: P2PGroup, *, base_index: int,
+                  result: torch.Tensor | None = None,
+                  record: torch.Tensor | None = None, overlap: bool = False) -> torch.Tensor:
+    """exsum_p2p_sum: one launch per rank — shard sum, record exchange over
+    peer memory, merge.  Every rank gets the full array's exact sum."""
+    if not shard.is_cuda or shard.dtype != torch.float64:
+        raise ValueError("p2p_exact_sum: shard must be a CUDA float64 tensor")
+    x = shard.contiguous()
+    if result is None:
+        result = torch.empty(1, dtype=torch.float64, device=x.device)
+    grp.epoch += 1
+    ptrs = (C.c_void_p * grp.world)(*grp.ptrs)
+    _lib.call("exsum_p2p_sum", x.data_ptr() if x.numel() else None, x.numel(), base_index,
+              grp.rank, grp.world, ptrs, grp.epoch, result.data_ptr(),
+              record.data_ptr() if record is not None else None, grp.workspace.data_ptr(),
+              grp.workspace.numel(), torch.cuda.current_stream(x.device).cuda_stream,
+              1 if overlap else 0)
     return result
