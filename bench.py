@@ -190,6 +190,99 @@ def run_reference_arm(args, wl, n_total):
     print(json.dumps(line), flush=True)
 
 
+def run_small(args, wl, impl: str):
+    """Config 1: the small-superaccumulator case, N = 1e3.  One
+    step = one exact sum: SmallAccumulator() + add(span) + round()
+    (small_accumulator.cpp:174-189, 330-348) through the host C ABI (ours:
+    exsum_small_*; reference arm: the compiled reference, oracle/_ref).  Reported
+    per sum; the device path's latency for the same 1000 terms is listed too."""
+    import ctypes as C
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1505_05571_b200 import _lib
+    from paper_1505_05571_b200._lib import ExsumSmall
+    n = int(args.n) if args.n else wl["n"]
+    x = np.empty(n, dtype=np.float64)
+    _lib.call("exsum_host_gen", 1, args.seed, n, 0, n, x.ctypes.data)
+    steps = args.steps or 100_000
+    if impl == "reference":
+        from oracle import ref as R
+        r = R.get()
+        acc = (C.c_char * 560)()
+
+        def one():
+            r.lib.ref_small_init(acc)
+            r.lib.ref_small_add_array(acc, x.ctypes.data, n)
+            return r.lib.ref_small_round(acc)
+    else:
+        acc = ExsumSmall()
+        out = C.c_double()
+        lib = _lib.lib
+
+        def one():
+            lib.exsum_small_init(C.byref(acc))
+            lib.exsum_small_add_array(C.byref(acc), x.ctypes.data, n)
+            lib.exsum_small_round(C.byref(acc), C.byref(out))
+            return out.value
+    for _ in range(max(args.warmup, 3)):
+        res = one()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        res = one()
+    el = time.perf_counter() - t0
+    us = el / steps * 1e6
+    gbs = 8.0 * n / (el / steps) / 1e9
+    line = {
+        "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": 1, "steps": steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round(us / 1e3, 6),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded counter-based generator, BASELINE.json shapes)",
+        "config": {"workload": wl["desc"], "n_total": n,
+                   "parallelism": "1 host thread (small accumulator; no device)"},
+        "us_per_sum": round(us, 3),
+        "result_bits": hex(bits(res)),
+    }
+    if impl == "reference":
+        line.update({"impl": "reference",
+                     "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": 1,
+                                      "kind": "reference",
+                                      "sample": f"SmallAccumulator add(span)+round of {n} terms x {steps}"},
+                     "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                             "d2h_bytes_per_step": 0}})
+    else:
+        import torch
+        from paper_1505_05571_b200 import ops
+        xd = torch.from_numpy(x).cuda()
+        resd = torch.empty(1, dtype=torch.float64, device="cuda")
+        part = torch.empty(ops.PARTIAL_BYTES, dtype=torch.uint8, device="cuda")
+        ws = ops.Workspace(xd.device)
+        for _ in range(20):
+            ops.exact_sum_tensor(xd, result=resd, partial=part, workspace=ws, overlap=True)
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        for _ in range(2000):
+            ops.exact_sum_tensor(xd, result=resd, partial=part, workspace=ws, overlap=True)
+        en.record()
+        torch.cuda.synchronize()
+        dev_us = st.elapsed_time(en) / 2000 * 1e3
+        from oracle.port import checker
+        chk = checker()
+        line.update({
+            "device_us_per_sum": round(dev_us, 3),
+            "bit_exact_vs_oracle": bits(res) == bits(chk.exact_sum(x, "small"))
+            and bits(resd.item()) == bits(res),
+            "roofline": {"bound": "latency", "achieved": round(8.0 * n / (dev_us * 1e3), 3),
+                         "peak": None, "unit": "GB/s", "frac": None, "traffic": None,
+                         "kernel": "exsum_sum_kernel (1 CTA)", "kernel_ms": round(dev_us / 1e3, 6)},
+            "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0,
+                    "path": "host C ABI exsum_small_* (config 1 is the CPU-side case)"},
+            "gpu_launches": 0,
+        })
+    print(json.dumps(line), flush=True)
+
+
 def run_reference_segmented(args, wl, chk, threads):
     """Reference CPU arm for config 5: exact_sum(large) per segment, OpenMP over
     segments on a bounded sample of the segment list.  The
@@ -382,6 +475,8 @@ def main():
         raise SystemExit("--gpus > 1 must be launched with torch.distributed.run (one rank per GPU)")
     n_arg = int(args.n) if args.n else wl["n"]
     n_total = n_arg * world if wl["per_gpu"] else n_arg
+    if args.config == 1:
+        return run_small(args, wl, args.impl)
     if args.impl == "reference":
         return run_reference_arm(args, wl, n_total)
     if args.config == 5:
