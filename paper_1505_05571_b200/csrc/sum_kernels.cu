@@ -69,6 +69,9 @@
 #ifndef EXSUM_UNIFORM_FAST
 #define EXSUM_UNIFORM_FAST 1  // single-sum kernel: register fast path for one-slot batches
 #endif
+#ifndef EXSUM_XOR_LOP
+#define EXSUM_XOR_LOP 1  // sign complement with two LOP3 (ALU) instead of LEA + 2 IMAD (FMA)
+#endif
 #ifndef EXSUM_TIMELINE
 #define EXSUM_TIMELINE 0  // diagnostics build: per-warp %globaltimer stamps (scripts/timeline.py)
 #endif
@@ -173,10 +176,12 @@ __device__ __forceinline__ void zero_warp(unsigned char *warp_smem, int lane) {
 
 // The term as three 32-bit words of its complemented, shifted significand
 // (u2:u1:u0 = s ? ~(m << sh) : m << sh; a negative term's +1 is the carry-in
-// s + s) and e' = max(e, 1).  Pipe-balanced: the B200 integer ALU pipe and the
-// FMA pipe each retire 16 lanes/clk/SMSP (measured, profiles/r01_pipe_probe_*):
-// SHF/LOP3/IADD3/VIMNMX on the ALU pipe, IMAD (x ^ s = x (2s + 1) + s for
-// s in {0,-1}) on the FMA pipe.
+// s + s) and e' = max(e, 1).  The B200 integer ALU pipe and the FMA pipe each
+// retire 16 lanes/clk/SMSP (measured, profiles/r01_pipe_probe_*); the decode
+// keeps a few IMADs on the FMA pipe, but the sign complement is two LOP3s: one
+// instruction fewer per term than IMAD-based xor (x (2s + 1) + s), which
+// measured faster both in bursts and under the power cap
+// (profiles/r01_variants_xorlop.log).
 __device__ __forceinline__ void decode96(uint32_t lo, uint32_t hi, uint32_t e, uint32_t &s,
                                          uint32_t &u0, uint32_t &u1, uint32_t &u2,
                                          uint32_t &ep) {
@@ -186,9 +191,15 @@ __device__ __forceinline__ void decode96(uint32_t lo, uint32_t hi, uint32_t e, u
   asm("mad.lo.u32 %0, %1, -1, %2;" : "=r"(d) : "r"(e), "r"(ep));          // FMA: 1 iff e == 0
   asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x100000u));  // (a&b)|c
   asm("mad.lo.u32 %0, %1, -1048576, %2;" : "=r"(mh) : "r"(d), "r"(mhi));  // FMA: drop implicit 1
+#if EXSUM_XOR_LOP
+  (void)m1;
+  asm("xor.b32 %0, %1, %2;" : "=r"(lx) : "r"(lo), "r"(s));                 // ALU: lo ^ s
+  asm("xor.b32 %0, %1, %2;" : "=r"(mx) : "r"(mh), "r"(s));                 // ALU: mh ^ s
+#else
   asm("mad.lo.u32 %0, %1, 2, 1;" : "=r"(m1) : "r"(s));                    // FMA: +-1
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(lx) : "r"(lo), "r"(m1), "r"(s));  // FMA: lo ^ s
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(mx) : "r"(mh), "r"(m1), "r"(s));  // FMA: mh ^ s
+#endif
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(s), "r"(lx), "r"(ep));   // shift mod 32
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lx), "r"(mx), "r"(ep));
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mx), "r"(s), "r"(ep));

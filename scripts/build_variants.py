@@ -11,6 +11,7 @@ VARIANTS = {
     "backoff15": ("EXSUM_UNIFORM_BACKOFF=15",),
     "timeline": ("EXSUM_TIMELINE=1",),
     "seg4": ("EXSUM_SEG_VEC=4",),
+    "xorimad": ("EXSUM_XOR_LOP=0",),
     "w8s65": ("EXSUM_SLOTS=65",),
     "w9v8": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9"),
     "w9v7": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9", "EXSUM_VEC_PER_LANE=7"),
