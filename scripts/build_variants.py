@@ -2,8 +2,14 @@
 import sys
 from pathlib import Path
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
-from paper_1505_05571_b200.build import build_variant  # noqa: E402
+import importlib.util  # noqa: E402
+
+# build.py by path: importing the package would load the library it builds
+_spec = importlib.util.spec_from_file_location(
+    "_exsum_b200_build", Path(__file__).resolve().parents[1] / "paper_1505_05571_b200" / "build.py")
+_builder = importlib.util.module_from_spec(_spec)
+_spec.loader.exec_module(_builder)
+build_variant = _builder.build_variant
 
 VARIANTS = {
     "nofast": ("EXSUM_UNIFORM_FAST=0",),
