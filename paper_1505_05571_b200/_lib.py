@@ -55,7 +55,7 @@ class ExsumError(RuntimeError):
 def _load() -> C.CDLL:
     if not LIB_PATH.exists():
         raise ImportError(
-            f"{LIB_PATH} is missing: build it with `python -m paper_1505_05571_b200.build` "
+            f"{LIB_PATH} is missing: build it with `python paper_1505_05571_b200/build.py` "
             "(the exact-sum path has no CPU fallback)")
     return C.CDLL(str(LIB_PATH))
 
