@@ -102,6 +102,14 @@ int exsum_large_round(exsum_large *acc, double *out);
 int exsum_large_mean(exsum_large *acc, uint64_t n, double *out);
 /* LargeAccumulator::small() — large_accumulator.hpp:75-76 (copy out) */
 int exsum_large_small(const exsum_large *acc, exsum_small *out);
+/* LargeAccumulator::counts()[ix] — large_accumulator.hpp:79-81: adds left
+ * before the chunk transfers (4096 on first use, counting down), -1 = unused. */
+int exsum_large_count(const exsum_large *acc, int ix, int *count);
+/* LargeAccumulator::chunk_in_use(ix) — large_accumulator.hpp:82-84 (0 or 1). */
+int exsum_large_chunk_in_use(const exsum_large *acc, int ix);
+/* LargeAccumulator::chunk_word(ix) — large_accumulator.hpp:85-86: the wrapped
+ * sum of raw bit patterns; meaningful only while the chunk is in use. */
+int exsum_large_chunk_word(const exsum_large *acc, int ix, uint64_t *word);
 /* LargeAccumulator::chunks_in_use — large_accumulator.cpp:143-149 */
 int exsum_large_chunks_in_use(const exsum_large *acc);
 

@@ -42,6 +42,8 @@ class Ref:
             "ref_large_drain": (None, [vp]), "ref_large_round": (dbl, [vp]),
             "ref_large_small": (None, [vp, vp]), "ref_large_count": (i32, [vp, i32]),
             "ref_large_chunks_in_use": (i32, [vp]),
+            "ref_large_chunk_in_use": (i32, [vp, i32]),
+            "ref_large_chunk_word": (u64, [vp, i32]),
             "ref_exact_sum": (dbl, [vp, sz, i32]),
             "ref_exact_mean": (i32, [vp, sz, i32, C.POINTER(dbl)]),
             "ref_parallel_exact_sum": (dbl, [vp, sz, i32, sz]),

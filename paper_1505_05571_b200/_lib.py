@@ -86,6 +86,9 @@ _SIGNATURES = {
     "exsum_large_mean": (_i32, [_vp, _u64, _dp]),
     "exsum_large_small": (_i32, [_vp, _sp]),
     "exsum_large_chunks_in_use": (_i32, [_vp]),
+    "exsum_large_count": (_i32, [_vp, _i32, C.POINTER(_i32)]),
+    "exsum_large_chunk_in_use": (_i32, [_vp, _i32]),
+    "exsum_large_chunk_word": (_i32, [_vp, _i32, C.POINTER(_u64)]),
     "exsum_sqnorm": (_i32, [_vp, _sz, _dp]),
     "exsum_dot": (_i32, [_vp, _sz, _vp, _sz, _dp]),
     "exsum_partial_from_array": (_i32, [_vp, _sz, _u64, _pp]),

@@ -177,3 +177,20 @@ class LargeAccumulator:
 
     def chunks_in_use(self) -> int:
         return lib.exsum_large_chunks_in_use(self._h)
+
+    def count(self, ix: int) -> int:
+        """counts()[ix] (large_accumulator.hpp:79-81)."""
+        c = C.c_int()
+        _lib.call("exsum_large_count", self._h, ix, C.byref(c))
+        return c.value
+
+    def counts(self) -> list[int]:
+        return [self.count(ix) for ix in range(4096)]
+
+    def chunk_in_use(self, ix: int) -> bool:
+        return bool(lib.exsum_large_chunk_in_use(self._h, ix))
+
+    def chunk_word(self, ix: int) -> int:
+        w = C.c_uint64()
+        _lib.call("exsum_large_chunk_word", self._h, ix, C.byref(w))
+        return w.value

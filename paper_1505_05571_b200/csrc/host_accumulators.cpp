@@ -355,6 +355,23 @@ int exsum_large_small(const exsum_large *acc, exsum_small *out) {
   return EXSUM_OK;
 }
 
+int exsum_large_count(const exsum_large *acc, int ix, int *count) {
+  if (!acc || !count || ix < 0 || ix >= kBins) return EXSUM_EINVAL;
+  *count = acc->left[ix];
+  return EXSUM_OK;
+}
+
+int exsum_large_chunk_in_use(const exsum_large *acc, int ix) {
+  if (!acc || ix < 0 || ix >= kBins) return 0;
+  return static_cast<int>((acc->used[ix >> 6] >> (ix & 63)) & 1u);
+}
+
+int exsum_large_chunk_word(const exsum_large *acc, int ix, uint64_t *word) {
+  if (!acc || !word || ix < 0 || ix >= kBins) return EXSUM_EINVAL;
+  *word = acc->word[ix];
+  return EXSUM_OK;
+}
+
 int exsum_large_chunks_in_use(const exsum_large *acc) {
   if (!acc) return 0;
   int used = 0;

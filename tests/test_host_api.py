@@ -245,3 +245,33 @@ def test_criterion8_budget_stress():
     s.add(v)
     assert s.adds_until_propagate() == 2046
     assert s.round() == 2048 * v
+
+
+def test_large_introspection_matches_reference():
+    """counts() / chunk_in_use / chunk_word (large_accumulator.hpp:79-86) equal the
+    reference's after the same adds; SPEC.md:240 (count after the first add is
+    4095) and :251 (the 4096-ones chunk word is 0 mod 2^64 before its transfer)."""
+    from oracle import ref as R
+    L = LargeAccumulator()
+    L.add(1.0)
+    assert L.count(0x3FF) == 4095 and L.chunk_in_use(0x3FF) and L.count(0x400) == -1
+    L = LargeAccumulator()
+    L.add_array([1.0] * 4096)
+    assert L.count(0x3FF) == 0 and L.chunk_word(0x3FF) == 0
+    if not R.available():
+        pytest.skip("compiled reference not built")
+    r = R.get()
+    rng = np.random.default_rng(5)
+    x = _random_doubles(rng, 20_000)
+    x[::997] = 1.0
+    for n in (0, 1, 7, 4097, 20_000):
+        L = LargeAccumulator()
+        L.add_array(x[:n])
+        h = r.lib.ref_large_new()
+        r.lib.ref_large_add_array(h, np.ascontiguousarray(x[:n]).ctypes.data, n)
+        for ix in range(4096):
+            assert L.count(ix) == r.lib.ref_large_count(h, ix), (n, ix)
+            assert L.chunk_in_use(ix) == bool(r.lib.ref_large_chunk_in_use(h, ix)), (n, ix)
+            if L.chunk_in_use(ix):
+                assert L.chunk_word(ix) == r.lib.ref_large_chunk_word(h, ix), (n, ix)
+        r.lib.ref_large_free(h)
