@@ -1287,7 +1287,20 @@ int launch_status() { return cudaGetLastError() == cudaSuccess ? EXSUM_OK : EXSU
 
 // Grid for a sum of n terms: one CTA per SM, fewer for small inputs (keep at
 // least ~4 K terms per warp so the per-CTA fixed cost stays amortised).
-unsigned grid_for(unsigned long long n, int sms) {
+#ifndef EXSUM_MAX_CTAS
+#define EXSUM_MAX_CTAS 0  // experiment: cap the sum grid below the SM count (0 = no cap)
+#endif
+#ifndef EXSUM_OVERLAP_SHORT
+#define EXSUM_OVERLAP_SHORT 150000000ull  // overlapped sums up to this many terms leave SMs free
+#endif
+// Overlapped (programmatic dependent launch) sums of up to EXSUM_OVERLAP_SHORT
+// terms run on 8/9 of the SMs: the free SMs let the next sum in the stream start
+// streaming while this one drains, which outweighs their share of a short sum
+// (config 2 sustained +4%, 30 M terms +20%); longer or non-overlapped sums use
+// every SM (profiles/r01_grid_sweep.log).
+unsigned grid_for(unsigned long long n, int sms, bool overlap = false) {
+  if (EXSUM_MAX_CTAS > 0 && sms > EXSUM_MAX_CTAS) sms = EXSUM_MAX_CTAS;
+  if (overlap && n <= EXSUM_OVERLAP_SHORT) sms -= sms / 9;
   const unsigned long long per_cta = 4096ull * kWarps;
   unsigned long long g = (n + per_cta - 1) / per_cta;
   if (g < 1) g = 1;
@@ -1311,7 +1324,8 @@ int sum_launch(const double *d_x, size_t n, uint64_t base_index, void *d_ws, siz
   const P2PArgs X = p2p ? *p2p : P2PArgs{};
   cudaLaunchConfig_t cfg = {};
   // emulated ranks: the whole SM set split into equal co-resident groups
-  cfg.gridDim = dim3(G.groups > 1 ? (sms / G.groups) * G.groups : grid_for(n, sms));
+  cfg.gridDim = dim3(G.groups > 1 ? (sms / G.groups) * G.groups
+                                   : grid_for(n, sms, (flags & EXSUM_SUM_OVERLAP) != 0));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = static_cast<cudaStream_t>(stream);

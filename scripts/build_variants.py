@@ -18,6 +18,8 @@ VARIANTS = {
     "timeline": ("EXSUM_TIMELINE=1",),
     "seg4": ("EXSUM_SEG_VEC=4",),
     "xorimad": ("EXSUM_XOR_LOP=0",),
+    "cta132": ("EXSUM_MAX_CTAS=132",),
+    "fullgrid": ("EXSUM_OVERLAP_SHORT=0",),
     "w8s65": ("EXSUM_SLOTS=65",),
     "w9v8": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9"),
     "w9v7": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9", "EXSUM_VEC_PER_LANE=7"),
