@@ -56,10 +56,12 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--nccl", action="store_true",
-                   help="use the exsum_nccl_sum step even at N=1 (1-rank communicator)")
+                   help="exchange records with exsum_nccl_sum (NCCL all-gather + merge kernel); "
+                        "also at N=1 (1-rank communicator).  Default at N>1: the fused "
+                        "exsum_p2p_sum, checked against NCCL once, NCCL if the check fails")
     p.add_argument("--p2p", action="store_true",
-                   help="exchange records with exsum_p2p_sum (fused, NVLink peer memory) "
-                        "instead of NCCL; also at N=1 (1-rank group)")
+                   help="exsum_p2p_sum (fused, NVLink peer memory) also at N=1 (1-rank group); "
+                        "with --nccl: check the two against each other first")
     return p.parse_args()
 
 
@@ -511,8 +513,35 @@ def main():
     # N > 1: one exsum_nccl_sum per step — shard sum kernel, ncclAllGather of the
     # 592-byte records, merge kernel — inside the C library (the C-ABI form of
     # parallel_exact_sum); every rank ends with the full array's exact sum.
-    p2p = P2PGroup(dev) if args.p2p else None
-    comm = NcclCommunicator(dev) if (p2p is None and (world > 1 or args.nccl)) else None
+    # N > 1: the fused peer-memory exchange (exsum_p2p_sum) is preferred; it is
+    # checked once against the NCCL step on this box (collectively: every rank
+    # must agree bit for bit) and NCCL is used if the check or the setup fails.
+    p2p, comm, exchange_note = None, None, None
+    if world > 1 or args.nccl or args.p2p:
+        want_p2p = args.p2p or (world > 1 and not args.nccl)
+        if want_p2p:
+            try:
+                p2p = P2PGroup(dev)
+            except Exception as exc:  # noqa: BLE001  (IPC / peer access unavailable)
+                exchange_note = f"p2p setup failed ({type(exc).__name__}); NCCL used"
+                p2p = None
+        if world > 1 or args.nccl or p2p is None:
+            comm = NcclCommunicator(dev)
+        if p2p is not None and comm is not None:
+            r_p2p = bits(float(p2p_exact_sum(x, p2p, base_index=begin, result=res).item()))
+            r_nccl = bits(float(nccl_exact_sum(x, comm, base_index=begin, result=res).item()))
+            ok = torch.tensor([1 if (r_p2p == r_nccl and not p2p.error_epoch()) else 0],
+                              dtype=torch.int32, device=dev)
+            if world > 1:
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()):
+                exchange_note = "exsum_p2p_sum checked equal to exsum_nccl_sum on every rank"
+                comm.close()
+                comm = None
+            else:
+                exchange_note = "exsum_p2p_sum disagreed with NCCL on some rank; NCCL used"
+                p2p.close()
+                p2p = None
 
     def step():
         if p2p is not None:
@@ -641,6 +670,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": steps * (2 if comm is not None else 1),  # p2p: 1 per step
+            "exchange": exchange_note,
             "clocks": clocks.report(),
             "result_bits": hex(result_bits),
             "bit_exact_vs_oracle": parity,
