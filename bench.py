@@ -547,7 +547,7 @@ def main():
         if p2p is not None:
             return p2p_exact_sum(x, p2p, base_index=begin, result=res, overlap=True)
         if comm is not None:
-            return nccl_exact_sum(x, comm, base_index=begin, result=res)
+            return nccl_exact_sum(x, comm, base_index=begin, result=res, overlap=True)
         ops.exact_sum_tensor(x, base_index=begin, result=res, partial=part, workspace=ws,
                              overlap=True)
         return res

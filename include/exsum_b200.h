@@ -235,10 +235,11 @@ int exsum_nccl_comm_destroy(void *comm);
 size_t exsum_nccl_workspace_bytes(int nranks);
 /* This rank's shard d_shard[0..n) = logical indices [base_index, base_index + n):
  * sum kernel -> ncclAllGather of the records -> merge kernel, stream-ordered and
- * graph-capturable.  Outputs (either may be NULL) are identical on every rank. */
+ * graph-capturable.  Outputs (either may be NULL) are identical on every rank.
+ * flags: EXSUM_SUM_OVERLAP for the sum kernel, as for exsum_cuda_sum_ex. */
 int exsum_nccl_sum(const double *d_shard, size_t n, uint64_t base_index, void *comm,
                    double *d_result, exsum_partial *d_partial, void *d_ws, size_t ws_bytes,
-                   void *stream);
+                   void *stream, unsigned flags);
 
 /* ------------------------------------------------------------ value files */
 /* exsum::FileFormat (io.hpp:23-29): bin = raw little-endian doubles; text =

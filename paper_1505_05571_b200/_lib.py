@@ -110,7 +110,7 @@ _SIGNATURES = {
     "exsum_nccl_comm_init": (_i32, [C.POINTER(_vp), _i32, _vp, _i32]),
     "exsum_nccl_comm_destroy": (_i32, [_vp]),
     "exsum_nccl_workspace_bytes": (_sz, [_i32]),
-    "exsum_nccl_sum": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "exsum_nccl_sum": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _vp, _sz, _vp, C.c_uint]),
     "exsum_p2p_mailbox_bytes": (_sz, [_i32]),
     "exsum_p2p_mailbox_alloc": (_i32, [_i32, C.POINTER(_vp)]),
     "exsum_p2p_mailbox_free": (_i32, [_vp]),

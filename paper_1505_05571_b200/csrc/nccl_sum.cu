@@ -134,7 +134,7 @@ size_t exsum_nccl_workspace_bytes(int nranks) {
 
 int exsum_nccl_sum(const double *d_shard, size_t n, uint64_t base_index, void *comm,
                    double *d_result, exsum_partial *d_partial, void *d_ws, size_t ws_bytes,
-                   void *stream) {
+                   void *stream, unsigned flags) {
   if (!comm || !d_ws || (n && !d_shard)) return EXSUM_EINVAL;
   const NcclApi *api = nccl();
   if (!api) return EXSUM_ENCCL;
@@ -145,7 +145,8 @@ int exsum_nccl_sum(const double *d_shard, size_t n, uint64_t base_index, void *c
   unsigned char *ws = static_cast<unsigned char *>(d_ws);
   exsum_partial *rec = reinterpret_cast<exsum_partial *>(ws + record_offset());
   exsum_partial *gathered = reinterpret_cast<exsum_partial *>(ws + gather_offset());
-  int st = exsum_cuda_sum(d_shard, n, base_index, nullptr, rec, d_ws, record_offset(), stream);
+  int st = exsum_cuda_sum_ex(d_shard, n, base_index, nullptr, rec, d_ws, record_offset(), stream,
+                             flags);
   if (st != EXSUM_OK) return st;
   if (api->AllGather(rec, gathered, sizeof(exsum_partial), ncclUint8,
                      static_cast<ncclComm_t>(comm),

@@ -127,7 +127,7 @@ class NcclCommunicator:
 
 def nccl_exact_sum(shard: torch.Tensor, comm: NcclCommunicator, *, base_index: int,
                    result: torch.Tensor | None = None,
-                   record: torch.Tensor | None = None) -> torch.Tensor:
+                   record: torch.Tensor | None = None, overlap: bool = False) -> torch.Tensor:
     """exsum_nccl_sum: exact sum of the logical array of which ``shard`` holds
     [base_index, base_index + len).  Returns the 1-element float64 result
     (identical bits on every rank); ``record`` (592 B uint8) receives the merged
@@ -140,7 +140,7 @@ def nccl_exact_sum(shard: torch.Tensor, comm: NcclCommunicator, *, base_index: i
     stream = torch.cuda.current_stream(x.device).cuda_stream
     _lib.call("exsum_nccl_sum", x.data_ptr() if x.numel() else None, x.numel(), base_index,
               comm.comm, result.data_ptr(), record.data_ptr() if record is not None else None,
-              comm.workspace.data_ptr(), comm.workspace.numel(), stream)
+              comm.workspace.data_ptr(), comm.workspace.numel(), stream, 1 if overlap else 0)
     return result
 
 

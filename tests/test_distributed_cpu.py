@@ -108,7 +108,7 @@ def test_nccl_entry_points_without_gpu():
     comm = C.c_void_p()
     assert _lib.lib.exsum_nccl_comm_init(C.byref(comm), 0, uid, 0) == _lib.EXSUM_EINVAL
     assert _lib.lib.exsum_nccl_comm_init(C.byref(comm), 2, uid, 2) == _lib.EXSUM_EINVAL
-    assert _lib.lib.exsum_nccl_sum(None, 0, 0, None, None, None, None, 0, None) == _lib.EXSUM_EINVAL
+    assert _lib.lib.exsum_nccl_sum(None, 0, 0, None, None, None, None, 0, None, 0) == _lib.EXSUM_EINVAL
     assert _lib.lib.exsum_nccl_comm_destroy(None) == _lib.EXSUM_EINVAL
     sizes = [_lib.lib.exsum_nccl_workspace_bytes(w) for w in (1, 2, 8)]
     assert _lib.lib.exsum_nccl_workspace_bytes(0) == 0
