@@ -92,3 +92,22 @@ def test_host_generator_is_deterministic_and_sharded():
     vals = set(np.unique(x).tolist())
     unpaired = [v for v in vals if -v not in vals]
     assert len(unpaired) <= 10_000 + 10
+
+
+def _build_cpp_demo(tmp_path):
+    import subprocess
+    libdir = ROOT / "paper_1505_05571_b200" / "lib"
+    exe = tmp_path / "capi_demo"
+    subprocess.run(["/usr/bin/g++", "-std=c++17", "-O2", "-Wall", "-Werror", f"-I{ROOT / 'include'}",
+                    str(ROOT / "tests" / "cpp" / "capi_demo.cpp"), f"-L{libdir}", "-lexsum_b200",
+                    f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_cpp_caller_host(tmp_path):
+    """A C++ program that includes exsum_b200.h and links the library (no Python)."""
+    import subprocess
+    exe = _build_cpp_demo(tmp_path)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert "host ok" in r.stdout

@@ -304,3 +304,14 @@ def test_more_than_2_pow_32_terms(cuda):
     assert got == 0x7FF0000000000AAA and part.first_nan == (1 << 32) + 3
     del x
     torch.cuda.empty_cache()
+
+
+def test_cpp_caller_device(cuda, tmp_path):
+    """The C++ caller's device part: exsum_context_sum on a host array equals the
+    host large accumulator, through the C ABI only."""
+    import subprocess
+    from test_capi import _build_cpp_demo
+    exe = _build_cpp_demo(tmp_path)
+    r = subprocess.run([str(exe), "--device"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert "device ok" in r.stdout
