@@ -18,23 +18,31 @@
 // ATOMS.CAST.SPIN.64 CAS loops on sm_100a, random-bin read-modify-writes cost
 // ~3.5x in bank conflicts, and U[0,1) puts half of all terms in one bin.
 //
-// Per-term cost (~25 SASS: 12 ALU, 8 FMA, 4 LSU) is balanced between the
-// integer ALU and FMA pipes (IMAD forms for xor-with-sign and addresses).
-// Loads are 256-bit (LDG.E.NA.ENL2.256), "rolling": a vector's registers are
-// refilled with the next batch's vector right after its four terms are added,
-// with a cp.async.bulk L2 prefetch one batch further ahead.  When every lane's
-// batch falls in one slot (narrow exponent ranges) the batch is summed in
-// registers and the slot gets one read-modify-write.  The sustained rate is
-// bounded by the 1 kW power cap, so fewer instructions and fewer shared-memory
-// accesses per term translate directly into throughput.
+// Per-term cost: 23.9 SASS instructions (14 integer ALU, 5 FMA-pipe IMADs, 4.25
+// LSU) and 6 shared wavefronts.  Loads are 256-bit (LDG.E.NA.ENL2.256),
+// "rolling": a vector's registers are refilled with the next batch's vector
+// right after its four terms are added, with a cp.async.bulk L2 prefetch one
+// batch further ahead.  When every lane's batch falls in one slot (narrow
+// exponent ranges) the batch is summed in registers and the slot gets one
+// read-modify-write.  Inf/NaN are added blindly and cancelled by a per-batch
+// fix-up.  Sustained rates sit at the 1 kW power cap, so energy per term (not
+// DRAM) bounds the general path.
+//
+// Term sources (kOp): x[i]; fl(x[i]^2) for sqnorm; fl(a[i] b[i]) for dot, with
+// the reference's x86 NaN rules applied in the fix-up.
 //
 // Kernels
-//   exsum_sum_kernel        K1+K2+K3: persistent grid (1 CTA per SM), each warp
-//                           streams a contiguous range; the CTA combines its
-//                           lanes into 67 chunk sums, REDG.ADD.64 into the
-//                           workspace; the last CTA canonicalises, resolves
-//                           Inf/NaN by first index and rounds (warp-parallel).
-//                           Launchable with programmatic dependent launch.
+//   exsum_sum_kernel<kOp>   K1+K2+K3: persistent grid (1 CTA per SM; 8/9 of the
+//                           SMs for short overlapped sums), each warp streams a
+//                           contiguous range; the CTA combines its lanes into 67
+//                           chunk sums, REDG.ADD.64 into the workspace; the last
+//                           CTA canonicalises, resolves Inf/NaN by first index
+//                           and rounds (warp-parallel).  Launchable with
+//                           programmatic dependent launch.  With P2P arguments
+//                           the last CTA also exchanges the record with the
+//                           other ranks over peer memory and merges
+//                           (exsum_p2p_sum); with a group split, one cooperative
+//                           launch emulates several ranks (tests).
 //   exsum_segmented_kernel  K4: one warp per segment (dynamic claim), compact
 //                           loop body (instruction-cache bound otherwise).
 //   exsum_merge_kernel      K5: merge of k gathered partial records + round.
