@@ -315,3 +315,40 @@ def test_cpp_caller_device(cuda, tmp_path):
     r = subprocess.run([str(exe), "--device"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr
     assert "device ok" in r.stdout
+
+
+def test_cuda_graph_capture(cuda):
+    """The device entry points inside a captured CUDA graph (replayed several
+    times, workspace reused): exact sum with and without programmatic dependent
+    launch, the segmented sum and dot give the eager bits."""
+    x = gen(3, 5_000_003, 4)
+    y = gen(1, 5_000_003, 5)
+    offs = torch.tensor([0, 10, 1_000_000, 1_000_000, 5_000_003], dtype=torch.int64, device="cuda")
+    want = dev_sum(x)[0]
+    want_seg = ops.exact_sum_segmented(x, offs).cpu().numpy().view(np.uint64).copy()
+    want_dot = bits_of(ops.exact_dot_tensor(x, y)[0].item())
+    for overlap in (False, True):
+        ws = ops.Workspace(x.device)
+        res = torch.empty(3, dtype=torch.float64, device="cuda")
+        part = torch.empty(ops.PARTIAL_BYTES, dtype=torch.uint8, device="cuda")
+        seg_ws = ops.Workspace(x.device)
+        dot_ws = ops.Workspace(x.device)
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm-up on the capture stream
+            ops.exact_sum_tensor(x, result=res[0:1], partial=part, workspace=ws, overlap=overlap)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            ops.exact_sum_tensor(x, result=res[0:1], partial=part, workspace=ws, overlap=overlap)
+            ops.exact_sum_tensor(x, result=res[1:2], partial=part, workspace=ws, overlap=overlap)
+            seg = ops.exact_sum_segmented(x, offs, workspace=seg_ws)
+            ops.exact_dot_tensor(x, y, result=res[2:3], workspace=dot_ws)
+        for _ in range(3):
+            res.zero_()
+            g.replay()
+        torch.cuda.synchronize()
+        got = res.cpu().numpy().view(np.uint64)
+        assert int(got[0]) == want and int(got[1]) == want, overlap
+        assert int(got[2]) == want_dot, overlap
+        assert np.array_equal(seg.cpu().numpy().view(np.uint64), want_seg), overlap
