@@ -488,8 +488,8 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1505_05571_b200 import _lib, ops
-    from paper_1505_05571_b200.distributed import (NcclCommunicator, P2PGroup, nccl_exact_sum,
-                                                   p2p_exact_sum, shard_bounds)
+    from paper_1505_05571_b200.distributed import (NcclCommunicator, P2PGroup, exchange_partials,
+                                                   nccl_exact_sum, p2p_exact_sum, shard_bounds)
 
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -613,10 +613,13 @@ def main():
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
+        exchanged = world > 1 or comm is not None or p2p is not None
         for _ in range(e2e_steps):
-            if world > 1:
-                v, rec = ctx.sum(hx.numpy(), want_partial=True)
-                recs = exchange_partials(torch.frombuffer(bytearray(bytes(rec)), dtype=torch.uint8).to(dev))
+            if exchanged:
+                # the shard's record with global indices -> all ranks' records -> merge
+                v, rec = ctx.sum(hx.numpy(), want_partial=True, base_index=begin)
+                rec_t = torch.frombuffer(bytearray(bytes(rec)), dtype=torch.uint8).to(dev)
+                recs = exchange_partials(rec_t) if world > 1 else rec_t.view(1, -1)
                 e_res = float(ops.merge_partials(recs)[0].item())
             else:
                 e_res = ctx.sum_ptr(hx.data_ptr(), n_local)
@@ -627,8 +630,8 @@ def main():
         el = float(te[0])
         assert bits(e_res) == result_bits, "e2e path disagrees with the device path"
         e2e = {"value": round(8.0 * n_total * e2e_steps / el / 1e9, 3), "unit": "GB/s",
-               "h2d_bytes_per_step": 8 * n_local + (ops.PARTIAL_BYTES if world > 1 else 0),
-               "d2h_bytes_per_step": 8 + (ops.PARTIAL_BYTES if world > 1 else 0),
+               "h2d_bytes_per_step": 8 * n_local + (ops.PARTIAL_BYTES if exchanged else 0),
+               "d2h_bytes_per_step": 8 + (ops.PARTIAL_BYTES if exchanged else 0),
                "path": "exsum_context_sum (pinned host -> 2 x 256 MB staging ring, copy/compute overlap)"}
         del hx, ctx
 

@@ -204,6 +204,10 @@ exsum_context *exsum_context_create(int device, size_t staging_bytes);
 void exsum_context_free(exsum_context *ctx);
 int exsum_context_sum(exsum_context *ctx, const double *h_x, size_t n, double *h_result,
                       exsum_partial *h_partial);
+/* The same for a shard whose first element has global index base_index (the
+ * partial record's Inf/NaN indices are global, ready for exsum_partial_merge). */
+int exsum_context_sum_at(exsum_context *ctx, const double *h_x, size_t n, uint64_t base_index,
+                         double *h_result, exsum_partial *h_partial);
 /* exact_sum(read_values(path, format)) without materialising the array: a bin
  * file is read chunk by chunk into pinned host buffers that feed the staging
  * ring (disk read, host->device copy and accumulate overlap); a text file is

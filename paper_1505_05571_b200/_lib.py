@@ -131,6 +131,7 @@ _SIGNATURES = {
     "exsum_context_create": (_vp, [_i32, _sz]),
     "exsum_context_free": (None, [_vp]),
     "exsum_context_sum": (_i32, [_vp, _vp, _sz, _dp, _pp]),
+    "exsum_context_sum_at": (_i32, [_vp, _vp, _sz, _u64, _dp, _pp]),
     "exsum_cuda_gen": (_i32, [_i32, _u64, _u64, _u64, _sz, _vp, _vp]),
     "exsum_host_gen": (_i32, [_i32, _u64, _u64, _u64, _sz, _vp]),
     "exsum_host_gen_offsets": (_i32, [_u64, _sz, _u64, _u64, _vp]),

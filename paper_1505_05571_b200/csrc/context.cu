@@ -97,6 +97,11 @@ void exsum_context_free(exsum_context *ctx) { destroy(ctx); }
 
 int exsum_context_sum(exsum_context *c, const double *h_x, size_t n, double *h_result,
                       exsum_partial *h_partial) {
+  return exsum_context_sum_at(c, h_x, n, 0, h_result, h_partial);
+}
+
+int exsum_context_sum_at(exsum_context *c, const double *h_x, size_t n, uint64_t base_index,
+                         double *h_result, exsum_partial *h_partial) {
   if (!c || (n && !h_x) || (!h_result && !h_partial)) return EXSUM_EINVAL;
   int prev = 0;
   cudaGetDevice(&prev);
@@ -115,7 +120,8 @@ int exsum_context_sum(exsum_context *c, const double *h_x, size_t n, double *h_r
       st = EXSUM_ECUDA;
       break;
     }
-    st = exsum_cuda_accumulate(c->stage[b], len, off, c->ws, c->ws_bytes, c->compute);
+    st = exsum_cuda_accumulate(c->stage[b], len, base_index + off, c->ws, c->ws_bytes,
+                               c->compute);
     if (st == EXSUM_OK && cudaEventRecord(c->consumed[b], c->compute) != cudaSuccess)
       st = EXSUM_ECUDA;
     off += len;

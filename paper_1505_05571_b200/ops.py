@@ -216,13 +216,15 @@ class HostContext:
             lib.exsum_context_free(h)
             self._h = None
 
-    def sum(self, values, want_partial: bool = False):
+    def sum(self, values, want_partial: bool = False, base_index: int = 0):
+        """exact_sum of a host array (exsum_context_sum_at); base_index = global
+        index of values[0] for the record's Inf/NaN indices."""
         a = values.numpy() if isinstance(values, torch.Tensor) else values
         a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
         out = C.c_double()
         part = ExsumPartial()
-        _lib.call("exsum_context_sum", self._h, a.ctypes.data, a.size, C.byref(out),
-                  C.byref(part) if want_partial else None)
+        _lib.call("exsum_context_sum_at", self._h, a.ctypes.data, a.size, base_index,
+                  C.byref(out), C.byref(part) if want_partial else None)
         return (out.value, part) if want_partial else out.value
 
     def sum_ptr(self, ptr: int, n: int) -> float:

@@ -352,3 +352,26 @@ def test_cuda_graph_capture(cuda):
         assert int(got[0]) == want and int(got[1]) == want, overlap
         assert int(got[2]) == want_dot, overlap
         assert np.array_equal(seg.cpu().numpy().view(np.uint64), want_seg), overlap
+
+
+def test_context_sum_at_global_indices(cuda, checker):
+    """exsum_context_sum_at: a host shard's record carries global Inf/NaN indices,
+    so shard records merged on the host give the serial bits."""
+    rng = np.random.default_rng(31)
+    h = rng.normal(size=3_000_000)
+    bits_view = h.view(np.uint64)
+    bits_view[2_500_000] = 0x7FF0000000000AAA  # first NaN (shard 2)
+    bits_view[2_900_000] = 0x7FF0000000000BBB
+    bits_view[10] = 0x7FF0000000000000        # +Inf in shard 0
+    want = bits_of(checker.exact_sum(h))
+    ctx = ops.HostContext(0, staging_bytes=1 << 20)
+    cuts = [0, 1_000_000, 2_000_000, 3_000_000]
+    recs = []
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        _, rec = ctx.sum(h[a:b], want_partial=True, base_index=a)
+        recs.append(rec)
+    assert recs[2].first_nan == 2_500_000 and recs[0].first_pos_inf == 10
+    from paper_1505_05571_b200.distributed import merge_records
+    arr = torch.frombuffer(bytearray(b"".join(bytes(r) for r in recs)), dtype=torch.uint8)
+    got, _ = merge_records(arr)
+    assert bits_of(got) == want == 0x7FF0000000000AAA
