@@ -167,19 +167,34 @@ class P2PGroup:
         self.ptrs[self.rank] = self._own
         self._opened = []
         if self.world > 1:
+            # Every rank reaches every collective below, whatever fails locally,
+            # and the outcome is agreed on (MIN of a success flag): either all
+            # ranks hold a complete peer mapping or all raise.
             h = (C.c_char * 64)()
-            _lib.call("exsum_ipc_get_handle", self._own, h)
+            ok = _lib.lib.exsum_ipc_get_handle(self._own, h) == _lib.EXSUM_OK
             handles = [None] * self.world
-            dist.all_gather_object(handles, bytes(h.raw), group=group)
+            dist.all_gather_object(handles, bytes(h.raw) if ok else None, group=group)
             for r, hb in enumerate(handles):
-                if r == self.rank:
+                if r == self.rank or not ok:
+                    continue
+                if hb is None:
+                    ok = False
                     continue
                 p = C.c_void_p()
                 with torch.cuda.device(self.device):
-                    _lib.call("exsum_ipc_open", (C.c_char * 64).from_buffer_copy(hb), C.byref(p))
+                    st = _lib.lib.exsum_ipc_open((C.c_char * 64).from_buffer_copy(hb), C.byref(p))
+                if st != _lib.EXSUM_OK:
+                    ok = False
+                    continue
                 self.ptrs[r] = p.value
                 self._opened.append(p.value)
-            dist.barrier(group=group)  # every mailbox mapped before anyone writes
+            on_gpu = dist.get_backend(group) == "nccl"
+            flag = torch.tensor([1 if ok else 0], dtype=torch.int32,
+                                device=self.device if on_gpu else "cpu")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)  # also the barrier:
+            if not int(flag.item()):                                # all mapped before use
+                self.close()
+                raise RuntimeError("P2PGroup: peer mapping failed on some rank")
         self.epoch = 0
         nbytes = int(_lib.lib.exsum_cuda_workspace_bytes())
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
