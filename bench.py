@@ -368,7 +368,7 @@ def run_segmented(args, wl):
     step()
     torch.cuda.synchronize()
     per = time.perf_counter() - t
-    steps = args.steps or max(5, min(2000, int(0.5 / max(per, 1e-6))))
+    steps = agreed_steps(args.steps or max(5, min(2000, int(0.5 / max(per, 1e-6)))), world, dev)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -459,6 +459,18 @@ def run_segmented(args, wl):
 
 
 # ---------------------------------------------------------------- GPU arm
+
+def agreed_steps(steps: int, world: int, dev) -> int:
+    """Every rank must time the same number of steps (the P2P exchange pairs
+    step e on every rank): the maximum of the ranks' choices."""
+    if world <= 1:
+        return steps
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([steps], dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return int(t.item())
+
 
 def ncu_traffic(config: int):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
@@ -561,7 +573,7 @@ def main():
         step()
     torch.cuda.synchronize()
     per = (time.perf_counter() - t0) / 5
-    steps = args.steps or max(10, min(20000, int(0.5 / max(per, 1e-6))))
+    steps = agreed_steps(args.steps or max(10, min(20000, int(0.5 / max(per, 1e-6)))), world, dev)
 
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
