@@ -185,10 +185,15 @@ int exsum_cuda_finalize(double *d_result, exsum_partial *d_partial, void *d_ws,
 /* One exact_sum per segment: segment i is d_x[d_offsets[i] .. d_offsets[i+1]).
  * d_offsets has nseg + 1 nondecreasing entries.  No reference batch API exists;
  * semantics = exact_sum(segment_i) for every i.
- * d_partials may be NULL; otherwise nseg records, indices local to the segment. */
+ * d_partials may be NULL; otherwise nseg records, indices local to the segment.
+ * With ws_bytes >= exsum_cuda_segmented_workspace_bytes(nseg) the segments are
+ * scheduled longest first (a second, one-CTA launch orders them; the order
+ * cannot change any result), otherwise in index order.  exsum_cuda_workspace_init
+ * with the full ws_bytes prepares both (it zeroes the order state as well). */
 int exsum_cuda_sum_segmented(const double *d_x, const uint64_t *d_offsets, size_t nseg,
                              double *d_out, exsum_partial *d_partials, void *d_ws,
                              size_t ws_bytes, void *stream);
+size_t exsum_cuda_segmented_workspace_bytes(size_t nseg);
 
 /* Merge k partial records resident on the device (after an all-gather of the
  * shards' records): parallel_exact_sum's merge phase, vector_ops.cpp:64-70. */

@@ -103,6 +103,7 @@ _SIGNATURES = {
     "exsum_cuda_accumulate": (_i32, [_vp, _sz, _u64, _vp, _sz, _vp]),
     "exsum_cuda_finalize": (_i32, [_vp, _vp, _vp, _sz, _vp]),
     "exsum_cuda_sum_segmented": (_i32, [_vp, _vp, _sz, _vp, _vp, _vp, _sz, _vp]),
+    "exsum_cuda_segmented_workspace_bytes": (_sz, [_sz]),
     "exsum_cuda_merge": (_i32, [_vp, _sz, _vp, _vp, _vp]),
     "exsum_shard_bounds": (_i32, [_u64, _i32, _i32, C.POINTER(_u64), C.POINTER(_u64)]),
     "exsum_nccl_available": (_i32, [C.POINTER(_i32)]),

@@ -83,6 +83,14 @@
 #ifndef EXSUM_TIMELINE
 #define EXSUM_TIMELINE 0  // diagnostics build: per-warp %globaltimer stamps (scripts/timeline.py)
 #endif
+#ifndef EXSUM_SEG_AHEAD
+#define EXSUM_SEG_AHEAD 0  // segmented kernel: claim the next segment during the current one
+                           // (1: a step per batch, 2: after the first loads; both measured
+                           // slower, profiles/r01_variants_seg_ahead.log)
+#endif
+#ifndef EXSUM_SCALARS_LATE
+#define EXSUM_SCALARS_LATE 1  // scalar head/tail terms after the first batch's loads
+#endif
 #ifndef EXSUM_UNIFORM_BACKOFF
 #define EXSUM_UNIFORM_BACKOFF 7  // batches to skip the one-slot test after a miss
 #endif
@@ -134,6 +142,9 @@ constexpr int kUniformBackoff = EXSUM_UNIFORM_BACKOFF;
 #if EXSUM_TIMELINE
 // [warp][0..3]: start, loop end, flush end (after the CTA's REDs), last-CTA end
 __device__ unsigned long long g_timeline[148 * 16 * 4 + 8];
+// segmented kernel: per warp, summed phase durations (ns) over its segments:
+// [0] claim, [1] clear, [2] accumulate, [3] chunks, [4] emit, [5] segments, [6] terms
+__device__ unsigned long long g_seg_timeline[148 * 16 * 8];
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -651,28 +662,41 @@ __device__ __forceinline__ uint32_t uniform_slot(const Batch<V, kOp> &b) {
 //   kSplit:   separate unguarded steady-state body (larger code, fewer instrs)
 //   kScan:    scanning Inf/NaN fix-up (for data with frequent specials)
 //   kOp:      term source (kSum, kSqnorm, kDot, kDotScalarB); y used by dots
-template <int V, bool kUniform, bool kSplit, bool kScan, int kOp = kSum>
+// hook() runs once per batch, after the batch's refills are issued (the
+// segmented kernel advances its claim of the next segment there).
+struct NoHook {
+  __device__ __forceinline__ void start() const {}
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <int V, bool kUniform, bool kSplit, bool kScan, int kOp = kSum, class Hook = NoHook>
 __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
                                                 const double *__restrict__ y,
                                                 unsigned long long begin, unsigned long long end,
                                                 unsigned long long index_base, const Lane &a,
-                                                Specials &sp, int &norm_count, int lane) {
+                                                Specials &sp, int &norm_count, int lane,
+                                                Hook hook = Hook{}) {
   constexpr int kNormEvery = 2016 / (4 * V);  // batches between renormalisations
   static_assert(kNormEvery >= 1, "batch too large for the carry budget");
   if (begin >= end) return;
-  // Scalar head up to 32-byte alignment of &x[pos], scalar tail after the vectors.
+  // Scalar head up to 32-byte alignment of &x[pos], scalar tail after the
+  // vectors; they are added after the first batch's loads are issued so that
+  // their load latency overlaps it.
   const uintptr_t addr = reinterpret_cast<uintptr_t>(x + begin);
   unsigned long long head = ((32u - (addr & 31u)) & 31u) >> 3;
   if (head > end - begin) head = end - begin;
-  if (lane < static_cast<int>(head))
-    add_elem_checked<kOp>(a, sp, x, y, begin + lane, index_base + begin + lane);
   const unsigned long long vbeg_t = begin + head;  // first vector's term position
   const long long nvec = static_cast<long long>((end - vbeg_t) >> 2);
   const double *X4 = x + vbeg_t;                   // 32-byte aligned
   const double *Y4 = kOp >= kDot ? y + vbeg_t : X4;
   const unsigned long long tail_t = vbeg_t + 4ull * static_cast<unsigned long long>(nvec);
-  if (lane < static_cast<int>(end - tail_t))
-    add_elem_checked<kOp>(a, sp, x, y, tail_t + lane, index_base + tail_t + lane);
+  auto scalars = [&]() {
+    if (lane < static_cast<int>(head))
+      add_elem_checked<kOp>(a, sp, x, y, begin + lane, index_base + begin + lane);
+    if (lane < static_cast<int>(end - tail_t))
+      add_elem_checked<kOp>(a, sp, x, y, tail_t + lane, index_base + tail_t + lane);
+  };
+  if (nvec <= 0 || !EXSUM_SCALARS_LATE) scalars();
   if (nvec <= 0) return;
   constexpr long long kStep = V * 32;
   const unsigned long long ib = index_base + vbeg_t;
@@ -681,6 +705,8 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
   }
   Batch<V, kOp> b;
   load_batch<V, kOp>(b, X4, Y4, 0, nvec, lane);
+  if (EXSUM_SCALARS_LATE) scalars();
+  hook.start();
   int backoff = 0;
   for (long long v = 0; v < nvec; v += kStep) {
     const long long nv = v + kStep;
@@ -710,6 +736,7 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
         emax = batch_rolling<V, true, kOp>(a, b, X4, Y4, nv, nvec, lane);
       }
     }
+    hook();
     if (__builtin_expect(emax == 0x7FFu, 0))
       fixup_specials<V, kScan, kOp>(a, sp, X4, Y4, v, nvec, lane, ib);
     if (++norm_count >= kNormEvery) {
@@ -738,14 +765,25 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
 //      (zero below the lowest nonzero digit z, -d_z at z, ~d_i above);
 //   4. lane 0 rounds a 3-digit window at the leading digit with a sticky ballot.
 // row: 67 chunk values in shared memory (any representation with |c| < 2^62).
+__device__ void warp_emit_v(long long v0, long long v1, long long v2, unsigned long long P,
+                            unsigned long long M, unsigned long long N,
+                            unsigned long long payload, double *result, exsum_partial *partial,
+                            int lane);
+
 __device__ void warp_emit(const long long *row, unsigned long long P, unsigned long long M,
                           unsigned long long N, unsigned long long payload, double *result,
                           exsum_partial *partial, int lane) {
+  warp_emit_v(row[lane], row[lane + 32], lane < 3 ? row[lane + 64] : 0, P, M, N, payload, result,
+              partial, lane);
+}
+
+// The same with the row already in registers (lane holds chunks lane, lane + 32, lane + 64).
+__device__ void warp_emit_v(long long v0, long long v1, long long v2, unsigned long long P,
+                            unsigned long long M, unsigned long long N,
+                            unsigned long long payload, double *result, exsum_partial *partial,
+                            int lane) {
   const unsigned FULL = 0xffffffffu;
-  long long v[3];
-  v[0] = row[lane];
-  v[1] = row[lane + 32];
-  v[2] = lane < 3 ? row[lane + 64] : 0;
+  long long v[3] = {v0, v1, v2};
   // 1. carries: chunk i keeps its low 32 bits, passes the rest to i + 1; chunk 66 keeps all.
   while (true) {
     long long c[3];
@@ -1172,41 +1210,240 @@ __global__ void exsum_finalize_kernel(Workspace *ws, double *result, exsum_parti
 
 // ------------------------------------------------------------------------- K4
 
+// Longest-first claim order (LPT list scheduling) for the segmented kernel.
+// Warps claim segments dynamically, so the finish is set by the last segments
+// claimed; with claims one segment ahead (below) a warp may also sit on a long
+// unstarted segment.  Claiming the longest first bounds both by the shortest
+// segments.  Two small launches bucket the lengths by octave with 8
+// sub-buckets (a coarse descending sort is enough for list scheduling):
+//   hist:    per-CTA shared histograms -> global counts; the last CTA turns
+//            them into descending bucket bases and re-zeroes the counts;
+//   scatter: per-CTA ranks within each bucket, one global atomic per bucket
+//            per CTA to reserve its range, order[base + rank] = segment.
+// Order within a bucket is arbitrary, which cannot change any result (each
+// segment is summed by one warp either way).
+constexpr int kOrderThreads = 1024;
+constexpr int kOrderBuckets = 512;
+constexpr unsigned long long kOrderMaxSegs = 1ull << 24;  // beyond: index order
+struct OrderState {                    // zeroed by exsum_cuda_workspace_init
+  unsigned int hist[kOrderBuckets];    // counts (zero between calls)
+  unsigned int base[kOrderBuckets];    // bucket cursors of the current call
+  unsigned int done;                   // hist CTAs finished (zero between calls)
+  unsigned int pad_[63];
+};
+constexpr size_t kOrderStateOffset = (sizeof(Workspace) + 255) & ~size_t{255};
+constexpr size_t kOrderOffset = kOrderStateOffset + sizeof(OrderState);  // order[] in d_ws
+
+__device__ __forceinline__ int length_bucket(unsigned long long len) {
+  if (len < 8) return static_cast<int>(len);
+  const int msb = 63 - __clzll(static_cast<long long>(len));
+  return msb * 8 + static_cast<int>((len >> (msb - 3)) & 7u);
+}
+
+__global__ void __launch_bounds__(kOrderThreads)
+exsum_segment_hist_kernel(const unsigned long long *__restrict__ offs, unsigned long long nseg,
+                          OrderState *st) {
+  __shared__ unsigned int h[kOrderBuckets];
+  __shared__ bool last;
+  const unsigned t = threadIdx.x;
+  for (unsigned k = t; k < kOrderBuckets; k += kOrderThreads) h[k] = 0u;
+  __syncthreads();
+  const unsigned long long s = static_cast<unsigned long long>(blockIdx.x) * kOrderThreads + t;
+  if (s < nseg) atomicAdd(&h[length_bucket(offs[s + 1] - offs[s])], 1u);
+  __syncthreads();
+  for (unsigned k = t; k < kOrderBuckets; k += kOrderThreads)
+    if (h[k]) atomicAdd(&st->hist[k], h[k]);
+  __threadfence();
+  __syncthreads();
+  if (t == 0) last = atomicAdd(&st->done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // base[k] := number of segments in buckets above k (descending lengths).
+  // 512 counts, one warp: each lane owns 16 consecutive buckets.
+  if (t < 32) {
+    unsigned v[16], sum = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      v[i] = __ldcg(&st->hist[16 * t + i]);
+      st->hist[16 * t + i] = 0u;
+      sum += v[i];
+    }
+    unsigned above = sum;  // inclusive suffix sum over lanes >= t
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned w = __shfl_down_sync(0xffffffffu, above, o);
+      if (t + o < 32) above += w;
+    }
+    above -= sum;  // buckets of higher lanes
+#pragma unroll
+    for (int i = 15; i >= 0; --i) {
+      st->base[16 * t + i] = above;
+      above += v[i];
+    }
+    if (t == 0) st->done = 0u;
+  }
+}
+
+__global__ void __launch_bounds__(kOrderThreads)
+exsum_segment_scatter_kernel(const unsigned long long *__restrict__ offs, unsigned long long nseg,
+                             OrderState *st, unsigned int *__restrict__ order) {
+  __shared__ unsigned int cnt[kOrderBuckets];
+  const unsigned t = threadIdx.x;
+  for (unsigned k = t; k < kOrderBuckets; k += kOrderThreads) cnt[k] = 0u;
+  __syncthreads();
+  const unsigned long long s = static_cast<unsigned long long>(blockIdx.x) * kOrderThreads + t;
+  int key = 0;
+  unsigned r = 0;
+  if (s < nseg) {
+    key = length_bucket(offs[s + 1] - offs[s]);
+    r = atomicAdd(&cnt[key], 1u);
+  }
+  __syncthreads();
+  for (unsigned k = t; k < kOrderBuckets; k += kOrderThreads)
+    if (cnt[k]) cnt[k] = atomicAdd(&st->base[k], cnt[k]);  // this CTA's range in bucket k
+  __syncthreads();
+  if (s < nseg) order[cnt[key] + r] = static_cast<unsigned>(s);
+}
+
+// Lane 0's claim of the segment after the current one, advanced one step per
+// batch of the current segment so that each dependent round trip (claim
+// atomic -> order[] -> offsets -> L2 prefetch of the head and tail) completes
+// behind a batch of streaming instead of stalling the warp between segments.
+struct ClaimAhead {
+  unsigned int *counter;
+  const unsigned int *order;
+  const unsigned long long *offs;
+  const double *x;
+  unsigned long long nseg;
+  unsigned int c, s;
+  unsigned long long b, e;
+  int stage;  // 0: none, 1: claimed (c), 2: resolved (s), 3: bounds (b, e), 4: prefetched
+
+  __device__ __forceinline__ void step() {
+    switch (stage) {
+      case 0:
+        // inline PTX: a plain atomicAdd in a lane-0 branch becomes a
+        // warp-aggregated atomic whose result is waited for at once
+        asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(c) : "l"(counter) : "memory");
+        break;
+      case 1:
+        s = c < nseg ? (order ? __ldcg(order + c) : c) : static_cast<unsigned int>(nseg);
+        break;
+      case 2:
+        if (s < nseg) {
+          b = __ldg(offs + s);
+          e = __ldg(offs + s + 1);
+        }
+        break;
+      case 3:
+        if (s < nseg && e > b) {
+          constexpr unsigned long long kHead = EXSUM_SEG_VEC * 32 * 4;  // one batch of terms
+          const unsigned long long he = e - b > kHead ? b + kHead : e;
+          const uintptr_t p0 = reinterpret_cast<uintptr_t>(x + b) & ~uintptr_t{15};
+          const uintptr_t p1 = reinterpret_cast<uintptr_t>(x + he);
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0),
+                       "r"(static_cast<uint32_t>((p1 - p0 + 15) & ~uintptr_t{15}))
+                       : "memory");
+          if (he < e) {  // the scalar tail (last 32 bytes)
+            const uintptr_t t0 = reinterpret_cast<uintptr_t>(x + e - 4) & ~uintptr_t{15};
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], 48;" ::"l"(t0) : "memory");
+          }
+        }
+        break;
+      default:
+        return;
+    }
+    ++stage;
+  }
+};
+
+// EXSUM_SEG_AHEAD 1: one claim step per batch; 2: the claim's round trips
+// right after the first batch's loads are issued (their latency overlaps it),
+// the L2 prefetch after the loop.
+struct ClaimHook {
+  ClaimAhead *ca;
+  int lane;
+  __device__ __forceinline__ void start() const {
+    if (EXSUM_SEG_AHEAD == 2 && lane == 0)
+      while (ca->stage < 3) ca->step();
+  }
+  __device__ __forceinline__ void operator()() const {
+    if (EXSUM_SEG_AHEAD == 1 && lane == 0) ca->step();
+  }
+};
+
 __global__ void __launch_bounds__(kThreads, 1)
 exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *__restrict__ offs,
                        unsigned long long nseg, Workspace *__restrict__ ws, double *out,
-                       exsum_partial *partials) {
+                       exsum_partial *partials, const unsigned int *__restrict__ order) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  long long *rows = reinterpret_cast<long long *>(smem + kWarps * kWarpSmem);
+  long long *row = rows + warp * kChunks;
   unsigned char *wsm = smem + warp * kWarpSmem;
-  long long *row = reinterpret_cast<long long *>(smem + kWarps * kWarpSmem) + warp * kChunks;
   const Lane a = lane_view(wsm, lane);
+  ClaimAhead ca{&ws->seg_next, order, offs, x, nseg, 0u, 0u, 0ull, 0ull, 0};
+  if (lane == 0)
+    while (ca.stage < 3) ca.step();  // the first claim
+#if EXSUM_TIMELINE
+  unsigned long long ph[7] = {0, 0, 0, 0, 0, 0, 0}, tq = gtimer(), tn;
+#define EXSUM_SEG_PHASE(i) (tn = gtimer(), ph[i] += tn - tq, tq = tn)
+#else
+#define EXSUM_SEG_PHASE(i) ((void)0)
+#endif
+  EXSUM_SEG_PHASE(0);
   while (true) {
-    unsigned int s = 0;
-    if (lane == 0) s = atomicAdd(&ws->seg_next, 1u);
-    s = __shfl_sync(0xffffffffu, s, 0);
+    const unsigned int s = __shfl_sync(0xffffffffu, ca.s, 0);
     if (s >= nseg) break;
+    const unsigned long long b = __shfl_sync(0xffffffffu, ca.b, 0),
+                             e = __shfl_sync(0xffffffffu, ca.e, 0);
+    ca.stage = 0;
     zero_warp(wsm, lane);
     __syncwarp();
-    const unsigned long long b = offs[s], e = offs[s + 1];
-    Specials sp{~0ull, ~0ull, ~0ull};
     int norm_count = 0;
+    EXSUM_SEG_PHASE(1);
+#if EXSUM_TIMELINE
+    ph[5] += 1;
+    ph[6] += e - b;
+#endif
+    Specials sp{~0ull, ~0ull, ~0ull};
     // indices local to the segment: position - b
-    warp_accumulate<EXSUM_SEG_VEC, false, EXSUM_SEG_SPLIT != 0, true>(x, x, b, e, 0ull - b, a, sp,
-                                                                      norm_count, lane);
+#if EXSUM_SEG_AHEAD
+    // claim the next segment while this one streams
+    warp_accumulate<EXSUM_SEG_VEC, false, EXSUM_SEG_SPLIT != 0, true>(
+        x, x, b, e, 0ull - b, a, sp, norm_count, lane, ClaimHook{&ca, lane});
+    if (lane == 0)
+      while (ca.stage < 4) ca.step();  // short segments: finish the claim here
+#else
+    warp_accumulate<EXSUM_SEG_VEC, false, EXSUM_SEG_SPLIT != 0, true>(x, x, b, e, 0ull - b, a,
+                                                                      sp, norm_count, lane);
+    EXSUM_SEG_PHASE(2);
+    if (lane == 0)
+      while (ca.stage < 3) ca.step();
+    EXSUM_SEG_PHASE(0);
+#endif
     warp_chunks(wsm, lane, row);
     const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                              N = warp_min_u64(sp.N);
     __syncwarp();
+    EXSUM_SEG_PHASE(3);
     const unsigned long long payload =
         N != ~0ull ? __ldg(reinterpret_cast<const unsigned long long *>(x) + b + N) : 0ull;
     warp_emit(row, P, M, N, payload, out + s, partials ? partials + s : nullptr, lane);
     __syncwarp();
+    EXSUM_SEG_PHASE(4);
   }
+#if EXSUM_TIMELINE
+  if (lane == 0 && blockIdx.x < 148)
+    for (int i = 0; i < 7; ++i) g_seg_timeline[(blockIdx.x * kWarps + warp) * 8 + i] = ph[i];
+#endif
+#undef EXSUM_SEG_PHASE
   // Last warp out resets the claim counters for the next launch.
   if (lane == 0) {
     const unsigned int total = gridDim.x * kWarps;
+    __threadfence();
     if (atomicAdd(&ws->seg_done, 1u) == total - 1) {
       ws->seg_next = 0;
       ws->seg_done = 0;
@@ -1389,7 +1626,9 @@ size_t exsum_cuda_workspace_bytes(void) { return sizeof(Workspace); }
 
 int exsum_cuda_workspace_init(void *d_ws, size_t ws_bytes, void *stream) {
   if (!d_ws || ws_bytes < sizeof(Workspace)) return EXSUM_EINVAL;
-  return cudaMemsetAsync(d_ws, 0, sizeof(Workspace), static_cast<cudaStream_t>(stream)) ==
+  // the segment-order state too when the workspace has room for it
+  const size_t z = ws_bytes >= kOrderOffset ? kOrderOffset : sizeof(Workspace);
+  return cudaMemsetAsync(d_ws, 0, z, static_cast<cudaStream_t>(stream)) ==
                  cudaSuccess
              ? EXSUM_OK
              : EXSUM_ECUDA;
@@ -1541,11 +1780,30 @@ int exsum_cuda_sum_segmented(const double *d_x, const uint64_t *d_offsets, size_
   if (st) return st;
   unsigned long long g = (nseg + kWarps - 1) / kWarps;
   if (g > static_cast<unsigned long long>(sms)) g = sms;
+  const auto *offs = reinterpret_cast<const unsigned long long *>(d_offsets);
+  // Longest-first claim order when the caller's workspace has room for it and
+  // there are more segments than warps (otherwise every warp gets at most one).
+  unsigned int *order = nullptr;
+  if (ws_bytes >= exsum_cuda_segmented_workspace_bytes(nseg) && nseg <= kOrderMaxSegs &&
+      nseg > g * kWarps) {
+    auto *base = static_cast<unsigned char *>(d_ws);
+    auto *st = reinterpret_cast<OrderState *>(base + kOrderStateOffset);
+    order = reinterpret_cast<unsigned int *>(base + kOrderOffset);
+    const unsigned og = static_cast<unsigned>((nseg + kOrderThreads - 1) / kOrderThreads);
+    exsum_segment_hist_kernel<<<og, kOrderThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        offs, nseg, st);
+    exsum_segment_scatter_kernel<<<og, kOrderThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+        offs, nseg, st, order);
+  }
   exsum_segmented_kernel<<<static_cast<unsigned>(g), kThreads, kSmem,
                            static_cast<cudaStream_t>(stream)>>>(
-      d_x, reinterpret_cast<const unsigned long long *>(d_offsets), nseg,
-      static_cast<Workspace *>(d_ws), d_out, d_partials);
+      d_x, offs, nseg, static_cast<Workspace *>(d_ws), d_out, d_partials, order);
   return launch_status();
+}
+
+size_t exsum_cuda_segmented_workspace_bytes(size_t nseg) {
+  if (nseg > kOrderMaxSegs) return sizeof(Workspace);
+  return kOrderOffset + 4 * nseg;
 }
 
 int exsum_cuda_merge(const exsum_partial *d_parts, size_t k, double *d_result,
@@ -1557,6 +1815,12 @@ int exsum_cuda_merge(const exsum_partial *d_parts, size_t k, double *d_result,
 }
 
 #if EXSUM_TIMELINE
+int exsum_debug_seg_timeline(unsigned long long *out, size_t count) {
+  if (!out || count > sizeof(g_seg_timeline) / 8) return EXSUM_EINVAL;
+  return cudaMemcpyFromSymbol(out, g_seg_timeline, count * 8) == cudaSuccess ? EXSUM_OK
+                                                                             : EXSUM_ECUDA;
+}
+
 int exsum_debug_timeline(unsigned long long *out, size_t count) {
   if (!out || count > sizeof(g_timeline) / 8) return EXSUM_EINVAL;
   return cudaMemcpyFromSymbol(out, g_timeline, count * 8) == cudaSuccess ? EXSUM_OK : EXSUM_ECUDA;

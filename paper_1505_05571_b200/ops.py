@@ -29,7 +29,7 @@ __all__ = ["exact_sum", "exact_mean", "exact_sum_tensor", "exact_sum_segmented",
            "exact_sqnorm_tensor", "exact_dot_tensor", "read_values", "write_values",
            "exact_sum_file",
            "merge_partials", "partial_from_tensor", "Workspace", "HostContext",
-           "PARTIAL_BYTES", "WORKSPACE_BYTES"]
+           "PARTIAL_BYTES", "WORKSPACE_BYTES", "segmented_workspace_bytes"]
 
 PARTIAL_BYTES = C.sizeof(ExsumPartial)
 WORKSPACE_BYTES = int(lib.exsum_cuda_workspace_bytes())
@@ -43,14 +43,15 @@ def _stream_handle(device: torch.device) -> int:
 class Workspace:
     """Zero-initialised device workspace (exsum_cuda_workspace_init) bound to one device."""
 
-    def __init__(self, device: torch.device | int | str | None = None):
+    def __init__(self, device: torch.device | int | str | None = None, nbytes: int = 0):
         dev = torch.device("cuda", torch.cuda.current_device()) if device is None \
             else torch.device(device)
         if dev.type != "cuda":
             raise ValueError("Workspace needs a CUDA device")
         self.device = dev
-        self.buf = torch.empty(WORKSPACE_BYTES, dtype=torch.uint8, device=dev)
-        _lib.call("exsum_cuda_workspace_init", self.buf.data_ptr(), WORKSPACE_BYTES,
+        self.nbytes = max(int(nbytes), WORKSPACE_BYTES)  # > WORKSPACE_BYTES: segment order room
+        self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=dev)
+        _lib.call("exsum_cuda_workspace_init", self.buf.data_ptr(), self.nbytes,
                   _stream_handle(dev))
 
     @property
@@ -69,6 +70,26 @@ def _workspace(device: torch.device) -> Workspace:
         ws = _ws_cache.get(key)
         if ws is None:
             ws = _ws_cache[key] = Workspace(device)
+        return ws
+
+
+def segmented_workspace_bytes(nseg: int) -> int:
+    """Workspace size that lets exsum_cuda_sum_segmented schedule nseg segments
+    longest first (exsum_cuda_segmented_workspace_bytes)."""
+    return int(lib.exsum_cuda_segmented_workspace_bytes(int(nseg)))
+
+
+_seg_ws_cache: dict[tuple[int, int], Workspace] = {}
+
+
+def _segmented_workspace(device: torch.device, nseg: int) -> Workspace:
+    key = (device.index if device.index is not None else torch.cuda.current_device(),
+           _stream_handle(device))
+    need = segmented_workspace_bytes(nseg)
+    with _ws_lock:
+        ws = _seg_ws_cache.get(key)
+        if ws is None or ws.nbytes < need:
+            ws = _seg_ws_cache[key] = Workspace(device, need)
         return ws
 
 
@@ -295,12 +316,16 @@ def exact_mean(values, method: str = "large") -> float:
 
 def exact_sum_segmented(x: torch.Tensor, offsets: torch.Tensor, *,
                         partials: bool = False,
-                        workspace: Workspace | None = None):
+                        workspace: Workspace | None = None,
+                        longest_first: bool = True):
     """One exact sum per segment: out[i] = exact_sum(x[offsets[i]:offsets[i+1]]).
 
     x: CUDA float64; offsets: CUDA int64/uint64 with nseg + 1 nondecreasing entries.
     Returns a float64 tensor of nseg sums (and the uint8 [nseg, 592] partial
     records if ``partials``; their Inf/NaN indices are local to each segment).
+    Segments are scheduled longest first when ``longest_first`` and the
+    workspace has room for the order (``segmented_workspace_bytes``; the
+    default workspace does); the bits are the same either way.
     """
     if not (x.is_cuda and offsets.is_cuda):
         raise ValueError("exact_sum_segmented needs CUDA tensors")
@@ -315,10 +340,10 @@ def exact_sum_segmented(x: torch.Tensor, offsets: torch.Tensor, *,
         if partials else None
     if nseg <= 0:
         return (out, parts) if partials else out
-    ws = workspace or _workspace(dev)
+    ws = workspace or _segmented_workspace(dev, nseg)
     _lib.call("exsum_cuda_sum_segmented", x.data_ptr(), offsets.data_ptr(), nseg,
               out.data_ptr(), parts.data_ptr() if partials else None, ws.ptr,
-              WORKSPACE_BYTES, _stream_handle(dev))
+              ws.nbytes if longest_first else WORKSPACE_BYTES, _stream_handle(dev))
     return (out, parts) if partials else out
 
 

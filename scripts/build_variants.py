@@ -25,6 +25,11 @@ VARIANTS = {
     "w9v7": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9", "EXSUM_VEC_PER_LANE=7"),
     "w9v6": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9", "EXSUM_VEC_PER_LANE=6"),
     "segsplit": ("EXSUM_SEG_SPLIT=1",),
+    "noahead": ("EXSUM_SEG_AHEAD=0",),
+    "noahead_early": ("EXSUM_SEG_AHEAD=0", "EXSUM_SCALARS_LATE=0"),
+    "early": ("EXSUM_SCALARS_LATE=0",),
+    "ahead1": ("EXSUM_SEG_AHEAD=1",),
+    "ahead2": ("EXSUM_SEG_AHEAD=2",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 verbose = "-v" in names

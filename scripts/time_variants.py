@@ -26,7 +26,7 @@ for config, n, K in %s:
         x = torch.empty(tot, dtype=torch.float64, device=dev)
         _lib.call("exsum_cuda_gen_segmented", 1, 0, tot, x.data_ptr(), torch.cuda.current_stream().cuda_stream)
         o = torch.from_numpy(offs.astype(np.int64)).to(dev)
-        ws = ops.Workspace(dev)
+        ws = ops.Workspace(dev, ops.segmented_workspace_bytes(n) if os.environ.get("TV_SEG_ORDER") == "longest" else 0)
         for _ in range(3):
             r = ops.exact_sum_segmented(x, o, workspace=ws)
         torch.cuda.synchronize()

@@ -211,6 +211,40 @@ def test_config5_segmented(cuda, checker):
         assert np.array_equal(got, want), int((got != want).sum())
         kinds = (want >> np.uint64(52)) & np.uint64(0x7FF)
         assert (kinds == 0x7FF).any() and (kinds != 0x7FF).any()  # both outcomes occur
+        # index-order claims (workspace without room for the order): same bits
+        idx = ops.exact_sum_segmented(x, torch.from_numpy(offs.astype(np.int64)).cuda(),
+                                      longest_first=False)
+        assert np.array_equal(idx.cpu().numpy().view(np.uint64), want)
+        del x
+
+
+def test_segment_order_edge_cases(cuda, checker):
+    """Longest-first scheduling over ragged segment lists: empty segments, a
+    few huge ones among many tiny ones, all-equal lengths, fewer segments than
+    warps, repeated calls on one workspace (the claim counter resets); records
+    (partials) as well as rounded sums match the index-order run and the checker."""
+    rng = np.random.default_rng(77)
+    cases = [
+        np.zeros(5000, dtype=np.int64),                                   # all empty
+        np.full(3000, 7, dtype=np.int64),                                 # equal lengths
+        rng.integers(0, 3, 20_000),                                       # tiny, many empty
+        np.concatenate([rng.integers(0, 50, 9000), [2_000_000, 1_500_000, 0, 1]]),
+        rng.integers(0, 2000, 100),                                       # < warps: no order pass
+        np.exp(rng.uniform(0, np.log(3e5), 4000)).astype(np.int64),
+    ]
+    for lens in cases:
+        offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+        total = int(offs[-1])
+        x = gen(3, max(total, 1), seed=int(lens.size))[:total]
+        od = torch.from_numpy(offs).cuda()
+        ws = ops.Workspace(x.device, ops.segmented_workspace_bytes(lens.size))
+        a, pa = ops.exact_sum_segmented(x, od, partials=True, workspace=ws)
+        a2 = ops.exact_sum_segmented(x, od, workspace=ws)  # reuse: counters were reset
+        b, pb = ops.exact_sum_segmented(x, od, partials=True, longest_first=False)
+        want = checker.segmented_sum(x.cpu().numpy(), offs.astype(np.uint64)).view(np.uint64)
+        for got in (a, a2, b):
+            assert np.array_equal(got.cpu().numpy().view(np.uint64), want), lens.size
+        assert torch.equal(pa, pb)
         del x
 
 
