@@ -88,6 +88,10 @@
                            // (1: a step per batch, 2: after the first loads; both measured
                            // slower, profiles/r01_variants_seg_ahead.log)
 #endif
+#ifndef EXSUM_SUM_SCAN
+#define EXSUM_SUM_SCAN 1  // single-sum kernel: scanning Inf/NaN fix-up (0: per-term loop; 1.43x
+                          // faster on 1e-4 Inf/NaN data, neutral otherwise: r01_variants_sumscan.log)
+#endif
 #ifndef EXSUM_SCALARS_LATE
 #define EXSUM_SCALARS_LATE 1  // scalar head/tail terms after the first batch's loads
 #endif
@@ -1116,7 +1120,7 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
   const Lane a = lane_view(wsm, lane);
   Specials sp{~0ull, ~0ull, ~0ull};
   int norm_count = 0;
-  warp_accumulate<V, EXSUM_UNIFORM_FAST != 0, true, false, kOp>(
+  warp_accumulate<V, EXSUM_UNIFORM_FAST != 0, true, EXSUM_SUM_SCAN != 0 && kOp == kSum, kOp>(
       x, y, tb, te, base_index, a, sp, norm_count, lane);
 
   // K2: the warp's 67 chunk sums.

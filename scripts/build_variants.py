@@ -28,6 +28,7 @@ VARIANTS = {
     "noahead": ("EXSUM_SEG_AHEAD=0",),
     "noahead_early": ("EXSUM_SEG_AHEAD=0", "EXSUM_SCALARS_LATE=0"),
     "early": ("EXSUM_SCALARS_LATE=0",),
+    "sumloop": ("EXSUM_SUM_SCAN=0",),
     "ahead1": ("EXSUM_SEG_AHEAD=1",),
     "ahead2": ("EXSUM_SEG_AHEAD=2",),
 }

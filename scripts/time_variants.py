@@ -1,6 +1,7 @@
 """Time kernel variants (lib/variants/*.so) on configs 2/3 (1e8) and 4 (1e9).
 
 Each variant runs in its own process (EXSUM_LIB selects the .so).
+Config 6 = one sum over config-5 values (frequent Inf/NaN).
 TV_OVERLAP=1 launches back-to-back sums with programmatic dependent launch
 (the bench's mode); TV_CONFIGS=2,3 restricts the configs.  Prints one
 line per (variant, config): ms per sum, GB/s, result bits (must agree).
@@ -41,7 +42,10 @@ for config, n, K in %s:
         del x; torch.cuda.empty_cache()
         continue
     x = torch.empty(n, dtype=torch.float64, device=dev)
-    _lib.call("exsum_cuda_gen", config, 1, n, 0, n, x.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    if config == 6:  # one sum over config-5 values (1e-4 Inf/NaN, wide exponents)
+        _lib.call("exsum_cuda_gen_segmented", 1, 0, n, x.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    else:
+        _lib.call("exsum_cuda_gen", config, 1, n, 0, n, x.data_ptr(), torch.cuda.current_stream().cuda_stream)
     res = torch.empty(1, dtype=torch.float64, device=dev)
     part = torch.empty(ops.PARTIAL_BYTES, dtype=torch.uint8, device=dev)
     ws = ops.Workspace(dev)
@@ -60,7 +64,8 @@ for config, n, K in %s:
 print("RESULT", json.dumps(out))
 '''
 
-cases = [(2, 100_000_000, 20), (3, 100_000_000, 20), (4, 1_000_000_000, 5), (5, 65_536, 5)]
+cases = [(2, 100_000_000, 20), (3, 100_000_000, 20), (4, 1_000_000_000, 5), (5, 65_536, 5),
+         (6, 100_000_000, 20)]
 if os.environ.get("TV_CONFIGS"):
     keep = {int(c) for c in os.environ["TV_CONFIGS"].split(",")}
     cases = [c for c in cases if c[0] in keep]

@@ -162,6 +162,27 @@ def test_configs_moderate(config, cuda, checker):
         assert list(part.acc.chunk) == list(ch), (config, n)
 
 
+def test_frequent_specials_single_sum(cuda, checker):
+    """One sum over data with frequent Inf/NaN (config-5 values: 1e-4 specials,
+    so most batches take the scanning fix-up), with random NaN payloads
+    planted: result bits, canonical chunks and inf/nan state against the
+    reference, for whole arrays and for finite-only subranges."""
+    rng = np.random.default_rng(5)
+    n = 3_000_001
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    _lib.call("exsum_cuda_gen_segmented", 9, 0, n, x.data_ptr(), stream())
+    h = x.cpu().numpy().copy()
+    idx = rng.choice(n, 40, replace=False)
+    h.view(np.uint64)[idx] = np.uint64(0x7FF0000000000000) | rng.integers(1, 1 << 51, 40).astype(np.uint64)
+    for arr in (h, h[h.view(np.uint64) & np.uint64(0x7FF0000000000000) != np.uint64(0x7FF0000000000000)],
+                h[::-1].copy()):
+        got, part = dev_sum(to_dev(arr, 1))
+        assert got == bits_of(checker.exact_sum(arr))
+        ch, top, ib, nb = checker.canonical(arr)
+        assert list(part.acc.chunk) == list(ch)
+        assert (part.acc.inf_bits, part.acc.nan_bits) == (ib, nb)
+
+
 def test_config1_small_superaccumulator(cuda, checker):
     # BASELINE config 1: N = 1000 U[-1,1), the reference's small method
     x = gen(1, 1000, 42)
