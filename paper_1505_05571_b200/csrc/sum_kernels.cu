@@ -88,6 +88,9 @@
                            // (1: a step per batch, 2: after the first loads; both measured
                            // slower, profiles/r01_variants_seg_ahead.log)
 #endif
+#ifndef EXSUM_RMW_ORDER
+#define EXSUM_RMW_ORDER 0  // add_term: 0 ld L,H st L,H; 1 ld L,H st H,L; 2 ld H,L st H,L
+#endif
 #ifndef EXSUM_SUM_SCAN
 #define EXSUM_SUM_SCAN 1  // single-sum kernel: scanning Inf/NaN fix-up (0: per-term loop; 1.43x
                           // faster on 1e-4 Inf/NaN data, neutral otherwise: r01_variants_sumscan.log)
@@ -256,16 +259,24 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
   asm("shr.u32 %0, %1, 5;" : "=r"(k) : "r"(ep));
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(k), "r"(a.c128), "r"(a.sl));
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));
+#if EXSUM_RMW_ORDER == 0
+#define EXSUM_RMW_LD "ld.shared.u32 l, [%0];\n\tld.shared.v2.u32 {h0, h1}, [%1];\n\t"
+#define EXSUM_RMW_ST "st.shared.u32 [%0], l;\n\tst.shared.v2.u32 [%1], {h0, h1};\n\t}"
+#elif EXSUM_RMW_ORDER == 1
+#define EXSUM_RMW_LD "ld.shared.u32 l, [%0];\n\tld.shared.v2.u32 {h0, h1}, [%1];\n\t"
+#define EXSUM_RMW_ST "st.shared.v2.u32 [%1], {h0, h1};\n\tst.shared.u32 [%0], l;\n\t}"
+#else
+#define EXSUM_RMW_LD "ld.shared.v2.u32 {h0, h1}, [%1];\n\tld.shared.u32 l, [%0];\n\t"
+#define EXSUM_RMW_ST "st.shared.v2.u32 [%1], {h0, h1};\n\tst.shared.u32 [%0], l;\n\t}"
+#endif
   asm volatile(
       "{\n\t.reg .u32 l, h0, h1, cf;\n\t"
-      "ld.shared.u32 l, [%0];\n\t"
-      "ld.shared.v2.u32 {h0, h1}, [%1];\n\t"
+      EXSUM_RMW_LD
       "add.cc.u32 cf, %2, %2;\n\t"
       "addc.cc.u32 l, l, %3;\n\t"
       "addc.cc.u32 h0, h0, %4;\n\t"
       "addc.u32 h1, h1, %5;\n\t"
-      "st.shared.u32 [%0], l;\n\t"
-      "st.shared.v2.u32 [%1], {h0, h1};\n\t}"
+      EXSUM_RMW_ST
       :
       : "r"(la), "r"(ha), "r"(s), "r"(u0), "r"(u1), "r"(u2)
       : "memory");

@@ -29,6 +29,8 @@ VARIANTS = {
     "noahead_early": ("EXSUM_SEG_AHEAD=0", "EXSUM_SCALARS_LATE=0"),
     "early": ("EXSUM_SCALARS_LATE=0",),
     "sumloop": ("EXSUM_SUM_SCAN=0",),
+    "rmw1": ("EXSUM_RMW_ORDER=1",),
+    "rmw2": ("EXSUM_RMW_ORDER=2",),
     "ahead1": ("EXSUM_SEG_AHEAD=1",),
     "ahead2": ("EXSUM_SEG_AHEAD=2",),
 }
