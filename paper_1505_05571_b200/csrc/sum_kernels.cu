@@ -88,6 +88,9 @@
                            // (1: a step per batch, 2: after the first loads; both measured
                            // slower, profiles/r01_variants_seg_ahead.log)
 #endif
+#ifndef EXSUM_DIGITS
+#define EXSUM_DIGITS 0  // lane accumulators as 16-bit digit rows updated by shared reductions
+#endif
 #ifndef EXSUM_RMW_ORDER
 #define EXSUM_RMW_ORDER 0  // add_term: 0 ld L,H st L,H; 1 ld L,H st H,L; 2 ld H,L st H,L
 #endif
@@ -140,7 +143,15 @@ constexpr int kSlots = EXSUM_SLOTS;  // slots 0..63 take terms (e' >> 5), the re
 static_assert(kSlots == 65 || kSlots == 66, "slot count");
 constexpr int kLPlane = kSlots * 32 * 4;
 constexpr int kHPlane = kSlots * 32 * 8;
+#if EXSUM_DIGITS
+// Digit representation: 133 rows of lane-interleaved int32 digits, digit i of
+// weight 2^(16 i - 1075); a term touches 5 consecutive digits (red.shared.add,
+// no read-modify-write chain); 2^15 adds of headroom per digit.
+constexpr int kDigitRows = 133;  // 0..131 take term pieces, 132 only carries
+constexpr int kWarpSmem = kDigitRows * 32 * 4;          // 17,024 B
+#else
 constexpr int kWarpSmem = kLPlane + kHPlane;            // 25,344 B
+#endif
 constexpr int kScratch = kWarps * kChunks * 8;          // per-warp chunk rows
 constexpr int kSmem = kWarps * kWarpSmem + kScratch;    // 207,040 B (8 warps, 66 slots)
 constexpr int kPrefetchBatches = EXSUM_PREFETCH_BATCHES;
@@ -200,6 +211,59 @@ __device__ __forceinline__ void zero_warp(unsigned char *warp_smem, int lane) {
   for (int i = lane; i < n16; i += 32) p[i] = make_uint4(0, 0, 0, 0);
 }
 
+#if EXSUM_DIGITS
+// Add the term (lo, hi) with exponent field e to the lane's digits: the
+// 53-bit significand shifted by b = e' & 15 (<= 68 bits) as five 16-bit
+// pieces into digits d .. d+4, d = e' >> 4, each negated for a negative term
+// (IMAD on the FMA pipe).  Fire-and-forget shared reductions: no load, no
+// dependency between terms.
+__device__ __forceinline__ void add_term_digits(const Lane &a, uint32_t lo, uint32_t hi,
+                                                uint32_t e) {
+  uint32_t sm, ep, d, mhi, mh, b, dg, u0, u1, u2, addr;
+  asm("shr.s32 %0, %1, 31;" : "=r"(sm) : "r"(hi));
+  asm("or.b32 %0, %0, 1;" : "+r"(sm));                                     // +1 / -1
+  asm("max.u32 %0, %1, 1;" : "=r"(ep) : "r"(e));
+  asm("mad.lo.u32 %0, %1, -1, %2;" : "=r"(d) : "r"(e), "r"(ep));          // 1 iff e == 0
+  asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x100000u));
+  asm("mad.lo.u32 %0, %1, -1048576, %2;" : "=r"(mh) : "r"(d), "r"(mhi));
+  asm("and.b32 %0, %1, 15;" : "=r"(b) : "r"(ep));
+  asm("shr.u32 %0, %1, 4;" : "=r"(dg) : "r"(ep));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(0u), "r"(lo), "r"(b));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lo), "r"(mh), "r"(b));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mh), "r"(0u), "r"(b));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(dg), "r"(a.c128), "r"(a.sl));
+  const uint32_t q0 = (u0 & 0xFFFFu) * sm, q1 = (u0 >> 16) * sm, q2 = (u1 & 0xFFFFu) * sm,
+                 q3 = (u1 >> 16) * sm, q4 = u2 * sm;
+  asm volatile(
+      "red.shared.add.u32 [%0], %1;\n\t"
+      "red.shared.add.u32 [%0+128], %2;\n\t"
+      "red.shared.add.u32 [%0+256], %3;\n\t"
+      "red.shared.add.u32 [%0+384], %4;\n\t"
+      "red.shared.add.u32 [%0+512], %5;" ::"r"(addr),
+      "r"(q0), "r"(q1), "r"(q2), "r"(q3), "r"(q4)
+      : "memory");
+}
+
+// A signed 96-bit value (v2:v1:v0) of 32-bit slot k (weight 2^(32k - 1075))
+// into digits 2k .. 2k+5: five unsigned 16-bit pieces and a signed top piece.
+__device__ __forceinline__ void slot_add96_digits(const Lane &a, uint32_t k, uint32_t v0,
+                                                  uint32_t v1, uint32_t v2) {
+  uint32_t addr;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(k), "r"(a.c128 * 2u), "r"(a.sl));
+  const uint32_t top = static_cast<uint32_t>(static_cast<int32_t>(v2) >> 16);
+  asm volatile(
+      "red.shared.add.u32 [%0], %1;\n\t"
+      "red.shared.add.u32 [%0+128], %2;\n\t"
+      "red.shared.add.u32 [%0+256], %3;\n\t"
+      "red.shared.add.u32 [%0+384], %4;\n\t"
+      "red.shared.add.u32 [%0+512], %5;\n\t"
+      "red.shared.add.u32 [%0+640], %6;" ::"r"(addr),
+      "r"(v0 & 0xFFFFu), "r"(v0 >> 16), "r"(v1 & 0xFFFFu), "r"(v1 >> 16), "r"(v2 & 0xFFFFu),
+      "r"(top)
+      : "memory");
+}
+#endif
+
 // The term as three 32-bit words of its complemented, shifted significand
 // (u2:u1:u0 = s ? ~(m << sh) : m << sh; a negative term's +1 is the carry-in
 // s + s) and e' = max(e, 1).  The B200 integer ALU pipe and the FMA pipe each
@@ -234,6 +298,10 @@ __device__ __forceinline__ void decode96(uint32_t lo, uint32_t hi, uint32_t e, u
 // Read-modify-write of slot k with a 96-bit two's-complement value (no carry-in).
 __device__ __forceinline__ void slot_add96(const Lane &a, uint32_t k, uint32_t v0, uint32_t v1,
                                            uint32_t v2) {
+#if EXSUM_DIGITS
+  slot_add96_digits(a, k, v0, v1, v2);
+  return;
+#endif
   uint32_t la, ha;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(k), "r"(a.c128), "r"(a.sl));
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));
@@ -254,6 +322,10 @@ __device__ __forceinline__ void slot_add96(const Lane &a, uint32_t k, uint32_t v
 // Add one term (exponent field e != 2047, or 2047 for the blind add of an
 // Inf/NaN that the batch fix-up cancels) to the lane's slots.
 __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
+#if EXSUM_DIGITS
+  add_term_digits(a, lo, hi, e);
+  return;
+#endif
   uint32_t s, ep, k, la, ha, u0, u1, u2;
   decode96(lo, hi, e, s, u0, u1, u2, ep);
   asm("shr.u32 %0, %1, 5;" : "=r"(k) : "r"(ep));
@@ -287,6 +359,19 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
 // lane sum, 2^1024 x 2^31 terms).
 // Safe whenever every slot has absorbed <= 2047 terms (|H_k| < 2^63 - 2^52).
 __device__ __forceinline__ void normalize(const Lane &a) {
+#if EXSUM_DIGITS
+  // digits below the top in [0, 2^16), the carry-only top digit keeps the rest
+  int32_t *D = reinterpret_cast<int32_t *>(a.L);
+  long long cd = 0;
+#pragma unroll 7
+  for (int i = 0; i < kDigitRows - 1; ++i) {
+    const long long v = static_cast<long long>(D[32 * i]) + cd;
+    D[32 * i] = static_cast<int32_t>(v & 0xFFFF);
+    cd = v >> 16;
+  }
+  D[32 * (kDigitRows - 1)] += static_cast<int32_t>(cd);
+  return;
+#endif
   long long c = 0;
 #pragma unroll 6
   for (int k = 0; k < kSlots - 1; ++k) {
@@ -310,7 +395,68 @@ __device__ __forceinline__ void normalize(const Lane &a) {
 // Lane j sums the rows of slots j, j+32, j+64 with bank-skewed 128-bit reads
 // (8 lanes per wavefront hit 8 distinct 16-byte bank groups), then the chunk
 // values are assembled with shuffles: 24 LDS.128 per lane per round.
+#if EXSUM_DIGITS
+// Digit rows summed over the 32 lanes (lane j: rows j, j+32, ..., bank-skewed
+// 128-bit reads), then chunk c = R[2c] + 2^16 R[2c+1] (c < 66), chunk 66 =
+// R[132]; |R| < 2^36 so |chunk| < 2^53.
+__device__ __forceinline__ void warp_chunks_digits(unsigned char *warp_smem, int lane,
+                                                   long long *row) {
+  __syncwarp();
+  const int32_t *Dp = reinterpret_cast<const int32_t *>(warp_smem);
+  long long R[5];
+#pragma unroll
+  for (int r = 0; r < 5; ++r) {
+    const int i = 32 * r + lane;
+    long long acc = 0;
+    if (i < kDigitRows) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int4 v = *reinterpret_cast<const int4 *>(Dp + i * 32 + 4 * ((q + lane) & 7));
+        acc += static_cast<long long>(v.x) + v.y + static_cast<long long>(v.z) + v.w;
+      }
+    }
+    R[r] = acc;
+  }
+  const int src = (2 * lane) & 31;
+  long long v[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {  // chunks 32r + lane
+    const long long e0 = __shfl_sync(0xffffffffu, R[2 * r], src);
+    const long long e1 = __shfl_sync(0xffffffffu, R[2 * r], src + 1);
+    const long long o0 = r < 2 ? __shfl_sync(0xffffffffu, R[2 * r + 1], src) : 0ll;
+    const long long o1 = r < 2 ? __shfl_sync(0xffffffffu, R[2 * r + 1], src + 1) : 0ll;
+    const long long lo = lane < 16 ? e0 : o0, hi = lane < 16 ? e1 : o1;
+    v[r] = lo + hi * 65536ll;  // chunk 66: digit 132 alone (row 133 reads as 0)
+  }
+  // Two carry passes bring every chunk below the top into [0, 2^32 + 2) (from
+  // |c| < 2^53), the scale the CTA / grid / multi-launch chunk sums assume.
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    long long c[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const bool carries = 32 * r + lane < kChunks - 1;
+      c[r] = carries ? v[r] >> 32 : 0;
+      if (carries) v[r] &= 0xFFFFFFFFll;
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const long long up = __shfl_up_sync(0xffffffffu, c[r], 1);
+      const long long wrap = r ? __shfl_sync(0xffffffffu, c[r > 0 ? r - 1 : 0], 31) : 0ll;
+      v[r] += lane ? up : wrap;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    if (32 * r + lane < kChunks) row[32 * r + lane] = v[r];
+}
+#endif
+
 __device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, int lane, long long *row) {
+#if EXSUM_DIGITS
+  warp_chunks_digits(warp_smem, lane, row);
+  return;
+#endif
   __syncwarp();
   const uint32_t *Lp = reinterpret_cast<const uint32_t *>(warp_smem);
   const uint32_t *Hw = reinterpret_cast<const uint32_t *>(warp_smem + kLPlane);
@@ -691,7 +837,11 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
                                                 unsigned long long index_base, const Lane &a,
                                                 Specials &sp, int &norm_count, int lane,
                                                 Hook hook = Hook{}) {
+#if EXSUM_DIGITS
+  constexpr int kNormEvery = 32000 / (4 * V);  // digits: 2^15 adds of headroom
+#else
   constexpr int kNormEvery = 2016 / (4 * V);  // batches between renormalisations
+#endif
   static_assert(kNormEvery >= 1, "batch too large for the carry budget");
   if (begin >= end) return;
   // Scalar head up to 32-byte alignment of &x[pos], scalar tail after the

@@ -31,6 +31,7 @@ VARIANTS = {
     "sumloop": ("EXSUM_SUM_SCAN=0",),
     "rmw1": ("EXSUM_RMW_ORDER=1",),
     "rmw2": ("EXSUM_RMW_ORDER=2",),
+    "digits": ("EXSUM_DIGITS=1",),
     "ahead1": ("EXSUM_SEG_AHEAD=1",),
     "ahead2": ("EXSUM_SEG_AHEAD=2",),
 }
