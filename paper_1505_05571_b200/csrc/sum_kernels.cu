@@ -19,7 +19,7 @@
 // ~3.5x in bank conflicts, and U[0,1) puts half of all terms in one bin.
 //
 // Per-term cost: 23.9 SASS instructions (14 integer ALU, 5 FMA-pipe IMADs, 4.25
-// LSU) and 6 shared wavefronts.  Loads are 256-bit (LDG.E.NA.ENL2.256),
+// LSU) and 6 shared wavefronts.  Loads are 256-bit (LDG.E.EF.ENL2.256),
 // "rolling": a vector's registers are refilled with the next batch's vector
 // right after its four terms are added, with a cp.async.bulk L2 prefetch one
 // batch further ahead.  When every lane's batch falls in one slot (narrow
@@ -87,6 +87,10 @@
 #define EXSUM_SEG_AHEAD 0  // segmented kernel: claim the next segment during the current one
                            // (1: a step per batch, 2: after the first loads; both measured
                            // slower, profiles/r01_variants_seg_ahead.log)
+#endif
+#ifndef EXSUM_LDG_KIND
+#define EXSUM_LDG_KIND 2  // 256-bit loads: 0 nc+L1::no_allocate, 1 nc, 2 nc+L1::evict_first (3-4%
+                          // faster on configs 3-5 than 0: r01_variants_ldg.log), 3 plain
 #endif
 #ifndef EXSUM_DIGITS
 #define EXSUM_DIGITS 0  // lane accumulators as 16-bit digit rows updated by shared reductions
@@ -580,10 +584,21 @@ __device__ __forceinline__ void add_elem_checked(const Lane &a, Specials &sp, co
   }
 }
 
-// 256-bit streaming load (LDG.E.NA.ENL2.256): 4 terms per lane per instruction.
+// 256-bit streaming load (LDG.E.EF.ENL2.256): 4 terms per lane per instruction.
+#if EXSUM_LDG_KIND == 1
+#define EXSUM_LDG256 "ld.global.nc.v8.u32"
+#elif EXSUM_LDG_KIND == 2
+#define EXSUM_LDG256 "ld.global.nc.L1::evict_first.v8.u32"
+#elif EXSUM_LDG_KIND == 3
+#define EXSUM_LDG256 "ld.global.v8.u32"
+#elif EXSUM_LDG_KIND == 4
+#define EXSUM_LDG256 "ld.global.nc.L1::evict_first.L2::256B.v8.u32"
+#else
+#define EXSUM_LDG256 "ld.global.nc.L1::no_allocate.v8.u32"
+#endif
 __device__ __forceinline__ void ldg256(const double *p, uint32_t (&w)[8]) {
   asm volatile(
-      "ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      EXSUM_LDG256 " {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
       : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
         "=r"(w[7])
       : "l"(p));

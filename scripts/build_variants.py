@@ -32,6 +32,13 @@ VARIANTS = {
     "rmw1": ("EXSUM_RMW_ORDER=1",),
     "rmw2": ("EXSUM_RMW_ORDER=2",),
     "digits": ("EXSUM_DIGITS=1",),
+    "ldg1": ("EXSUM_LDG_KIND=1",),
+    "ldg0": ("EXSUM_LDG_KIND=0",),
+    "ldg3": ("EXSUM_LDG_KIND=3",),
+    "ldg4": ("EXSUM_LDG_KIND=4",),
+    "pf0": ("EXSUM_PREFETCH_BATCHES=0",),
+    "pf2": ("EXSUM_PREFETCH_BATCHES=2",),
+    "v6": ("EXSUM_VEC_PER_LANE=6",),
     "ahead1": ("EXSUM_SEG_AHEAD=1",),
     "ahead2": ("EXSUM_SEG_AHEAD=2",),
 }
