@@ -50,6 +50,18 @@ def test_struct_layouts():
     assert lib.exsum_cuda_workspace_bytes() >= 67 * 8
 
 
+def test_segmented_workspace_sizes():
+    """Room for the longest-first claim order: 4 bytes per segment after the
+    base workspace and the order state; beyond 2^24 segments the kernel claims
+    in index order and needs only the base workspace."""
+    base = lib.exsum_cuda_workspace_bytes()
+    w0 = lib.exsum_cuda_segmented_workspace_bytes(0)
+    assert w0 >= base
+    assert lib.exsum_cuda_segmented_workspace_bytes(65536) == w0 + 4 * 65536
+    assert lib.exsum_cuda_segmented_workspace_bytes(1 << 24) == w0 + 4 * (1 << 24)
+    assert lib.exsum_cuda_segmented_workspace_bytes((1 << 24) + 1) == base
+
+
 def test_status_codes_without_gpu():
     EINVAL = _lib.EXSUM_EINVAL
     assert lib.exsum_small_init(None) == EINVAL
