@@ -183,7 +183,8 @@ int exsum_cuda_finalize(double *d_result, exsum_partial *d_partial, void *d_ws,
                         size_t ws_bytes, void *stream);
 
 /* One exact_sum per segment: segment i is d_x[d_offsets[i] .. d_offsets[i+1]).
- * d_offsets has nseg + 1 nondecreasing entries.  No reference batch API exists;
+ * d_offsets has nseg + 1 nondecreasing entries (a decreasing pair is read as an
+ * empty segment, sum +0.0, never as a wrapped length).  No reference batch API exists;
  * semantics = exact_sum(segment_i) for every i.
  * d_partials may be NULL; otherwise nseg records, indices local to the segment.
  * With ws_bytes >= exsum_cuda_segmented_workspace_bytes(nseg) the segments are

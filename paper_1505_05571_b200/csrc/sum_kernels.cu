@@ -1514,6 +1514,7 @@ struct ClaimAhead {
         if (s < nseg) {
           b = __ldg(offs + s);
           e = __ldg(offs + s + 1);
+          if (e < b) e = b;  // decreasing offsets (a caller error): an empty segment, +0.0
         }
         break;
       case 3:

@@ -253,6 +253,14 @@ def test_segment_order_edge_cases(cuda, checker):
         rng.integers(0, 2000, 100),                                       # < warps: no order pass
         np.exp(rng.uniform(0, np.log(3e5), 4000)).astype(np.int64),
     ]
+    # a decreasing offset pair reads as an empty segment (+0.0), not a wrapped length
+    x = gen(2, 100, seed=3)
+    od = torch.tensor([0, 50, 20, 100], dtype=torch.int64, device="cuda")
+    got = ops.exact_sum_segmented(x, od).cpu().numpy().view(np.uint64)
+    h = x.cpu().numpy()
+    assert int(got[1]) == 0
+    assert int(got[0]) == bits_of(checker.exact_sum(h[:50]))
+    assert int(got[2]) == bits_of(checker.exact_sum(h[20:]))
     for lens in cases:
         offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
         total = int(offs[-1])
