@@ -88,6 +88,16 @@
                            // (1: a step per batch, 2: after the first loads; both measured
                            // slower, profiles/r01_variants_seg_ahead.log)
 #endif
+#ifndef EXSUM_SEG_CLAIM
+#define EXSUM_SEG_CLAIM 0  // segmented kernel (EXSUM_SEG_AHEAD 0): 1 = the next segment's claim
+                           // atomic is issued when the current segment starts and its two
+                           // dependent reads are spread over the epilogue; 0 = all three round
+                           // trips after the loop (0.3% faster: r01_variants_seg_claim.log)
+#endif
+#ifndef EXSUM_SEG_FUSED_CLEAR
+#define EXSUM_SEG_FUSED_CLEAR 0  // segmented kernel: warp_chunks zeroes the rows it reads instead
+                                 // of a separate clear (1.5% slower: r01_variants_seg_claim.log)
+#endif
 #ifndef EXSUM_LDG_KIND
 #define EXSUM_LDG_KIND 2  // 256-bit loads: 0 nc+L1::no_allocate, 1 nc, 2 nc+L1::evict_first (3-4%
                           // faster on configs 3-5 than 0: r01_variants_ldg.log), 3 plain
@@ -456,14 +466,21 @@ __device__ __forceinline__ void warp_chunks_digits(unsigned char *warp_smem, int
 }
 #endif
 
+// kZero: store zeros over every row word after reading it (the accumulator is
+// left cleared for the next segment: no separate zero_warp pass).
+template <bool kZero = false>
 __device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, int lane, long long *row) {
 #if EXSUM_DIGITS
   warp_chunks_digits(warp_smem, lane, row);
+  if (kZero) {
+    __syncwarp();
+    zero_warp(warp_smem, lane);
+  }
   return;
 #endif
   __syncwarp();
-  const uint32_t *Lp = reinterpret_cast<const uint32_t *>(warp_smem);
-  const uint32_t *Hw = reinterpret_cast<const uint32_t *>(warp_smem + kLPlane);
+  uint32_t *Lp = reinterpret_cast<uint32_t *>(warp_smem);
+  uint32_t *Hw = reinterpret_cast<uint32_t *>(warp_smem + kLPlane);
   long long sl[3], shl[3], shh[3];
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
@@ -473,12 +490,16 @@ __device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, int lane, 
       long long a = 0, bl = 0, bh = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(Lp + k * 32 + 4 * ((i + lane) & 7));
+        uint4 *p = reinterpret_cast<uint4 *>(Lp + k * 32 + 4 * ((i + lane) & 7));
+        const uint4 v = *p;
+        if (kZero) *p = make_uint4(0, 0, 0, 0);
         a += static_cast<long long>(v.x) + v.y + static_cast<long long>(v.z) + v.w;
       }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(Hw + k * 64 + 4 * ((i + lane) & 15));
+        uint4 *p = reinterpret_cast<uint4 *>(Hw + k * 64 + 4 * ((i + lane) & 15));
+        const uint4 v = *p;
+        if (kZero) *p = make_uint4(0, 0, 0, 0);
         bl += static_cast<long long>(v.x) + v.z;
         bh += static_cast<long long>(static_cast<int32_t>(v.y)) + static_cast<int32_t>(v.w);
       }
@@ -1568,6 +1589,7 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
   ClaimAhead ca{&ws->seg_next, order, offs, x, nseg, 0u, 0u, 0ull, 0ull, 0};
   if (lane == 0)
     while (ca.stage < 3) ca.step();  // the first claim
+  if (EXSUM_SEG_FUSED_CLEAR) zero_warp(wsm, lane);  // later segments: cleared by warp_chunks
 #if EXSUM_TIMELINE
   unsigned long long ph[7] = {0, 0, 0, 0, 0, 0, 0}, tq = gtimer(), tn;
 #define EXSUM_SEG_PHASE(i) (tn = gtimer(), ph[i] += tn - tq, tq = tn)
@@ -1581,7 +1603,10 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
     const unsigned long long b = __shfl_sync(0xffffffffu, ca.b, 0),
                              e = __shfl_sync(0xffffffffu, ca.e, 0);
     ca.stage = 0;
-    zero_warp(wsm, lane);
+#if !EXSUM_SEG_AHEAD && EXSUM_SEG_CLAIM
+    if (lane == 0) ca.step();  // the next claim's atomic; its result is read after the loop
+#endif
+    if (!EXSUM_SEG_FUSED_CLEAR) zero_warp(wsm, lane);
     __syncwarp();
     int norm_count = 0;
     EXSUM_SEG_PHASE(1);
@@ -1601,11 +1626,18 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
     warp_accumulate<EXSUM_SEG_VEC, false, EXSUM_SEG_SPLIT != 0, true>(x, x, b, e, 0ull - b, a,
                                                                       sp, norm_count, lane);
     EXSUM_SEG_PHASE(2);
+#if EXSUM_SEG_CLAIM
+    if (lane == 0) ca.step();  // order[] read (the atomic returned during the loop)
+#else
     if (lane == 0)
       while (ca.stage < 3) ca.step();
+#endif
     EXSUM_SEG_PHASE(0);
 #endif
-    warp_chunks(wsm, lane, row);
+    warp_chunks<EXSUM_SEG_FUSED_CLEAR != 0>(wsm, lane, row);
+#if !EXSUM_SEG_AHEAD && EXSUM_SEG_CLAIM
+    if (lane == 0) ca.step();  // offsets read, overlapping the emit
+#endif
     const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                              N = warp_min_u64(sp.N);
     __syncwarp();
@@ -1613,6 +1645,9 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
     const unsigned long long payload =
         N != ~0ull ? __ldg(reinterpret_cast<const unsigned long long *>(x) + b + N) : 0ull;
     warp_emit(row, P, M, N, payload, out + s, partials ? partials + s : nullptr, lane);
+#if !EXSUM_SEG_AHEAD && EXSUM_SEG_CLAIM
+    if (lane == 0) ca.step();  // L2 prefetch of the next segment's head
+#endif
     __syncwarp();
     EXSUM_SEG_PHASE(4);
   }

@@ -41,6 +41,9 @@ VARIANTS = {
     "v6": ("EXSUM_VEC_PER_LANE=6",),
     "ahead1": ("EXSUM_SEG_AHEAD=1",),
     "ahead2": ("EXSUM_SEG_AHEAD=2",),
+    "segboth": ("EXSUM_SEG_CLAIM=1", "EXSUM_SEG_FUSED_CLEAR=1"),
+    "claimearly": ("EXSUM_SEG_CLAIM=1",),
+    "fusedclear": ("EXSUM_SEG_FUSED_CLEAR=1",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 verbose = "-v" in names
