@@ -98,6 +98,17 @@
 #define EXSUM_SEG_FUSED_CLEAR 0  // segmented kernel: warp_chunks zeroes the rows it reads instead
                                  // of a separate clear (1.5% slower: r01_variants_seg_claim.log)
 #endif
+#ifndef EXSUM_FIX_L1
+#define EXSUM_FIX_L1 2  // scanning Inf/NaN fix-up re-reads: 0 ld.global.cg of each high word (L2
+                        // round trips), 1 the same L1-allocating (the batch's lines are often still
+                        // in L1; the flagged term's full re-read hits the scanned sector), 2 whole
+                        // 32-byte vectors, L1-allocating (8 wavefronts per 4 terms instead of per
+                        // term).  Config 5: 2.255 / 2.196 / 2.176 ms; 2-4 neutral
+                        // (r01_variants_fixup.log)
+#endif
+#ifndef EXSUM_NO_FIXUP
+#define EXSUM_NO_FIXUP 0  // timing probe only (wrong results on data with Inf/NaN): skip the fix-up
+#endif
 #ifndef EXSUM_LDG_KIND
 #define EXSUM_LDG_KIND 2  // 256-bit loads: 0 nc+L1::no_allocate, 1 nc, 2 nc+L1::evict_first (3-4%
                           // faster on configs 3-5 than 0: r01_variants_ldg.log), 3 plain
@@ -704,8 +715,9 @@ __device__ __forceinline__ void prefetch_batch(const double *X4, const double *Y
 // arithmetic, and always before the next renormalisation.  Kept inline (an
 // out-of-line call forces the lane's Specials into local memory).
 //   kScan = false: compact loop, one L2 round trip per term (cold data only).
-//   kScan = true:  all high words loaded at once into a bitmask, then only the
-//                  flagged terms are re-read (data with frequent specials).
+//   kScan = true:  the batch's vectors re-read at once (L1-allocating 256-bit
+//                  loads, usually L1 hits) into a bitmask of Inf/NaN terms, then
+//                  only the flagged terms are re-read (data with frequent specials).
 template <int V, bool kScan, int kOp>
 __device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, const double *X4,
                                                const double *Y4, long long v, long long nvec,
@@ -717,21 +729,54 @@ __device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, cons
     static_assert(4 * V <= 32, "scan mask holds one batch");
     const uint32_t *xh = reinterpret_cast<const uint32_t *>(X4);
     uint32_t mask = 0u;
+#if EXSUM_FIX_L1 == 2
+    // whole 32-byte vectors, L1-allocating (8 wavefronts per LDG.256 instead of
+    // 8 per 4-byte high word), four at a time
+    (void)xh;
+#pragma unroll
+    for (int h = 0; h < V; h += 4) {
+      uint32_t w[4][8];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const long long vec = v + (h + u) * 32 + lane;
+        if (h + u < V && vec < nvec) {
+          asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=r"(w[u][0]), "=r"(w[u][1]), "=r"(w[u][2]), "=r"(w[u][3]),
+                         "=r"(w[u][4]), "=r"(w[u][5]), "=r"(w[u][6]), "=r"(w[u][7])
+                       : "l"(X4 + 4 * vec));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) w[u][j] = 0u;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          mask |= static_cast<uint32_t>(exponent_field(w[u][2 * q + 1]) == 0x7FFu)
+                  << (4 * (h + u) + q);
+    }
+#else
 #pragma unroll
     for (int u = 0; u < V; ++u) {
       const long long vec = v + u * 32 + lane;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const uint32_t hi = vec < nvec ? __ldcg(xh + 2 * (4 * vec + q) + 1) : 0u;
+        const uint32_t hi =
+            vec < nvec ? (EXSUM_FIX_L1 ? __ldg(xh + 2 * (4 * vec + q) + 1)
+                                       : __ldcg(xh + 2 * (4 * vec + q) + 1))
+                       : 0u;
         mask |= static_cast<uint32_t>(exponent_field(hi) == 0x7FFu) << (4 * u + q);
       }
     }
+#endif
     while (mask) {
       const int i = __ffs(mask) - 1;
       mask &= mask - 1u;
       const long long vec = v + (i >> 2) * 32 + lane;
       const int q = i & 3;
-      const unsigned long long bits = __ldcg(xb + 4 * vec + q);
+      const unsigned long long bits =
+          EXSUM_FIX_L1 ? __ldg(xb + 4 * vec + q) : __ldcg(xb + 4 * vec + q);
       const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
       record_special(sp, lo, hi, ib + 4ull * static_cast<unsigned long long>(vec) + q);
       add_term(a, lo, hi ^ 0x80000000u, 0x7FFu);  // cancel the garbage add
@@ -938,7 +983,7 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
       }
     }
     hook();
-    if (__builtin_expect(emax == 0x7FFu, 0))
+    if (!EXSUM_NO_FIXUP && __builtin_expect(emax == 0x7FFu, 0))
       fixup_specials<V, kScan, kOp>(a, sp, X4, Y4, v, nvec, lane, ib);
     if (++norm_count >= kNormEvery) {
       normalize(a);

@@ -44,6 +44,9 @@ VARIANTS = {
     "segboth": ("EXSUM_SEG_CLAIM=1", "EXSUM_SEG_FUSED_CLEAR=1"),
     "claimearly": ("EXSUM_SEG_CLAIM=1",),
     "fusedclear": ("EXSUM_SEG_FUSED_CLEAR=1",),
+    "fixcg": ("EXSUM_FIX_L1=0",),
+    "fixl1": ("EXSUM_FIX_L1=1",),
+    "nofixup": ("EXSUM_NO_FIXUP=1",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 verbose = "-v" in names
