@@ -3,7 +3,8 @@
 Each variant runs in its own process (EXSUM_LIB selects the .so).
 Config 6 = one sum over config-5 values (frequent Inf/NaN).
 TV_OVERLAP=1 launches back-to-back sums with programmatic dependent launch
-(the bench's mode); TV_CONFIGS=2,3 restricts the configs.  Prints one
+(the bench's mode); TV_CONFIGS=2,3 restricts the configs; TV_SUSTAIN=S runs S seconds
+of back-to-back sums first and then times ~0.5 s (the power-capped steady state).  Prints one
 line per (variant, config): ms per sum, GB/s, result bits (must agree).
 """
 import json
@@ -53,6 +54,15 @@ for config, n, K in %s:
     for _ in range(3):
         ops.exact_sum_tensor(x, result=res, partial=part, workspace=ws, overlap=ov)
     torch.cuda.synchronize()
+    sus = float(os.environ.get("TV_SUSTAIN", "0"))  # seconds of back-to-back sums before timing
+    if sus > 0:
+        import time
+        t0 = time.time()
+        while time.time() - t0 < sus:
+            for _ in range(20):
+                ops.exact_sum_tensor(x, result=res, partial=part, workspace=ws, overlap=ov)
+            torch.cuda.synchronize()
+        K = max(K, int(0.5 / (1e-11 * n)) + 1)  # ~0.5 s timed at ~10 ps/term
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st.record()
     for _ in range(K):
