@@ -53,7 +53,7 @@ def main():
         m, kname = raw(rep)
         lines = [f"# ncu --set full --clock-control none: {tag}", f"kernel: {kname}", ""]
         lines += [f"{k:80s} {v} {u}" for k, (v, u) in m.items()]
-        (ROOT / "profiles" / f"ncu_{tag}.txt").write_text("\n".join(lines) + "\n")
+        (ROOT / "profiles" / f"r01_ncu_{tag}.txt").write_text("\n".join(lines) + "\n")
         f = lambda k: float(m[k][0].replace(",", "")) if k in m else None  # noqa: E731
         rd, wr = f("dram__bytes_read.sum"), f("dram__bytes_write.sum")
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
