@@ -109,6 +109,16 @@
 #ifndef EXSUM_NO_FIXUP
 #define EXSUM_NO_FIXUP 0  // timing probe only (wrong results on data with Inf/NaN): skip the fix-up
 #endif
+#ifndef EXSUM_GUARD32
+#define EXSUM_GUARD32 0  // guarded refills test a per-batch 32-bit count of the lane's remaining
+                         // vectors (one compare per vector) instead of a 64-bit index: fewer
+                         // instructions, but config 5 measured 3.5% slower with it (code layout of
+                         // the I-cache-sensitive segmented body; r01_variants_guard.log)
+#endif
+#ifndef EXSUM_PF_ALIGNED
+#define EXSUM_PF_ALIGNED 1  // L2 prefetch of the (32-byte aligned) x stream without the 16-byte
+                            // rounding arithmetic
+#endif
 #ifndef EXSUM_LDG_KIND
 #define EXSUM_LDG_KIND 2  // 256-bit loads: 0 nc+L1::no_allocate, 1 nc, 2 nc+L1::evict_first (3-4%
                           // faster on configs 3-5 than 0: r01_variants_ldg.log), 3 plain
@@ -689,24 +699,32 @@ __device__ __forceinline__ void load_batch(Batch<V, kOp> &b, const double *X4, c
 // Bulk L2 prefetch (cp.async.bulk.prefetch.L2) of the batch-sized stretch of
 // 32-byte vectors starting at vector v0, clipped to vend.  One lane issues it a
 // batch ahead of the register loads; it costs no registers and no shared memory.
-template <int V>
+// kAligned: X4 is 32-byte aligned (x always is after the head peel; kDotScalarB's
+// y is only 8-byte aligned).
+template <int V, bool kAligned = true>
 __device__ __forceinline__ void prefetch_l2(const double *X4, long long v0, long long vend) {
   if (v0 >= vend) return;
   long long nv = vend - v0;
   if (nv > V * 32) nv = V * 32;
   const uintptr_t p0 = reinterpret_cast<uintptr_t>(X4 + 4 * v0);
-  const uintptr_t p1 = p0 + static_cast<uintptr_t>(nv * 32);
-  const uintptr_t a0 = p0 & ~uintptr_t{15};  // kDotScalarB's y is only 8-byte aligned
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0),
-               "r"(static_cast<uint32_t>((p1 - a0 + 15) & ~uintptr_t{15}))
-               : "memory");
+  if constexpr (kAligned && EXSUM_PF_ALIGNED) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0),
+                 "r"(static_cast<uint32_t>(nv) * 32u)
+                 : "memory");
+  } else {
+    const uintptr_t p1 = p0 + static_cast<uintptr_t>(nv * 32);
+    const uintptr_t a0 = p0 & ~uintptr_t{15};
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0),
+                 "r"(static_cast<uint32_t>((p1 - a0 + 15) & ~uintptr_t{15}))
+                 : "memory");
+  }
 }
 
 template <int V, int kOp>
 __device__ __forceinline__ void prefetch_batch(const double *X4, const double *Y4, long long v0,
                                                long long vend) {
   prefetch_l2<V>(X4, v0, vend);
-  if constexpr (kOp >= kDot) prefetch_l2<V>(Y4, v0, vend);
+  if constexpr (kOp >= kDot) prefetch_l2<V, kOp == kDot>(Y4, v0, vend);
 }
 
 // Inf/NaN fix-up of one batch (rare): the batch's terms were added blindly;
@@ -831,6 +849,11 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
                                                   const double *X4, const double *Y4,
                                                   long long nv, long long nvec, int lane) {
   uint32_t emax = 0;
+  int r32 = 0;  // EXSUM_GUARD32: refill vector u exists iff u * 32 < r32
+  if constexpr (kGuard && EXSUM_GUARD32) {
+    const long long rem = nvec - nv - lane;
+    r32 = rem <= 0 ? 0 : rem > 0x7FFFFFFF ? 0x7FFFFFFF : static_cast<int>(rem);
+  }
 #pragma unroll
   for (int u = 0; u < V; ++u) {
     uint32_t lo[4], hi[4], e[4];
@@ -844,7 +867,7 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
 #pragma unroll
     for (int q = 0; q < 4; ++q) add_term(a, lo[q], hi[q], e[q]);
     const long long vec = nv + u * 32 + lane;
-    if (!kGuard || vec < nvec) {
+    if (!kGuard || (EXSUM_GUARD32 ? u * 32 < r32 : vec < nvec)) {
       load_vec<V, kOp>(b, u, X4, Y4, vec);
     } else {
       zero_vec<V, kOp>(b, u);

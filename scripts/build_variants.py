@@ -46,6 +46,8 @@ VARIANTS = {
     "fusedclear": ("EXSUM_SEG_FUSED_CLEAR=1",),
     "fixcg": ("EXSUM_FIX_L1=0",),
     "fixl1": ("EXSUM_FIX_L1=1",),
+    "pfold": ("EXSUM_PF_ALIGNED=0",),
+    "guard32": ("EXSUM_GUARD32=1",),
     "nofixup": ("EXSUM_NO_FIXUP=1",),
 }
 names = sys.argv[1:] or list(VARIANTS)
