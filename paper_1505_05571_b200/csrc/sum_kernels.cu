@@ -24,7 +24,8 @@
 // right after its four terms are added, with a cp.async.bulk L2 prefetch one
 // batch further ahead.  When every lane's batch falls in one slot (narrow
 // exponent ranges) the batch is summed in registers and the slot gets one
-// read-modify-write.  Inf/NaN are added blindly and cancelled by a per-batch
+// read-modify-write; when each lane's batch also has one sign (U[0,1)), the
+// magnitudes are summed without the sign complement (8.5 instructions/term).  Inf/NaN are added blindly and cancelled by a per-batch
 // fix-up.  Sustained rates sit at the 1 kW power cap, so energy per term (not
 // DRAM) bounds the general path.
 //
@@ -114,6 +115,11 @@
                          // vectors (one compare per vector) instead of a 64-bit index: fewer
                          // instructions, but config 5 measured 3.5% slower with it (code layout of
                          // the I-cache-sensitive segmented body; r01_variants_guard.log)
+#endif
+#ifndef EXSUM_UNIFORM_SIGNED
+#define EXSUM_UNIFORM_SIGNED 1  // one-slot batches (slot >= 1) whose lanes each hold one sign: sum
+                                // the magnitudes (no sign complement, no denormal handling; 8
+                                // instructions per term instead of ~16), negate once per lane
 #endif
 #ifndef EXSUM_PF_ALIGNED
 #define EXSUM_PF_ALIGNED 1  // L2 prefetch of the (32-byte aligned) x stream without the 16-byte
@@ -900,12 +906,48 @@ __device__ __forceinline__ void batch_uniform(const Lane &a, Batch<V, kOp> &b, c
   slot_add96(a, k, r0, r1, r2);
 }
 
+// Magnitude fast path: every lane's batch lies in slot k >= 1 (no zeros or
+// denormals: e >= 32) and holds terms of one sign (neg: 0 or ~0u per lane).
+// The significands are summed unsigned in registers (|sum| < 2^89), negated
+// once if the lane's terms are negative, then one read-modify-write.
+template <int V, int kOp>
+__device__ __forceinline__ void batch_uniform_mag(const Lane &a, Batch<V, kOp> &b,
+                                                  const double *X4, const double *Y4,
+                                                  long long nv, int lane, uint32_t k,
+                                                  uint32_t neg) {
+  uint32_t r0 = 0, r1 = 0, r2 = 0;
+#pragma unroll
+  for (int u = 0; u < V; ++u) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t lo = b.w[u][2 * q], hi = b.w[u][2 * q + 1];
+      uint32_t t, mh, u0, u1, u2;
+      asm("shr.u32 %0, %1, 20;" : "=r"(t) : "r"(hi));  // sign | e; the funnel shifts take it mod 32
+      asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mh) : "r"(hi), "r"(0x100000u));
+      asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(0u), "r"(lo), "r"(t));
+      asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lo), "r"(mh), "r"(t));
+      asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mh), "r"(0u), "r"(t));
+      asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+          : "+r"(r0), "+r"(r1), "+r"(r2)
+          : "r"(u0), "r"(u1), "r"(u2));
+    }
+    load_vec<V, kOp>(b, u, X4, Y4, nv + u * 32 + lane);
+  }
+  // (r ^ neg) - neg: the two's complement for a negative lane
+  asm("{\n\t.reg .u32 c;\n\tsub.u32 c, 0, %3;\n\txor.b32 %0, %0, %3;\n\txor.b32 %1, %1, %3;\n\t"
+      "xor.b32 %2, %2, %3;\n\tadd.cc.u32 %0, %0, c;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.u32 %2, %2, 0;\n\t}"
+      : "+r"(r0), "+r"(r1), "+r"(r2)
+      : "r"(neg));
+  slot_add96(a, k, r0, r1, r2);
+}
+
 // One-slot test for a batch: the slot of a term is its top six exponent bits
 // (hi bits 25..30; e = 0 maps to slot 0 like e' = 1).  All terms share a slot
 // iff the AND and the OR of their high words agree on those bits; slot 63 may
 // hold Inf/NaN and never counts as uniform.  Returns the slot bits or ~0u.
+// *sign: 0 if the lane's terms are all positive, ~0u if all negative, 1 if mixed.
 template <int V, int kOp>
-__device__ __forceinline__ uint32_t uniform_slot(const Batch<V, kOp> &b) {
+__device__ __forceinline__ uint32_t uniform_slot(const Batch<V, kOp> &b, uint32_t *sign = nullptr) {
   uint32_t hor = 0u, hand = 0xFFFFFFFFu;
 #pragma unroll
   for (int u = 0; u < V; ++u)
@@ -914,6 +956,7 @@ __device__ __forceinline__ uint32_t uniform_slot(const Batch<V, kOp> &b) {
       hor |= b.w[u][2 * q + 1];
       hand &= b.w[u][2 * q + 1];
     }
+  if (sign) *sign = ((hor ^ hand) >> 31) ? 1u : static_cast<uint32_t>(static_cast<int32_t>(hor) >> 31);
   const uint32_t kbits = hor & 0x7E000000u;
   return (kbits == (hand & 0x7E000000u) && kbits != 0x7E000000u) ? (kbits >> 25) : ~0u;
 }
@@ -983,20 +1026,26 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
     products_in_place<V, kOp>(b);
     uint32_t emax = 0;
     const bool steady = nv + kStep <= nvec;  // next batch complete: unguarded refills
-    uint32_t k = ~0u;
+    uint32_t k = ~0u, sgn = 1u;
     if constexpr (kUniform) {
       if (steady) {
         if (backoff > 0) {
           --backoff;
         } else {
-          k = uniform_slot<V, kOp>(b);
+          k = uniform_slot<V, kOp>(b, &sgn);
           if (!__all_sync(0xffffffffu, k != ~0u)) {
             k = ~0u;
             backoff = kUniformBackoff;  // wide data rarely turns uniform
           }
         }
       }
-      if (k != ~0u) batch_uniform<V, kOp>(a, b, X4, Y4, nv, lane, k);
+      if (k != ~0u) {
+        if (EXSUM_UNIFORM_SIGNED && __all_sync(0xffffffffu, sgn != 1u && k >= 1u)) {
+          batch_uniform_mag<V, kOp>(a, b, X4, Y4, nv, lane, k, sgn);
+        } else {
+          batch_uniform<V, kOp>(a, b, X4, Y4, nv, lane, k);
+        }
+      }
     }
     if (k == ~0u) {
       if (kSplit && steady) {

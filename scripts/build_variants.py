@@ -48,6 +48,7 @@ VARIANTS = {
     "fixl1": ("EXSUM_FIX_L1=1",),
     "pfold": ("EXSUM_PF_ALIGNED=0",),
     "guard32": ("EXSUM_GUARD32=1",),
+    "nomag": ("EXSUM_UNIFORM_SIGNED=0",),
     "nofixup": ("EXSUM_NO_FIXUP=1",),
 }
 names = sys.argv[1:] or list(VARIANTS)
