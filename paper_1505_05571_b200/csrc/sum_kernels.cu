@@ -25,9 +25,10 @@
 // batch further ahead.  When every lane's batch falls in one slot (narrow
 // exponent ranges) the batch is summed in registers and the slot gets one
 // read-modify-write; when each lane's batch also has one sign (U[0,1)), the
-// magnitudes are summed without the sign complement (8.5 instructions/term).  Inf/NaN are added blindly and cancelled by a per-batch
-// fix-up.  Sustained rates sit at the 1 kW power cap, so energy per term (not
-// DRAM) bounds the general path.
+// magnitudes are summed without the sign complement (8.5 instructions/term).
+// Inf/NaN are added blindly and cancelled by a per-batch fix-up.  Sustained
+// rates sit at the 1 kW power cap, so energy per term (not DRAM) bounds the
+// general path.
 //
 // Term sources (kOp): x[i]; fl(x[i]^2) for sqnorm; fl(a[i] b[i]) for dot, with
 // the reference's x86 NaN rules applied in the fix-up.
