@@ -70,9 +70,6 @@
 #ifndef EXSUM_SEG_VEC
 #define EXSUM_SEG_VEC 8  // segmented kernel: vectors per lane per batch
 #endif
-#ifndef EXSUM_SEG_SPLIT
-#define EXSUM_SEG_SPLIT 0  // segmented kernel: separate unguarded steady-state body
-#endif
 #ifndef EXSUM_PREFETCH_BATCHES
 #define EXSUM_PREFETCH_BATCHES 1  // L2 bulk-prefetch distance, in batches
 #endif
@@ -85,21 +82,6 @@
 #ifndef EXSUM_TIMELINE
 #define EXSUM_TIMELINE 0  // diagnostics build: per-warp %globaltimer stamps (scripts/timeline.py)
 #endif
-#ifndef EXSUM_SEG_AHEAD
-#define EXSUM_SEG_AHEAD 0  // segmented kernel: claim the next segment during the current one
-                           // (1: a step per batch, 2: after the first loads; both measured
-                           // slower, profiles/r01_variants_seg_ahead.log)
-#endif
-#ifndef EXSUM_SEG_CLAIM
-#define EXSUM_SEG_CLAIM 0  // segmented kernel (EXSUM_SEG_AHEAD 0): 1 = the next segment's claim
-                           // atomic is issued when the current segment starts and its two
-                           // dependent reads are spread over the epilogue; 0 = all three round
-                           // trips after the loop (0.3% faster: r01_variants_seg_claim.log)
-#endif
-#ifndef EXSUM_SEG_FUSED_CLEAR
-#define EXSUM_SEG_FUSED_CLEAR 0  // segmented kernel: warp_chunks zeroes the rows it reads instead
-                                 // of a separate clear (1.5% slower: r01_variants_seg_claim.log)
-#endif
 #ifndef EXSUM_FIX_L1
 #define EXSUM_FIX_L1 2  // scanning Inf/NaN fix-up re-reads: 0 ld.global.cg of each high word (L2
                         // round trips), 1 the same L1-allocating (the batch's lines are often still
@@ -107,15 +89,6 @@
                         // 32-byte vectors, L1-allocating (8 wavefronts per 4 terms instead of per
                         // term).  Config 5: 2.255 / 2.196 / 2.176 ms; 2-4 neutral
                         // (r01_variants_fixup.log)
-#endif
-#ifndef EXSUM_NO_FIXUP
-#define EXSUM_NO_FIXUP 0  // timing probe only (wrong results on data with Inf/NaN): skip the fix-up
-#endif
-#ifndef EXSUM_GUARD32
-#define EXSUM_GUARD32 0  // guarded refills test a per-batch 32-bit count of the lane's remaining
-                         // vectors (one compare per vector) instead of a 64-bit index: fewer
-                         // instructions, but config 5 measured 3.5% slower with it (code layout of
-                         // the I-cache-sensitive segmented body; r01_variants_guard.log)
 #endif
 #ifndef EXSUM_UNIFORM_SIGNED
 #define EXSUM_UNIFORM_SIGNED 1  // one-slot batches (slot >= 1) whose lanes each hold one sign: sum
@@ -130,18 +103,9 @@
 #define EXSUM_LDG_KIND 2  // 256-bit loads: 0 nc+L1::no_allocate, 1 nc, 2 nc+L1::evict_first (3-4%
                           // faster on configs 3-5 than 0: r01_variants_ldg.log), 3 plain
 #endif
-#ifndef EXSUM_DIGITS
-#define EXSUM_DIGITS 0  // lane accumulators as 16-bit digit rows updated by shared reductions
-#endif
-#ifndef EXSUM_RMW_ORDER
-#define EXSUM_RMW_ORDER 0  // add_term: 0 ld L,H st L,H; 1 ld L,H st H,L; 2 ld H,L st H,L
-#endif
 #ifndef EXSUM_SUM_SCAN
 #define EXSUM_SUM_SCAN 1  // single-sum kernel: scanning Inf/NaN fix-up (0: per-term loop; 1.43x
                           // faster on 1e-4 Inf/NaN data, neutral otherwise: r01_variants_sumscan.log)
-#endif
-#ifndef EXSUM_SCALARS_LATE
-#define EXSUM_SCALARS_LATE 1  // scalar head/tail terms after the first batch's loads
 #endif
 #ifndef EXSUM_UNIFORM_BACKOFF
 #define EXSUM_UNIFORM_BACKOFF 7  // batches to skip the one-slot test after a miss
@@ -185,15 +149,7 @@ constexpr int kSlots = EXSUM_SLOTS;  // slots 0..63 take terms (e' >> 5), the re
 static_assert(kSlots == 65 || kSlots == 66, "slot count");
 constexpr int kLPlane = kSlots * 32 * 4;
 constexpr int kHPlane = kSlots * 32 * 8;
-#if EXSUM_DIGITS
-// Digit representation: 133 rows of lane-interleaved int32 digits, digit i of
-// weight 2^(16 i - 1075); a term touches 5 consecutive digits (red.shared.add,
-// no read-modify-write chain); 2^15 adds of headroom per digit.
-constexpr int kDigitRows = 133;  // 0..131 take term pieces, 132 only carries
-constexpr int kWarpSmem = kDigitRows * 32 * 4;          // 17,024 B
-#else
 constexpr int kWarpSmem = kLPlane + kHPlane;            // 25,344 B
-#endif
 constexpr int kScratch = kWarps * kChunks * 8;          // per-warp chunk rows
 constexpr int kSmem = kWarps * kWarpSmem + kScratch;    // 207,040 B (8 warps, 66 slots)
 constexpr int kPrefetchBatches = EXSUM_PREFETCH_BATCHES;
@@ -253,58 +209,6 @@ __device__ __forceinline__ void zero_warp(unsigned char *warp_smem, int lane) {
   for (int i = lane; i < n16; i += 32) p[i] = make_uint4(0, 0, 0, 0);
 }
 
-#if EXSUM_DIGITS
-// Add the term (lo, hi) with exponent field e to the lane's digits: the
-// 53-bit significand shifted by b = e' & 15 (<= 68 bits) as five 16-bit
-// pieces into digits d .. d+4, d = e' >> 4, each negated for a negative term
-// (IMAD on the FMA pipe).  Fire-and-forget shared reductions: no load, no
-// dependency between terms.
-__device__ __forceinline__ void add_term_digits(const Lane &a, uint32_t lo, uint32_t hi,
-                                                uint32_t e) {
-  uint32_t sm, ep, d, mhi, mh, b, dg, u0, u1, u2, addr;
-  asm("shr.s32 %0, %1, 31;" : "=r"(sm) : "r"(hi));
-  asm("or.b32 %0, %0, 1;" : "+r"(sm));                                     // +1 / -1
-  asm("max.u32 %0, %1, 1;" : "=r"(ep) : "r"(e));
-  asm("mad.lo.u32 %0, %1, -1, %2;" : "=r"(d) : "r"(e), "r"(ep));          // 1 iff e == 0
-  asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x100000u));
-  asm("mad.lo.u32 %0, %1, -1048576, %2;" : "=r"(mh) : "r"(d), "r"(mhi));
-  asm("and.b32 %0, %1, 15;" : "=r"(b) : "r"(ep));
-  asm("shr.u32 %0, %1, 4;" : "=r"(dg) : "r"(ep));
-  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(0u), "r"(lo), "r"(b));
-  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lo), "r"(mh), "r"(b));
-  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mh), "r"(0u), "r"(b));
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(dg), "r"(a.c128), "r"(a.sl));
-  const uint32_t q0 = (u0 & 0xFFFFu) * sm, q1 = (u0 >> 16) * sm, q2 = (u1 & 0xFFFFu) * sm,
-                 q3 = (u1 >> 16) * sm, q4 = u2 * sm;
-  asm volatile(
-      "red.shared.add.u32 [%0], %1;\n\t"
-      "red.shared.add.u32 [%0+128], %2;\n\t"
-      "red.shared.add.u32 [%0+256], %3;\n\t"
-      "red.shared.add.u32 [%0+384], %4;\n\t"
-      "red.shared.add.u32 [%0+512], %5;" ::"r"(addr),
-      "r"(q0), "r"(q1), "r"(q2), "r"(q3), "r"(q4)
-      : "memory");
-}
-
-// A signed 96-bit value (v2:v1:v0) of 32-bit slot k (weight 2^(32k - 1075))
-// into digits 2k .. 2k+5: five unsigned 16-bit pieces and a signed top piece.
-__device__ __forceinline__ void slot_add96_digits(const Lane &a, uint32_t k, uint32_t v0,
-                                                  uint32_t v1, uint32_t v2) {
-  uint32_t addr;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(addr) : "r"(k), "r"(a.c128 * 2u), "r"(a.sl));
-  const uint32_t top = static_cast<uint32_t>(static_cast<int32_t>(v2) >> 16);
-  asm volatile(
-      "red.shared.add.u32 [%0], %1;\n\t"
-      "red.shared.add.u32 [%0+128], %2;\n\t"
-      "red.shared.add.u32 [%0+256], %3;\n\t"
-      "red.shared.add.u32 [%0+384], %4;\n\t"
-      "red.shared.add.u32 [%0+512], %5;\n\t"
-      "red.shared.add.u32 [%0+640], %6;" ::"r"(addr),
-      "r"(v0 & 0xFFFFu), "r"(v0 >> 16), "r"(v1 & 0xFFFFu), "r"(v1 >> 16), "r"(v2 & 0xFFFFu),
-      "r"(top)
-      : "memory");
-}
-#endif
 
 // The term as three 32-bit words of its complemented, shifted significand
 // (u2:u1:u0 = s ? ~(m << sh) : m << sh; a negative term's +1 is the carry-in
@@ -340,10 +244,6 @@ __device__ __forceinline__ void decode96(uint32_t lo, uint32_t hi, uint32_t e, u
 // Read-modify-write of slot k with a 96-bit two's-complement value (no carry-in).
 __device__ __forceinline__ void slot_add96(const Lane &a, uint32_t k, uint32_t v0, uint32_t v1,
                                            uint32_t v2) {
-#if EXSUM_DIGITS
-  slot_add96_digits(a, k, v0, v1, v2);
-  return;
-#endif
   uint32_t la, ha;
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(k), "r"(a.c128), "r"(a.sl));
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));
@@ -364,25 +264,13 @@ __device__ __forceinline__ void slot_add96(const Lane &a, uint32_t k, uint32_t v
 // Add one term (exponent field e != 2047, or 2047 for the blind add of an
 // Inf/NaN that the batch fix-up cancels) to the lane's slots.
 __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
-#if EXSUM_DIGITS
-  add_term_digits(a, lo, hi, e);
-  return;
-#endif
   uint32_t s, ep, k, la, ha, u0, u1, u2;
   decode96(lo, hi, e, s, u0, u1, u2, ep);
   asm("shr.u32 %0, %1, 5;" : "=r"(k) : "r"(ep));
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(k), "r"(a.c128), "r"(a.sl));
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));
-#if EXSUM_RMW_ORDER == 0
 #define EXSUM_RMW_LD "ld.shared.u32 l, [%0];\n\tld.shared.v2.u32 {h0, h1}, [%1];\n\t"
 #define EXSUM_RMW_ST "st.shared.u32 [%0], l;\n\tst.shared.v2.u32 [%1], {h0, h1};\n\t}"
-#elif EXSUM_RMW_ORDER == 1
-#define EXSUM_RMW_LD "ld.shared.u32 l, [%0];\n\tld.shared.v2.u32 {h0, h1}, [%1];\n\t"
-#define EXSUM_RMW_ST "st.shared.v2.u32 [%1], {h0, h1};\n\tst.shared.u32 [%0], l;\n\t}"
-#else
-#define EXSUM_RMW_LD "ld.shared.v2.u32 {h0, h1}, [%1];\n\tld.shared.u32 l, [%0];\n\t"
-#define EXSUM_RMW_ST "st.shared.v2.u32 [%1], {h0, h1};\n\tst.shared.u32 [%0], l;\n\t}"
-#endif
   asm volatile(
       "{\n\t.reg .u32 l, h0, h1, cf;\n\t"
       EXSUM_RMW_LD
@@ -401,19 +289,6 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
 // lane sum, 2^1024 x 2^31 terms).
 // Safe whenever every slot has absorbed <= 2047 terms (|H_k| < 2^63 - 2^52).
 __device__ __forceinline__ void normalize(const Lane &a) {
-#if EXSUM_DIGITS
-  // digits below the top in [0, 2^16), the carry-only top digit keeps the rest
-  int32_t *D = reinterpret_cast<int32_t *>(a.L);
-  long long cd = 0;
-#pragma unroll 7
-  for (int i = 0; i < kDigitRows - 1; ++i) {
-    const long long v = static_cast<long long>(D[32 * i]) + cd;
-    D[32 * i] = static_cast<int32_t>(v & 0xFFFF);
-    cd = v >> 16;
-  }
-  D[32 * (kDigitRows - 1)] += static_cast<int32_t>(cd);
-  return;
-#endif
   long long c = 0;
 #pragma unroll 6
   for (int k = 0; k < kSlots - 1; ++k) {
@@ -437,78 +312,11 @@ __device__ __forceinline__ void normalize(const Lane &a) {
 // Lane j sums the rows of slots j, j+32, j+64 with bank-skewed 128-bit reads
 // (8 lanes per wavefront hit 8 distinct 16-byte bank groups), then the chunk
 // values are assembled with shuffles: 24 LDS.128 per lane per round.
-#if EXSUM_DIGITS
-// Digit rows summed over the 32 lanes (lane j: rows j, j+32, ..., bank-skewed
-// 128-bit reads), then chunk c = R[2c] + 2^16 R[2c+1] (c < 66), chunk 66 =
-// R[132]; |R| < 2^36 so |chunk| < 2^53.
-__device__ __forceinline__ void warp_chunks_digits(unsigned char *warp_smem, int lane,
-                                                   long long *row) {
-  __syncwarp();
-  const int32_t *Dp = reinterpret_cast<const int32_t *>(warp_smem);
-  long long R[5];
-#pragma unroll
-  for (int r = 0; r < 5; ++r) {
-    const int i = 32 * r + lane;
-    long long acc = 0;
-    if (i < kDigitRows) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int4 v = *reinterpret_cast<const int4 *>(Dp + i * 32 + 4 * ((q + lane) & 7));
-        acc += static_cast<long long>(v.x) + v.y + static_cast<long long>(v.z) + v.w;
-      }
-    }
-    R[r] = acc;
-  }
-  const int src = (2 * lane) & 31;
-  long long v[3];
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {  // chunks 32r + lane
-    const long long e0 = __shfl_sync(0xffffffffu, R[2 * r], src);
-    const long long e1 = __shfl_sync(0xffffffffu, R[2 * r], src + 1);
-    const long long o0 = r < 2 ? __shfl_sync(0xffffffffu, R[2 * r + 1], src) : 0ll;
-    const long long o1 = r < 2 ? __shfl_sync(0xffffffffu, R[2 * r + 1], src + 1) : 0ll;
-    const long long lo = lane < 16 ? e0 : o0, hi = lane < 16 ? e1 : o1;
-    v[r] = lo + hi * 65536ll;  // chunk 66: digit 132 alone (row 133 reads as 0)
-  }
-  // Two carry passes bring every chunk below the top into [0, 2^32 + 2) (from
-  // |c| < 2^53), the scale the CTA / grid / multi-launch chunk sums assume.
-#pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
-    long long c[3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const bool carries = 32 * r + lane < kChunks - 1;
-      c[r] = carries ? v[r] >> 32 : 0;
-      if (carries) v[r] &= 0xFFFFFFFFll;
-    }
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const long long up = __shfl_up_sync(0xffffffffu, c[r], 1);
-      const long long wrap = r ? __shfl_sync(0xffffffffu, c[r > 0 ? r - 1 : 0], 31) : 0ll;
-      v[r] += lane ? up : wrap;
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < 3; ++r)
-    if (32 * r + lane < kChunks) row[32 * r + lane] = v[r];
-}
-#endif
 
-// kZero: store zeros over every row word after reading it (the accumulator is
-// left cleared for the next segment: no separate zero_warp pass).
-template <bool kZero = false>
 __device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, int lane, long long *row) {
-#if EXSUM_DIGITS
-  warp_chunks_digits(warp_smem, lane, row);
-  if (kZero) {
-    __syncwarp();
-    zero_warp(warp_smem, lane);
-  }
-  return;
-#endif
   __syncwarp();
-  uint32_t *Lp = reinterpret_cast<uint32_t *>(warp_smem);
-  uint32_t *Hw = reinterpret_cast<uint32_t *>(warp_smem + kLPlane);
+  const uint32_t *Lp = reinterpret_cast<const uint32_t *>(warp_smem);
+  const uint32_t *Hw = reinterpret_cast<const uint32_t *>(warp_smem + kLPlane);
   long long sl[3], shl[3], shh[3];
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
@@ -518,16 +326,12 @@ __device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, int lane, 
       long long a = 0, bl = 0, bh = 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        uint4 *p = reinterpret_cast<uint4 *>(Lp + k * 32 + 4 * ((i + lane) & 7));
-        const uint4 v = *p;
-        if (kZero) *p = make_uint4(0, 0, 0, 0);
+        const uint4 v = *reinterpret_cast<const uint4 *>(Lp + k * 32 + 4 * ((i + lane) & 7));
         a += static_cast<long long>(v.x) + v.y + static_cast<long long>(v.z) + v.w;
       }
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        uint4 *p = reinterpret_cast<uint4 *>(Hw + k * 64 + 4 * ((i + lane) & 15));
-        const uint4 v = *p;
-        if (kZero) *p = make_uint4(0, 0, 0, 0);
+        const uint4 v = *reinterpret_cast<const uint4 *>(Hw + k * 64 + 4 * ((i + lane) & 15));
         bl += static_cast<long long>(v.x) + v.z;
         bh += static_cast<long long>(static_cast<int32_t>(v.y)) + static_cast<int32_t>(v.w);
       }
@@ -856,11 +660,6 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
                                                   const double *X4, const double *Y4,
                                                   long long nv, long long nvec, int lane) {
   uint32_t emax = 0;
-  int r32 = 0;  // EXSUM_GUARD32: refill vector u exists iff u * 32 < r32
-  if constexpr (kGuard && EXSUM_GUARD32) {
-    const long long rem = nvec - nv - lane;
-    r32 = rem <= 0 ? 0 : rem > 0x7FFFFFFF ? 0x7FFFFFFF : static_cast<int>(rem);
-  }
 #pragma unroll
   for (int u = 0; u < V; ++u) {
     uint32_t lo[4], hi[4], e[4];
@@ -874,7 +673,7 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
 #pragma unroll
     for (int q = 0; q < 4; ++q) add_term(a, lo[q], hi[q], e[q]);
     const long long vec = nv + u * 32 + lane;
-    if (!kGuard || (EXSUM_GUARD32 ? u * 32 < r32 : vec < nvec)) {
+    if (!kGuard || vec < nvec) {
       load_vec<V, kOp>(b, u, X4, Y4, vec);
     } else {
       zero_vec<V, kOp>(b, u);
@@ -971,25 +770,13 @@ __device__ __forceinline__ uint32_t uniform_slot(const Batch<V, kOp> &b, uint32_
 //   kSplit:   separate unguarded steady-state body (larger code, fewer instrs)
 //   kScan:    scanning Inf/NaN fix-up (for data with frequent specials)
 //   kOp:      term source (kSum, kSqnorm, kDot, kDotScalarB); y used by dots
-// hook() runs once per batch, after the batch's refills are issued (the
-// segmented kernel advances its claim of the next segment there).
-struct NoHook {
-  __device__ __forceinline__ void start() const {}
-  __device__ __forceinline__ void operator()() const {}
-};
-
-template <int V, bool kUniform, bool kSplit, bool kScan, int kOp = kSum, class Hook = NoHook>
+template <int V, bool kUniform, bool kSplit, bool kScan, int kOp = kSum>
 __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
                                                 const double *__restrict__ y,
                                                 unsigned long long begin, unsigned long long end,
                                                 unsigned long long index_base, const Lane &a,
-                                                Specials &sp, int &norm_count, int lane,
-                                                Hook hook = Hook{}) {
-#if EXSUM_DIGITS
-  constexpr int kNormEvery = 32000 / (4 * V);  // digits: 2^15 adds of headroom
-#else
+                                                Specials &sp, int &norm_count, int lane) {
   constexpr int kNormEvery = 2016 / (4 * V);  // batches between renormalisations
-#endif
   static_assert(kNormEvery >= 1, "batch too large for the carry budget");
   if (begin >= end) return;
   // Scalar head up to 32-byte alignment of &x[pos], scalar tail after the
@@ -1009,8 +796,10 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
     if (lane < static_cast<int>(end - tail_t))
       add_elem_checked<kOp>(a, sp, x, y, tail_t + lane, index_base + tail_t + lane);
   };
-  if (nvec <= 0 || !EXSUM_SCALARS_LATE) scalars();
-  if (nvec <= 0) return;
+  if (nvec <= 0) {
+    scalars();
+    return;
+  }
   constexpr long long kStep = V * 32;
   const unsigned long long ib = index_base + vbeg_t;
   if (lane == 0) {
@@ -1018,8 +807,7 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
   }
   Batch<V, kOp> b;
   load_batch<V, kOp>(b, X4, Y4, 0, nvec, lane);
-  if (EXSUM_SCALARS_LATE) scalars();
-  hook.start();
+  scalars();
   int backoff = 0;
   for (long long v = 0; v < nvec; v += kStep) {
     const long long nv = v + kStep;
@@ -1055,8 +843,7 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
         emax = batch_rolling<V, true, kOp>(a, b, X4, Y4, nv, nvec, lane);
       }
     }
-    hook();
-    if (!EXSUM_NO_FIXUP && __builtin_expect(emax == 0x7FFu, 0))
+    if (__builtin_expect(emax == 0x7FFu, 0))
       fixup_specials<V, kScan, kOp>(a, sp, X4, Y4, v, nvec, lane, ib);
     if (++norm_count >= kNormEvery) {
       normalize(a);
@@ -1678,20 +1465,6 @@ struct ClaimAhead {
   }
 };
 
-// EXSUM_SEG_AHEAD 1: one claim step per batch; 2: the claim's round trips
-// right after the first batch's loads are issued (their latency overlaps it),
-// the L2 prefetch after the loop.
-struct ClaimHook {
-  ClaimAhead *ca;
-  int lane;
-  __device__ __forceinline__ void start() const {
-    if (EXSUM_SEG_AHEAD == 2 && lane == 0)
-      while (ca->stage < 3) ca->step();
-  }
-  __device__ __forceinline__ void operator()() const {
-    if (EXSUM_SEG_AHEAD == 1 && lane == 0) ca->step();
-  }
-};
 
 __global__ void __launch_bounds__(kThreads, 1)
 exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *__restrict__ offs,
@@ -1707,7 +1480,6 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
   ClaimAhead ca{&ws->seg_next, order, offs, x, nseg, 0u, 0u, 0ull, 0ull, 0};
   if (lane == 0)
     while (ca.stage < 3) ca.step();  // the first claim
-  if (EXSUM_SEG_FUSED_CLEAR) zero_warp(wsm, lane);  // later segments: cleared by warp_chunks
 #if EXSUM_TIMELINE
   unsigned long long ph[7] = {0, 0, 0, 0, 0, 0, 0}, tq = gtimer(), tn;
 #define EXSUM_SEG_PHASE(i) (tn = gtimer(), ph[i] += tn - tq, tq = tn)
@@ -1721,10 +1493,7 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
     const unsigned long long b = __shfl_sync(0xffffffffu, ca.b, 0),
                              e = __shfl_sync(0xffffffffu, ca.e, 0);
     ca.stage = 0;
-#if !EXSUM_SEG_AHEAD && EXSUM_SEG_CLAIM
-    if (lane == 0) ca.step();  // the next claim's atomic; its result is read after the loop
-#endif
-    if (!EXSUM_SEG_FUSED_CLEAR) zero_warp(wsm, lane);
+    zero_warp(wsm, lane);
     __syncwarp();
     int norm_count = 0;
     EXSUM_SEG_PHASE(1);
@@ -1734,28 +1503,13 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
 #endif
     Specials sp{~0ull, ~0ull, ~0ull};
     // indices local to the segment: position - b
-#if EXSUM_SEG_AHEAD
-    // claim the next segment while this one streams
-    warp_accumulate<EXSUM_SEG_VEC, false, EXSUM_SEG_SPLIT != 0, true>(
-        x, x, b, e, 0ull - b, a, sp, norm_count, lane, ClaimHook{&ca, lane});
-    if (lane == 0)
-      while (ca.stage < 4) ca.step();  // short segments: finish the claim here
-#else
-    warp_accumulate<EXSUM_SEG_VEC, false, EXSUM_SEG_SPLIT != 0, true>(x, x, b, e, 0ull - b, a,
+    warp_accumulate<EXSUM_SEG_VEC, false, false, true>(x, x, b, e, 0ull - b, a,
                                                                       sp, norm_count, lane);
     EXSUM_SEG_PHASE(2);
-#if EXSUM_SEG_CLAIM
-    if (lane == 0) ca.step();  // order[] read (the atomic returned during the loop)
-#else
     if (lane == 0)
       while (ca.stage < 3) ca.step();
-#endif
     EXSUM_SEG_PHASE(0);
-#endif
-    warp_chunks<EXSUM_SEG_FUSED_CLEAR != 0>(wsm, lane, row);
-#if !EXSUM_SEG_AHEAD && EXSUM_SEG_CLAIM
-    if (lane == 0) ca.step();  // offsets read, overlapping the emit
-#endif
+    warp_chunks(wsm, lane, row);
     const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                              N = warp_min_u64(sp.N);
     __syncwarp();
@@ -1763,9 +1517,6 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
     const unsigned long long payload =
         N != ~0ull ? __ldg(reinterpret_cast<const unsigned long long *>(x) + b + N) : 0ull;
     warp_emit(row, P, M, N, payload, out + s, partials ? partials + s : nullptr, lane);
-#if !EXSUM_SEG_AHEAD && EXSUM_SEG_CLAIM
-    if (lane == 0) ca.step();  // L2 prefetch of the next segment's head
-#endif
     __syncwarp();
     EXSUM_SEG_PHASE(4);
   }

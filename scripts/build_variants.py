@@ -24,14 +24,7 @@ VARIANTS = {
     "w9v8": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9"),
     "w9v7": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9", "EXSUM_VEC_PER_LANE=7"),
     "w9v6": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9", "EXSUM_VEC_PER_LANE=6"),
-    "segsplit": ("EXSUM_SEG_SPLIT=1",),
-    "noahead": ("EXSUM_SEG_AHEAD=0",),
-    "noahead_early": ("EXSUM_SEG_AHEAD=0", "EXSUM_SCALARS_LATE=0"),
-    "early": ("EXSUM_SCALARS_LATE=0",),
     "sumloop": ("EXSUM_SUM_SCAN=0",),
-    "rmw1": ("EXSUM_RMW_ORDER=1",),
-    "rmw2": ("EXSUM_RMW_ORDER=2",),
-    "digits": ("EXSUM_DIGITS=1",),
     "ldg1": ("EXSUM_LDG_KIND=1",),
     "ldg0": ("EXSUM_LDG_KIND=0",),
     "ldg3": ("EXSUM_LDG_KIND=3",),
@@ -39,17 +32,10 @@ VARIANTS = {
     "pf0": ("EXSUM_PREFETCH_BATCHES=0",),
     "pf2": ("EXSUM_PREFETCH_BATCHES=2",),
     "v6": ("EXSUM_VEC_PER_LANE=6",),
-    "ahead1": ("EXSUM_SEG_AHEAD=1",),
-    "ahead2": ("EXSUM_SEG_AHEAD=2",),
-    "segboth": ("EXSUM_SEG_CLAIM=1", "EXSUM_SEG_FUSED_CLEAR=1"),
-    "claimearly": ("EXSUM_SEG_CLAIM=1",),
-    "fusedclear": ("EXSUM_SEG_FUSED_CLEAR=1",),
     "fixcg": ("EXSUM_FIX_L1=0",),
     "fixl1": ("EXSUM_FIX_L1=1",),
     "pfold": ("EXSUM_PF_ALIGNED=0",),
-    "guard32": ("EXSUM_GUARD32=1",),
     "nomag": ("EXSUM_UNIFORM_SIGNED=0",),
-    "nofixup": ("EXSUM_NO_FIXUP=1",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 verbose = "-v" in names
