@@ -1412,59 +1412,26 @@ exsum_segment_scatter_kernel(const unsigned long long *__restrict__ offs, unsign
   if (s < nseg) order[cnt[key] + r] = static_cast<unsigned>(s);
 }
 
-// Lane 0's claim of the segment after the current one, advanced one step per
-// batch of the current segment so that each dependent round trip (claim
-// atomic -> order[] -> offsets -> L2 prefetch of the head and tail) completes
-// behind a batch of streaming instead of stalling the warp between segments.
-struct ClaimAhead {
-  unsigned int *counter;
-  const unsigned int *order;
-  const unsigned long long *offs;
-  const double *x;
-  unsigned long long nseg;
-  unsigned int c, s;
+// Lane 0's claim of the next segment: the claim atomic, the segment's entry in
+// the claim order, then its offsets (three dependent round trips, straight-line).
+struct SegmentClaim {
+  unsigned int s;
   unsigned long long b, e;
-  int stage;  // 0: none, 1: claimed (c), 2: resolved (s), 3: bounds (b, e), 4: prefetched
 
-  __device__ __forceinline__ void step() {
-    switch (stage) {
-      case 0:
-        // inline PTX: a plain atomicAdd in a lane-0 branch becomes a
-        // warp-aggregated atomic whose result is waited for at once
-        asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(c) : "l"(counter) : "memory");
-        break;
-      case 1:
-        s = c < nseg ? (order ? __ldcg(order + c) : c) : static_cast<unsigned int>(nseg);
-        break;
-      case 2:
-        if (s < nseg) {
-          b = __ldg(offs + s);
-          e = __ldg(offs + s + 1);
-          if (e < b) e = b;  // decreasing offsets (a caller error): an empty segment, +0.0
-        }
-        break;
-      case 3:
-        if (s < nseg && e > b) {
-          constexpr unsigned long long kHead = EXSUM_SEG_VEC * 32 * 4;  // one batch of terms
-          const unsigned long long he = e - b > kHead ? b + kHead : e;
-          const uintptr_t p0 = reinterpret_cast<uintptr_t>(x + b) & ~uintptr_t{15};
-          const uintptr_t p1 = reinterpret_cast<uintptr_t>(x + he);
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0),
-                       "r"(static_cast<uint32_t>((p1 - p0 + 15) & ~uintptr_t{15}))
-                       : "memory");
-          if (he < e) {  // the scalar tail (last 32 bytes)
-            const uintptr_t t0 = reinterpret_cast<uintptr_t>(x + e - 4) & ~uintptr_t{15};
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], 48;" ::"l"(t0) : "memory");
-          }
-        }
-        break;
-      default:
-        return;
+  __device__ __forceinline__ void claim(unsigned int *counter, const unsigned int *order,
+                                        const unsigned long long *offs, unsigned long long nseg) {
+    unsigned int c;
+    // inline PTX: a plain atomicAdd in a lane-0 branch becomes a warp-aggregated
+    // atomic whose result is shuffled back at once
+    asm volatile("atom.global.add.u32 %0, [%1], 1;" : "=r"(c) : "l"(counter) : "memory");
+    s = c < nseg ? (order ? __ldcg(order + c) : c) : static_cast<unsigned int>(nseg);
+    if (s < nseg) {
+      b = __ldg(offs + s);
+      e = __ldg(offs + s + 1);
+      if (e < b) e = b;  // decreasing offsets (a caller error): an empty segment, +0.0
     }
-    ++stage;
   }
 };
-
 
 __global__ void __launch_bounds__(kThreads, 1)
 exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *__restrict__ offs,
@@ -1477,9 +1444,9 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
   long long *row = rows + warp * kChunks;
   unsigned char *wsm = smem + warp * kWarpSmem;
   const Lane a = lane_view(wsm, lane);
-  ClaimAhead ca{&ws->seg_next, order, offs, x, nseg, 0u, 0u, 0ull, 0ull, 0};
+  SegmentClaim ca{0u, 0ull, 0ull};
   if (lane == 0)
-    while (ca.stage < 3) ca.step();  // the first claim
+    ca.claim(&ws->seg_next, order, offs, nseg);  // the first claim
 #if EXSUM_TIMELINE
   unsigned long long ph[7] = {0, 0, 0, 0, 0, 0, 0}, tq = gtimer(), tn;
 #define EXSUM_SEG_PHASE(i) (tn = gtimer(), ph[i] += tn - tq, tq = tn)
@@ -1492,7 +1459,6 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
     if (s >= nseg) break;
     const unsigned long long b = __shfl_sync(0xffffffffu, ca.b, 0),
                              e = __shfl_sync(0xffffffffu, ca.e, 0);
-    ca.stage = 0;
     zero_warp(wsm, lane);
     __syncwarp();
     int norm_count = 0;
@@ -1507,7 +1473,7 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
                                                                       sp, norm_count, lane);
     EXSUM_SEG_PHASE(2);
     if (lane == 0)
-      while (ca.stage < 3) ca.step();
+      ca.claim(&ws->seg_next, order, offs, nseg);
     EXSUM_SEG_PHASE(0);
     warp_chunks(wsm, lane, row);
     const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
