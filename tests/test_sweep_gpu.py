@@ -126,3 +126,24 @@ def test_lengths_around_batches(cuda, checker):
             e = rng.integers(0, 2047, n, dtype=np.uint64)
             x = _bits((b & np.uint64(0x800FFFFFFFFFFFFF)) | (e << np.uint64(52)))
             _check(x, checker, offset=int(rng.integers(0, 4)), tag=(k, d))
+
+
+def test_one_sign_fast_path(cuda, checker):
+    """One-slot batches where each lane's terms share a sign (the magnitude
+    fast path): all negative, lane-alternating signs (per 4-term vector group
+    of 32), a single flipped term (mixed lane -> signed fast path), and a
+    magnitude run in slot 1 (e' = 32..63, just above the denormal slot)."""
+    rng = np.random.default_rng(21)
+    n = 4_000_000 + 12
+    u = rng.uniform(0.5, 1.0, n)
+    _check(-u, checker, tag="all-negative")
+    lane_sign = np.where(((np.arange(n) // 4) % 32) % 2 == 0, 1.0, -1.0)
+    _check(u * lane_sign, checker, offset=0, tag="lane-alternating")
+    _check(u * lane_sign, checker, offset=2, tag="lane-alternating-misaligned")
+    y = u.copy()
+    y[BATCH * 50 + 17] *= -1.0
+    _check(y, checker, tag="one-flip")
+    slot1 = _bits((np.uint64(40) << np.uint64(52)) |
+                  rng.integers(0, 2 ** 52, n, dtype=np.uint64))  # exponent field 40: slot 1
+    _check(slot1, checker, tag="slot1")
+    _check(-slot1, checker, offset=1, tag="slot1-negative")
