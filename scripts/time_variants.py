@@ -1,7 +1,8 @@
 """Time kernel variants (lib/variants/*.so) on configs 2/3 (1e8) and 4 (1e9).
 
 Each variant runs in its own process (EXSUM_LIB selects the .so).
-Config 6 = one sum over config-5 values (frequent Inf/NaN).
+Config 6 = one sum over config-5 values (frequent Inf/NaN); config 7 = config 1's
+U[-1,1) at 1e8 terms (mixed signs in one slot).
 TV_OVERLAP=1 launches back-to-back sums with programmatic dependent launch
 (the bench's mode); TV_CONFIGS=2,3 restricts the configs; TV_SUSTAIN=S runs S seconds
 of back-to-back sums first and then times ~0.5 s (the power-capped steady state).  Prints one
@@ -45,6 +46,8 @@ for config, n, K in %s:
     x = torch.empty(n, dtype=torch.float64, device=dev)
     if config == 6:  # one sum over config-5 values (1e-4 Inf/NaN, wide exponents)
         _lib.call("exsum_cuda_gen_segmented", 1, 0, n, x.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    elif config == 7:  # config 1's distribution (U[-1,1), mixed signs, one slot) at 1e8 terms
+        _lib.call("exsum_cuda_gen", 1, 1, n, 0, n, x.data_ptr(), torch.cuda.current_stream().cuda_stream)
     else:
         _lib.call("exsum_cuda_gen", config, 1, n, 0, n, x.data_ptr(), torch.cuda.current_stream().cuda_stream)
     res = torch.empty(1, dtype=torch.float64, device=dev)
@@ -75,7 +78,7 @@ print("RESULT", json.dumps(out))
 '''
 
 cases = [(2, 100_000_000, 20), (3, 100_000_000, 20), (4, 1_000_000_000, 5), (5, 65_536, 5),
-         (6, 100_000_000, 20)]
+         (6, 100_000_000, 20), (7, 100_000_000, 20)]
 if os.environ.get("TV_CONFIGS"):
     keep = {int(c) for c in os.environ["TV_CONFIGS"].split(",")}
     cases = [c for c in cases if c[0] in keep]
