@@ -17,6 +17,7 @@ VARIANTS = {
     "backoff15": ("EXSUM_UNIFORM_BACKOFF=15",),
     "timeline": ("EXSUM_TIMELINE=1",),
     "seg4": ("EXSUM_SEG_VEC=4",),
+    "seg6": ("EXSUM_SEG_VEC=6",),
     "xorimad": ("EXSUM_XOR_LOP=0",),
     "cta132": ("EXSUM_MAX_CTAS=132",),
     "fullgrid": ("EXSUM_OVERLAP_SHORT=0",),
