@@ -147,3 +147,21 @@ def test_one_sign_fast_path(cuda, checker):
                   rng.integers(0, 2 ** 52, n, dtype=np.uint64))  # exponent field 40: slot 1
     _check(slot1, checker, tag="slot1")
     _check(-slot1, checker, offset=1, tag="slot1-negative")
+
+
+def test_segmented_beyond_order_limit(cuda, checker):
+    """More segments than the longest-first order supports (2^24): the kernel
+    claims in index order; tiny and empty segments, specials and denormals."""
+    rng = np.random.default_rng(5)
+    nseg = (1 << 24) + 5
+    lens = rng.integers(0, 4, nseg)
+    lens[::1000] = rng.integers(50, 3000, lens[::1000].size)  # some longer ones
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    total = int(offs[-1])
+    b = rng.integers(0, 2 ** 64 - 1, total, dtype=np.uint64)
+    e = rng.integers(0, 2048, total, dtype=np.uint64)  # includes e = 0 and e = 2047
+    x = _bits((b & np.uint64(0x800FFFFFFFFFFFFF)) | (e << np.uint64(52)))
+    got = ops.exact_sum_segmented(torch.from_numpy(x).cuda(),
+                                  torch.from_numpy(offs.astype(np.int64)).cuda())
+    want = checker.segmented_sum(x, offs).view(np.uint64)
+    assert np.array_equal(got.cpu().numpy().view(np.uint64), want)
