@@ -99,6 +99,24 @@
 #define EXSUM_PF_ALIGNED 1  // L2 prefetch of the (32-byte aligned) x stream without the 16-byte
                             // rounding arithmetic
 #endif
+#ifndef EXSUM_DEBUG_CHECKS
+#define EXSUM_DEBUG_CHECKS 0  // debug build: every streaming load checks its vector index against
+                              // the range end (printf + trap on a violation)
+#endif
+#if EXSUM_DEBUG_CHECKS
+#include <cstdio>
+#define EXSUM_DCHECK(c)                                                          \
+  do {                                                                           \
+    if (!(c)) {                                                                  \
+      printf("EXSUM_DCHECK failed: %s (%s:%d)\n", #c, __FILE__, __LINE__);       \
+      __trap();                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define EXSUM_DCHECK(c) \
+  do {                  \
+  } while (0)
+#endif
 #ifndef EXSUM_LDG_KIND
 #define EXSUM_LDG_KIND 2  // 256-bit loads: 0 nc+L1::no_allocate, 1 nc, 2 nc+L1::evict_first (3-4%
                           // faster on configs 3-5 than 0: r01_variants_ldg.log), 3 plain
@@ -604,6 +622,7 @@ __device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, cons
       mask &= mask - 1u;
       const long long vec = v + (i >> 2) * 32 + lane;
       const int q = i & 3;
+      EXSUM_DCHECK(vec >= 0 && vec < nvec);
       const unsigned long long bits =
           EXSUM_FIX_L1 ? __ldg(xb + 4 * vec + q) : __ldcg(xb + 4 * vec + q);
       const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
@@ -674,6 +693,7 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
     for (int q = 0; q < 4; ++q) add_term(a, lo[q], hi[q], e[q]);
     const long long vec = nv + u * 32 + lane;
     if (!kGuard || vec < nvec) {
+      EXSUM_DCHECK(vec >= 0 && vec < nvec);
       load_vec<V, kOp>(b, u, X4, Y4, vec);
     } else {
       zero_vec<V, kOp>(b, u);
@@ -687,7 +707,8 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
 template <int V, int kOp>
 __device__ __forceinline__ void batch_uniform(const Lane &a, Batch<V, kOp> &b, const double *X4,
                                               const double *Y4, long long nv, int lane,
-                                              uint32_t k) {
+                                              uint32_t k, long long nvec) {
+  (void)nvec;  // EXSUM_DCHECK only
   uint32_t r0 = 0, r1 = 0, r2 = 0;
 #pragma unroll
   for (int u = 0; u < V; ++u) {
@@ -701,6 +722,7 @@ __device__ __forceinline__ void batch_uniform(const Lane &a, Batch<V, kOp> &b, c
           : "+r"(r0), "+r"(r1), "+r"(r2)
           : "r"(sg), "r"(u0), "r"(u1), "r"(u2));
     }
+    EXSUM_DCHECK(nv + u * 32 + lane < nvec);
     load_vec<V, kOp>(b, u, X4, Y4, nv + u * 32 + lane);
   }
   slot_add96(a, k, r0, r1, r2);
@@ -714,7 +736,8 @@ template <int V, int kOp>
 __device__ __forceinline__ void batch_uniform_mag(const Lane &a, Batch<V, kOp> &b,
                                                   const double *X4, const double *Y4,
                                                   long long nv, int lane, uint32_t k,
-                                                  uint32_t neg) {
+                                                  uint32_t neg, long long nvec) {
+  (void)nvec;  // EXSUM_DCHECK only
   uint32_t r0 = 0, r1 = 0, r2 = 0;
 #pragma unroll
   for (int u = 0; u < V; ++u) {
@@ -731,6 +754,7 @@ __device__ __forceinline__ void batch_uniform_mag(const Lane &a, Batch<V, kOp> &
           : "+r"(r0), "+r"(r1), "+r"(r2)
           : "r"(u0), "r"(u1), "r"(u2));
     }
+    EXSUM_DCHECK(nv + u * 32 + lane < nvec);
     load_vec<V, kOp>(b, u, X4, Y4, nv + u * 32 + lane);
   }
   // (r ^ neg) - neg: the two's complement for a negative lane
@@ -830,9 +854,9 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
       }
       if (k != ~0u) {
         if (EXSUM_UNIFORM_SIGNED && __all_sync(0xffffffffu, sgn != 1u && k >= 1u)) {
-          batch_uniform_mag<V, kOp>(a, b, X4, Y4, nv, lane, k, sgn);
+          batch_uniform_mag<V, kOp>(a, b, X4, Y4, nv, lane, k, sgn, nvec);
         } else {
-          batch_uniform<V, kOp>(a, b, X4, Y4, nv, lane, k);
+          batch_uniform<V, kOp>(a, b, X4, Y4, nv, lane, k, nvec);
         }
       }
     }

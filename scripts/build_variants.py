@@ -37,6 +37,7 @@ VARIANTS = {
     "fixl1": ("EXSUM_FIX_L1=1",),
     "pfold": ("EXSUM_PF_ALIGNED=0",),
     "nomag": ("EXSUM_UNIFORM_SIGNED=0",),
+    "debug": ("EXSUM_DEBUG_CHECKS=1",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 verbose = "-v" in names
