@@ -99,6 +99,10 @@
 #define EXSUM_PF_ALIGNED 1  // L2 prefetch of the (32-byte aligned) x stream without the 16-byte
                             // rounding arithmetic
 #endif
+#ifndef EXSUM_PF_PRED
+#define EXSUM_PF_PRED 1  // plain sums: the per-batch L2 prefetch predicated on lane 0 instead of a
+                         // lane-0 branch
+#endif
 #ifndef EXSUM_DEBUG_CHECKS
 #define EXSUM_DEBUG_CHECKS 0  // debug build: every streaming load checks its vector index against
                               // the range end (printf + trap on a violation)
@@ -556,6 +560,24 @@ __device__ __forceinline__ void prefetch_batch(const double *X4, const double *Y
   if constexpr (kOp >= kDot) prefetch_l2<V, kOp == kDot>(Y4, v0, vend);
 }
 
+// prefetch_l2 of the aligned x stream as straight-line code: every lane
+// computes the clipped size, the one bulk prefetch is predicated on lane 0
+// (no branch, so no reconvergence point in the streaming loop).
+template <int V>
+__device__ __forceinline__ void prefetch_l2_lane0(const double *X4, long long v0, long long vend,
+                                                  int lane) {
+  long long nv = vend - v0;
+  if (nv > V * 32) nv = V * 32;
+  const uint32_t bytes = nv > 0 ? static_cast<uint32_t>(nv) * 32u : 0u;
+  const uint32_t go = (lane == 0 && bytes) ? 1u : 0u;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+      "@q cp.async.bulk.prefetch.L2.global [%0], %1;\n\t}" ::"l"(
+          reinterpret_cast<uintptr_t>(X4 + 4 * v0)),
+      "r"(bytes), "r"(go)
+      : "memory");
+}
+
 // Inf/NaN fix-up of one batch (rare): the batch's terms were added blindly;
 // re-read the lane's terms, record each Inf/NaN by index and cancel its
 // (garbage) contribution with its sign-flipped twin — exact in the modular slot
@@ -835,7 +857,11 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
   int backoff = 0;
   for (long long v = 0; v < nvec; v += kStep) {
     const long long nv = v + kStep;
-    if (lane == 0) prefetch_batch<V, kOp>(X4, Y4, v + (kPrefetchBatches + 1) * kStep, nvec);
+    if constexpr (EXSUM_PF_PRED && kOp == kSum) {
+      prefetch_l2_lane0<V>(X4, v + (kPrefetchBatches + 1) * kStep, nvec, lane);
+    } else {
+      if (lane == 0) prefetch_batch<V, kOp>(X4, Y4, v + (kPrefetchBatches + 1) * kStep, nvec);
+    }
     products_in_place<V, kOp>(b);
     uint32_t emax = 0;
     const bool steady = nv + kStep <= nvec;  // next batch complete: unguarded refills

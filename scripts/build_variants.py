@@ -38,6 +38,7 @@ VARIANTS = {
     "pfold": ("EXSUM_PF_ALIGNED=0",),
     "nomag": ("EXSUM_UNIFORM_SIGNED=0",),
     "debug": ("EXSUM_DEBUG_CHECKS=1",),
+    "pfbranch": ("EXSUM_PF_PRED=0",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 verbose = "-v" in names
