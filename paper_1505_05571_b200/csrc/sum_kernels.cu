@@ -16,13 +16,15 @@
 //
 // Why not the reference's 4096 shared bins: 64-bit shared atomics compile to
 // ATOMS.CAST.SPIN.64 CAS loops on sm_100a, random-bin read-modify-writes cost
-// ~3.5x in bank conflicts, and U[0,1) puts half of all terms in one bin.
+// ~3.5x in bank conflicts, and U[0,1) puts half of all terms in one bin; even
+// without counts or transfers that step measures 0.04-2.0 TB/s
+// (scripts/probes/bins.cu, profiles/r01_probe_bins.log).
 //
 // Per-term cost: 23.9 SASS instructions (14 integer ALU, 5 FMA-pipe IMADs, 4.25
 // LSU) and 6 shared wavefronts.  Loads are 256-bit (LDG.E.EF.ENL2.256),
 // "rolling": a vector's registers are refilled with the next batch's vector
-// right after its four terms are added, with a cp.async.bulk L2 prefetch one
-// batch further ahead.  When every lane's batch falls in one slot (narrow
+// right after its four terms are added, with one 8 KB cp.async.bulk L2
+// prefetch per warp one batch further ahead (predicated on lane 0: no branch).  When every lane's batch falls in one slot (narrow
 // exponent ranges) the batch is summed in registers and the slot gets one
 // read-modify-write; when each lane's batch also has one sign (U[0,1)), the
 // magnitudes are summed without the sign complement (8.5 instructions/term).
