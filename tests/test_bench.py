@@ -1,0 +1,57 @@
+"""bench.py contract.  CPU: the reference arm (the compiled reference on a small
+sample) prints a line with the contract's keys.  GPU: the device arm at a
+reduced size prints every key, a bit-exact result and a sane roofline."""
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def test_reference_arm_line():
+    from oracle import ref as R
+    if not R.available():
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                          "--steps", "2", "--warmup", "3", "--n", "2e5"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    assert line["unit"] == "GB/s" and line["value"] > 0 and line["higher_is_better"] is True
+    assert line["steps"] == 2 and line["warmup"] >= 3 and line["n_gpus"] == 1
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] == line["value"]
+    assert line["e2e"] == {"value": line["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+    assert line["config"]["workload"].startswith("config2")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", [2, 5])
+def test_device_arm_line(config):
+    """bench.py's own arm at a reduced size: every contract key, a bit-exact
+    result and a positive roofline fraction."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    args = [sys.executable, str(ROOT / "bench.py"), "--config", str(config), "--steps", "5",
+            "--warmup", "3"]
+    args += ["--n", "1e7"] if config == 2 else ["--no-cpu-baseline"]
+    out = subprocess.run(args, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+                "roofline", "e2e", "gpu_launches", "clocks"):
+        assert key in line, key
+    assert line["steps"] == 5 and line["warmup"] >= 3 and line["gpu_launches"] >= 5
+    r = line["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 2
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["value"] > 0
+    assert "workload" in line["config"]
+    if config == 2:  # the CPU leg also checks the device result against the reference
+        assert line["bit_exact_vs_oracle"] is True
+        assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] > 0
