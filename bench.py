@@ -50,7 +50,9 @@ def parse():
     p.add_argument("--steps", type=int, default=0, help="timed steps (default: ~0.5 s)")
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--config", type=int, default=2, choices=sorted(WORKLOADS))
-    p.add_argument("--n", type=float, default=0, help="override terms (per GPU for weak configs)")
+    p.add_argument("--n", "--terms", dest="n", type=float, default=0,
+                   help="override terms (per GPU for weak configs); --terms under torchrun, whose "
+                        "own parser would take --n for one of its options")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--seed", type=int, default=1)
     p.add_argument("--seg-order", default="longest", choices=["longest", "index"],
