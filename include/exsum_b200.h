@@ -133,6 +133,13 @@ int exsum_partial_from_array(const double *x, size_t n, uint64_t base_index,
  * canonical record (may alias parts[0]) and/or the rounded result. */
 int exsum_partial_merge(const exsum_partial *parts, size_t k, exsum_partial *out,
                         double *result);
+/* The library's own multithreaded host exact sum (the host half of the hybrid
+ * exsum_context_sum): parallel_exact_sum (vector_ops.cpp:172-186) re-designed —
+ * count-free significand bins with carry-flag transfers, dynamic work claiming
+ * across `threads` host threads (<= 0: all), index-ordered Inf/NaN.  Bits equal
+ * exact_sum(x) (vector_ops.cpp:121-130).  Outputs: result and/or partial. */
+int exsum_host_sum(const double *x, size_t n, uint64_t base_index, int threads, double *result,
+                   exsum_partial *partial);
 /* Rounded value of a partial record (SmallAccumulator::round on its acc). */
 int exsum_partial_round(const exsum_partial *p, double *out);
 
@@ -202,12 +209,27 @@ int exsum_cuda_merge(const exsum_partial *d_parts, size_t k, double *d_result,
                      exsum_partial *d_out, void *stream);
 
 /* ------------------------------------------------ host-buffer convenience */
-/* A device context: workspace, pinned-free staging ring, copy + compute streams.
- * exsum_context_sum is exact_sum(values) for a HOST array: host->device copies
- * pipelined against the device accumulate, result copied back.  Blocking. */
+/* A device context: workspace, 3-slot device staging ring, copy + compute
+ * streams, and a pool of host worker threads.  exsum_context_sum is
+ * exact_sum(values) (vector_ops.cpp:121-130) for a HOST array, the call a
+ * reference user makes.  The array is split dynamically: the calling thread
+ * streams chunks host->device (pinned memory: direct DMA; pageable: through
+ * pinned bounce buffers) into the sm_100a accumulate kernel while the host
+ * workers sum other chunks with exsum_host_sum's kernel; the two exact records
+ * are merged (exsum_partial_merge), so the bits equal exact_sum for any split.
+ * Blocking.  A context serves one sum at a time (concurrent calls on one context
+ * serialise on its lock); use one context per thread for parallel sums.  A
+ * failed sum leaves the context reset and reusable. */
 typedef struct exsum_context exsum_context;
 exsum_context *exsum_context_create(int device, size_t staging_bytes);
 void exsum_context_free(exsum_context *ctx);
+/* Host workers beside the device: < 0 = every hardware thread (default),
+ * 0 = device only (PCIe-bound), k = k threads.  Arrays under 2^20 terms are
+ * always summed on the device alone. */
+int exsum_context_set_host_threads(exsum_context *ctx, int threads);
+/* Terms the last successful sum gave the device and the host workers. */
+int exsum_context_last_split(const exsum_context *ctx, uint64_t *device_terms,
+                             uint64_t *host_terms);
 int exsum_context_sum(exsum_context *ctx, const double *h_x, size_t n, double *h_result,
                       exsum_partial *h_partial);
 /* The same for a shard whose first element has global index base_index (the
@@ -288,6 +310,14 @@ int exsum_p2p_sum(const double *d_shard, size_t n, uint64_t base_index, int rank
                   void *const *mailboxes, uint64_t epoch, double *d_result,
                   exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
                   unsigned flags);
+/* flags bit for exsum_p2p_sum: sum and publish this rank's record and flag to
+ * every mailbox, but return without waiting; exsum_p2p_collect (a one-warp
+ * launch, no data) later waits for every rank's flag and merges.  With it,
+ * ranks that share one GPU can be run strictly one after another (tests):
+ * no kernel ever waits on a kernel that is not finished. */
+#define EXSUM_P2P_PUBLISH_ONLY 2u
+int exsum_p2p_collect(int rank, int nranks, void *const *mailboxes, uint64_t epoch,
+                      double *d_result, exsum_partial *d_partial, void *stream);
 /* The same protocol with nranks emulated ranks in ONE cooperative launch on one
  * GPU (rank r sums d_x[bounds[r], bounds[r+1]); d_mailboxes: nranks contiguous
  * mailboxes; d_ws: nranks contiguous workspaces; outputs: nranks results /
@@ -307,7 +337,8 @@ int exsum_ipc_close(void *d_ptr);
 /* --------------------------------------------------- synthetic data (bench) */
 /* Seeded counter-based generators for the BASELINE.json configs (SURVEY.md
  * §8(d)); the value at index i depends only on (config, seed, i, n), so shards
- * generate independently.  config: 1..4 (config 5 values: exsum_cuda_gen_segmented). */
+ * generate independently.  config: 1..4 (config 5 values: exsum_{cuda,host}_gen_segmented);
+ * host and device produce identical bits. */
 int exsum_cuda_gen(int config, uint64_t seed, uint64_t n_total, uint64_t first,
                    size_t count, double *d_out, void *stream);
 int exsum_host_gen(int config, uint64_t seed, uint64_t n_total, uint64_t first,
@@ -318,6 +349,8 @@ int exsum_host_gen_offsets(uint64_t seed, size_t nseg, uint64_t lo, uint64_t hi,
                            uint64_t *offsets);
 int exsum_cuda_gen_segmented(uint64_t seed, uint64_t first, size_t count, double *d_out,
                              void *stream);
+/* The same config-5 values on the host (bit-identical to exsum_cuda_gen_segmented). */
+int exsum_host_gen_segmented(uint64_t seed, uint64_t first, size_t count, double *out);
 
 /* Library build/version info: "exsum_b200 <version> sm_100a". */
 const char *exsum_version(void);

@@ -17,14 +17,15 @@ PORT_SO = HERE / "lib" / "libexsum_port.so"
 
 
 def ensure_built() -> Path:
-    src = HERE / "port" / "exsum_port.c"
-    if not PORT_SO.exists() or PORT_SO.stat().st_mtime < src.stat().st_mtime:
+    srcs = [HERE / "port" / f for f in ("exsum_port.c", "exsum_port.h", "synth_port.c")]
+    if not PORT_SO.exists() or PORT_SO.stat().st_mtime < max(s.stat().st_mtime for s in srcs):
         subprocess.run(["make", "-s", "-C", str(HERE), "port"], check=True)
     return PORT_SO
 
 
 class Port:
     kind = "port"
+    _shared = None
 
     def __init__(self):
         L = self.lib = C.CDLL(str(ensure_built()))
@@ -37,6 +38,8 @@ class Port:
             ("port_max_threads", i32, []),
             ("port_sqnorm", dbl, [vp, sz]),
             ("port_dot", i32, [vp, sz, vp, sz, C.POINTER(dbl)]),
+            ("port_gen", i32, [i32, u64, u64, u64, sz, vp]),
+            ("port_gen_offsets", i32, [u64, sz, u64, u64, vp]),
         ]:
             f = getattr(L, name)
             f.restype, f.argtypes = res, args
@@ -87,6 +90,28 @@ class Port:
 
     def max_threads(self) -> int:
         return self.lib.port_max_threads()
+
+
+def gen(config: int, seed: int, n_total: int, first: int = 0, count: int | None = None,
+        out: np.ndarray | None = None) -> np.ndarray:
+    """The benchmark inputs (synth_port.c, bit-identical to the product's generator)
+    without loading the product library: bench.py's reference arm uses this."""
+    count = n_total - first if count is None else count
+    x = np.empty(count, dtype=np.float64) if out is None else out
+    if Port._shared is None:
+        Port._shared = Port()
+    if Port._shared.lib.port_gen(config, seed, n_total, first, count, x.ctypes.data):
+        raise ValueError(f"port_gen: bad config {config}")
+    return x
+
+
+def gen_offsets(seed: int, nseg: int, lo: int = 1000, hi: int = 100_000) -> np.ndarray:
+    offs = np.zeros(nseg + 1, dtype=np.uint64)
+    if Port._shared is None:
+        Port._shared = Port()
+    if Port._shared.lib.port_gen_offsets(seed, nseg, lo, hi, offs.ctypes.data):
+        raise ValueError("port_gen_offsets: bad bounds")
+    return offs
 
 
 def checker():

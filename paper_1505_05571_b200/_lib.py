@@ -92,6 +92,7 @@ _SIGNATURES = {
     "exsum_sqnorm": (_i32, [_vp, _sz, _dp]),
     "exsum_dot": (_i32, [_vp, _sz, _vp, _sz, _dp]),
     "exsum_partial_from_array": (_i32, [_vp, _sz, _u64, _pp]),
+    "exsum_host_sum": (_i32, [_vp, _sz, _u64, _i32, _dp, _pp]),
     "exsum_partial_merge": (_i32, [_pp, _sz, _pp, _dp]),
     "exsum_partial_round": (_i32, [_pp, _dp]),
     "exsum_cuda_workspace_bytes": (_sz, []),
@@ -115,6 +116,7 @@ _SIGNATURES = {
     "exsum_p2p_mailbox_bytes": (_sz, [_i32]),
     "exsum_p2p_mailbox_alloc": (_i32, [_i32, C.POINTER(_vp)]),
     "exsum_p2p_mailbox_free": (_i32, [_vp]),
+    "exsum_p2p_collect": (_i32, [_i32, _i32, C.POINTER(_vp), _u64, _vp, _vp, _vp]),
     "exsum_p2p_sum": (_i32, [_vp, _sz, _u64, _i32, _i32, C.POINTER(_vp), _u64, _vp, _vp, _vp, _sz,
                              _vp, C.c_uint]),
     "exsum_p2p_emulate_sum": (_i32, [_vp, C.POINTER(_u64), _i32, _u64, _vp, _vp, _vp, _vp, _sz,
@@ -133,10 +135,13 @@ _SIGNATURES = {
     "exsum_context_free": (None, [_vp]),
     "exsum_context_sum": (_i32, [_vp, _vp, _sz, _dp, _pp]),
     "exsum_context_sum_at": (_i32, [_vp, _vp, _sz, _u64, _dp, _pp]),
+    "exsum_context_set_host_threads": (_i32, [_vp, _i32]),
+    "exsum_context_last_split": (_i32, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
     "exsum_cuda_gen": (_i32, [_i32, _u64, _u64, _u64, _sz, _vp, _vp]),
     "exsum_host_gen": (_i32, [_i32, _u64, _u64, _u64, _sz, _vp]),
     "exsum_host_gen_offsets": (_i32, [_u64, _sz, _u64, _u64, _vp]),
     "exsum_cuda_gen_segmented": (_i32, [_u64, _u64, _sz, _vp, _vp]),
+    "exsum_host_gen_segmented": (_i32, [_u64, _u64, _sz, _vp]),
     "exsum_version": (C.c_char_p, []),
 }
 

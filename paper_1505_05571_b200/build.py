@@ -24,8 +24,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = "/usr/bin/g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["sum_kernels.cu", "synth.cu", "context.cu", "nccl_sum.cu"]
-CXX_SOURCES = ["host_accumulators.cpp", "io.cpp"]
-HEADERS = [CSRC / "exsum_core.h", INCLUDE / "exsum_b200.h"]
+CXX_SOURCES = ["host_accumulators.cpp", "io.cpp", "host_sum.cpp"]
+HEADERS = [CSRC / "exsum_core.h", CSRC / "host_sum.h", INCLUDE / "exsum_b200.h"]
 
 
 def _stale(target: Path, deps: list[Path]) -> bool:
@@ -62,11 +62,12 @@ def build(verbose: bool = False, force: bool = False, defines: tuple[str, ...] =
         obj = build_dir / (src + ".o")
         objs.append(obj)
         if force or _stale(obj, [CSRC / src, *HEADERS]):
-            _run([CXX, *dflags, "-std=c++17", "-O2", "-fPIC", "-Wall", "-Wextra", *common_inc,
+            _run([CXX, *dflags, "-std=c++17", "-O3" if src == "host_sum.cpp" else "-O2", "-fPIC",
+                  "-pthread", "-Wall", "-Wextra", *common_inc,
                   "-c", str(CSRC / src), "-o", str(obj)], verbose)
     if force or _stale(lib, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs),
-              "-Xcompiler", "-fopenmp", "-lgomp", "-ldl"], verbose)
+              "-Xcompiler", "-fopenmp", "-lgomp", "-ldl", "-lpthread"], verbose)
     return lib
 
 

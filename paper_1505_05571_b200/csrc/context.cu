@@ -1,14 +1,24 @@
-// context.cu — exact sum of a HOST array through the device path.
+// context.cu — exact sum of a HOST array: the B200 and the host cores together.
 //
 // exsum_context_sum is the drop-in for exact_sum(values, ExactMethod::large)
 // (vector_ops.cpp:121-130) when the caller's values live in host memory, as
-// they do for every reference caller.  The array is streamed through a
-// two-buffer device staging ring: the copy stream moves chunk i+1 host->device
-// while the compute stream accumulates chunk i (exsum_cuda_accumulate with the
-// chunk's global base index, so Inf/NaN order is preserved); one finalize
-// launch rounds, and the 8-byte result (and optionally the 592-byte partial
-// record) is copied back.  Pinned host memory gives full PCIe/C2C bandwidth;
-// pageable memory works but is staged by the driver.
+// they do for every reference caller.  The array is split DYNAMICALLY between
+//
+//   * the device feeder (the calling thread): claims chunks from a shared
+//     cursor, copies each host->device over PCIe into a 3-slot device staging
+//     ring (copy stream) and accumulates it there (exsum_cuda_accumulate with the
+//     chunk's global base index, compute stream); at most two chunks in flight,
+//     so the DMA engine never idles and the device never hoards work;
+//   * the host workers (exsum_host::Pool, host_sum.cpp): claim small chunks
+//     from the same cursor and sum them with the library's own host kernel.
+//
+// Each side ends with an exact exsum_partial record (global Inf/NaN indices);
+// exsum_partial_merge combines them, so the bits equal exact_sum(values) for
+// any split.  Why both: PCIe caps the device at ~55 GB/s H2D, below what the
+// host cores stream; the device adds its PCIe rate on top of the cores'.
+// Pinned host memory is DMA'd directly; pageable memory is staged by the feeder
+// through pinned bounce buffers.  exsum_context_set_host_threads(ctx, 0) gives a
+// device-only sum (the PCIe-bound path).
 
 #include <cuda_runtime.h>
 #include <fcntl.h>
@@ -16,39 +26,54 @@
 #include <string.h>
 #include <unistd.h>
 
+#include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <new>
 #include <string>
 
 #include "exsum_b200.h"
+#include "host_sum.h"
+
+namespace {
+constexpr int kSlots = 3;     // device staging buffers
+constexpr int kInFlight = 2;  // chunks claimed by the feeder and not yet copied
+constexpr size_t kHostGrain = size_t{1} << 18;  // terms per host-worker claim (2 MB)
+}  // namespace
 
 struct exsum_context {
   int device = 0;
+  std::mutex busy;  // one sum at a time per context (staging, workspace, pool)
   void *ws = nullptr;
   size_t ws_bytes = 0;
-  double *stage[2] = {nullptr, nullptr};
+  double *stage[kSlots] = {};
   size_t stage_elems = 0;
   cudaStream_t copy = nullptr, compute = nullptr;
-  cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+  cudaEvent_t copied[kSlots] = {}, consumed[kSlots] = {};
   double *d_result = nullptr;
   exsum_partial *d_partial = nullptr;
-  double *host[2] = {nullptr, nullptr};  // pinned file-read buffers (first file sum)
-  cudaEvent_t h2d[2] = {nullptr, nullptr};
+  exsum_partial *h_partial = nullptr;  // pinned landing slot of the device record
+  double *host[kSlots] = {};           // pinned bounce buffers (pageable input, files)
+  int host_threads = -1;               // < 0: all hardware threads; 0: device only
+  exsum_host::Pool *pool = nullptr;
+  uint64_t last_device_terms = 0, last_host_terms = 0;
 };
 
 namespace {
 
 void destroy(exsum_context *c) {
   if (!c) return;
+  delete c->pool;
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < kSlots; ++i) {
     if (c->host[i]) cudaFreeHost(c->host[i]);
-    if (c->h2d[i]) cudaEventDestroy(c->h2d[i]);
     if (c->stage[i]) cudaFree(c->stage[i]);
     if (c->copied[i]) cudaEventDestroy(c->copied[i]);
     if (c->consumed[i]) cudaEventDestroy(c->consumed[i]);
   }
+  if (c->h_partial) cudaFreeHost(c->h_partial);
   if (c->ws) cudaFree(c->ws);
   if (c->d_result) cudaFree(c->d_result);
   if (c->d_partial) cudaFree(c->d_partial);
@@ -58,27 +83,102 @@ void destroy(exsum_context *c) {
   delete c;
 }
 
+int ensure_bounce(exsum_context *c) {
+  for (int i = 0; i < kSlots; ++i)
+    if (!c->host[i] && cudaMallocHost(&c->host[i], c->stage_elems * sizeof(double)) != cudaSuccess)
+      return EXSUM_ECUDA;
+  return EXSUM_OK;
+}
+
+// After a failed sum the workspace may hold part of an accumulation: clear it so
+// the next sum on this context starts from zero (drain both streams first).
+void reset_after_error(exsum_context *c) {
+  cudaGetLastError();
+  cudaStreamSynchronize(c->copy);
+  cudaStreamSynchronize(c->compute);
+  exsum_cuda_workspace_init(c->ws, c->ws_bytes, c->compute);
+  cudaStreamSynchronize(c->compute);
+}
+
+bool is_pinned(const void *p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+// Device feeder: claim chunks from *cursor until it passes n; copy + accumulate.
+// Returns the number of terms it took, or sets *st.
+uint64_t feed_device(exsum_context *c, const double *h_x, size_t n, uint64_t base,
+                     std::atomic<size_t> *cursor, bool pinned, bool hybrid, int *st) {
+  uint64_t taken = 0;
+  for (int i = 0;; ++i) {
+    const int b = i % kSlots;
+    if (i >= kInFlight && cudaEventSynchronize(c->copied[(i - kInFlight) % kSlots]) != cudaSuccess) {
+      *st = EXSUM_ECUDA;
+      break;
+    }
+    // guided claim: no more than a quarter of what is left while the host shares
+    const size_t seen = cursor->load(std::memory_order_relaxed);
+    if (seen >= n) break;
+    size_t want = c->stage_elems;
+    if (hybrid) want = std::min(want, std::max<size_t>((n - seen) / 4, size_t{1} << 16));
+    const size_t off = cursor->fetch_add(want, std::memory_order_relaxed);
+    if (off >= n) break;
+    const size_t len = std::min(want, n - off);
+    const double *src = h_x + off;
+    if (!pinned) {  // bounce b is free: its last copy (chunk i - kSlots) completed above
+      memcpy(c->host[b], src, len * sizeof(double));
+      src = c->host[b];
+    }
+    if ((i >= kSlots && cudaStreamWaitEvent(c->copy, c->consumed[b], 0) != cudaSuccess) ||
+        cudaMemcpyAsync(c->stage[b], src, len * sizeof(double), cudaMemcpyHostToDevice,
+                        c->copy) != cudaSuccess ||
+        cudaEventRecord(c->copied[b], c->copy) != cudaSuccess ||
+        cudaStreamWaitEvent(c->compute, c->copied[b], 0) != cudaSuccess) {
+      *st = EXSUM_ECUDA;
+      break;
+    }
+    *st = exsum_cuda_accumulate(c->stage[b], len, base + off, c->ws, c->ws_bytes, c->compute);
+    if (*st != EXSUM_OK) break;
+    if (cudaEventRecord(c->consumed[b], c->compute) != cudaSuccess) {
+      *st = EXSUM_ECUDA;
+      break;
+    }
+    taken += len;
+  }
+  return taken;
+}
+
 }  // namespace
 
 extern "C" {
 
 exsum_context *exsum_context_create(int device, size_t staging_bytes) {
-  if (staging_bytes < (size_t{1} << 20)) staging_bytes = size_t{1} << 20;
+  if (staging_bytes < (size_t{3} << 20)) staging_bytes = size_t{3} << 20;
   exsum_context *c = new (std::nothrow) exsum_context;
   if (!c) return nullptr;
   c->device = device;
   int prev = 0;
   cudaGetDevice(&prev);
   bool ok = cudaSetDevice(device) == cudaSuccess;
-  c->stage_elems = staging_bytes / 2 / sizeof(double);
+  // one device chunk: a third of the staging bytes, capped at 64 MB (PCIe runs at
+  // full rate from a few MB; smaller chunks balance better against the host)
+  c->stage_elems = std::min(staging_bytes / kSlots, size_t{64} << 20) / sizeof(double);
   c->stage_elems &= ~size_t{3};
   c->ws_bytes = exsum_cuda_workspace_bytes();
   ok = ok && cudaMalloc(&c->ws, c->ws_bytes) == cudaSuccess;
   ok = ok && cudaMalloc(&c->d_result, sizeof(double)) == cudaSuccess;
   ok = ok && cudaMalloc(&c->d_partial, sizeof(exsum_partial)) == cudaSuccess;
-  for (int i = 0; i < 2 && ok; ++i) {
+  ok = ok && cudaMallocHost(&c->h_partial, sizeof(exsum_partial)) == cudaSuccess;
+  for (int i = 0; i < kSlots && ok; ++i) {
     ok = cudaMalloc(&c->stage[i], c->stage_elems * sizeof(double)) == cudaSuccess;
-    ok = ok && cudaEventCreateWithFlags(&c->copied[i], cudaEventDisableTiming) == cudaSuccess;
+    // blocking-sync events: the feeder sleeps while DMA runs, leaving its core to
+    // the host workers
+    ok = ok && cudaEventCreateWithFlags(&c->copied[i], cudaEventDisableTiming |
+                                                           cudaEventBlockingSync) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->consumed[i], cudaEventDisableTiming) == cudaSuccess;
   }
   ok = ok && cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) == cudaSuccess;
@@ -95,6 +195,25 @@ exsum_context *exsum_context_create(int device, size_t staging_bytes) {
 
 void exsum_context_free(exsum_context *ctx) { destroy(ctx); }
 
+int exsum_context_set_host_threads(exsum_context *c, int threads) {
+  if (!c) return EXSUM_EINVAL;
+  std::lock_guard<std::mutex> lk(c->busy);
+  if (threads != c->host_threads) {
+    delete c->pool;
+    c->pool = nullptr;
+    c->host_threads = threads;
+  }
+  return EXSUM_OK;
+}
+
+int exsum_context_last_split(const exsum_context *c, uint64_t *device_terms,
+                             uint64_t *host_terms) {
+  if (!c) return EXSUM_EINVAL;
+  if (device_terms) *device_terms = c->last_device_terms;
+  if (host_terms) *host_terms = c->last_host_terms;
+  return EXSUM_OK;
+}
+
 int exsum_context_sum(exsum_context *c, const double *h_x, size_t n, double *h_result,
                       exsum_partial *h_partial) {
   return exsum_context_sum_at(c, h_x, n, 0, h_result, h_partial);
@@ -103,41 +222,54 @@ int exsum_context_sum(exsum_context *c, const double *h_x, size_t n, double *h_r
 int exsum_context_sum_at(exsum_context *c, const double *h_x, size_t n, uint64_t base_index,
                          double *h_result, exsum_partial *h_partial) {
   if (!c || (n && !h_x) || (!h_result && !h_partial)) return EXSUM_EINVAL;
+  std::lock_guard<std::mutex> lk(c->busy);
   int prev = 0;
   cudaGetDevice(&prev);
   if (cudaSetDevice(c->device) != cudaSuccess) return EXSUM_ECUDA;
-  int st = EXSUM_OK;
-  size_t off = 0;
-  int i = 0;
-  while (off < n && st == EXSUM_OK) {
-    const size_t len = (n - off < c->stage_elems) ? n - off : c->stage_elems;
-    const int b = i & 1;
-    if (cudaStreamWaitEvent(c->copy, c->consumed[b], 0) != cudaSuccess ||
-        cudaMemcpyAsync(c->stage[b], h_x + off, len * sizeof(double), cudaMemcpyHostToDevice,
-                        c->copy) != cudaSuccess ||
-        cudaEventRecord(c->copied[b], c->copy) != cudaSuccess ||
-        cudaStreamWaitEvent(c->compute, c->copied[b], 0) != cudaSuccess) {
-      st = EXSUM_ECUDA;
-      break;
+  const bool pinned = n == 0 || is_pinned(h_x);
+  int st = pinned ? EXSUM_OK : ensure_bounce(c);
+  // host workers: every hardware thread by default (the feeder mostly sleeps in
+  // blocking event waits); none for arrays too small to amortise a wake-up
+  int workers = c->host_threads < 0 ? exsum_host::default_threads() : c->host_threads;
+  if (n < (size_t{1} << 20)) workers = 0;
+  if (st == EXSUM_OK && workers > 0 && (!c->pool || c->pool->size() != workers + 1)) {
+    delete c->pool;
+    c->pool = new (std::nothrow) exsum_host::Pool(workers + 1);  // slot 0: the feeder
+    if (!c->pool || !c->pool->ok()) {
+      delete c->pool;
+      c->pool = nullptr;
+      workers = 0;
     }
-    st = exsum_cuda_accumulate(c->stage[b], len, base_index + off, c->ws, c->ws_bytes,
-                               c->compute);
-    if (st == EXSUM_OK && cudaEventRecord(c->consumed[b], c->compute) != cudaSuccess)
-      st = EXSUM_ECUDA;
-    off += len;
-    ++i;
   }
+  std::atomic<size_t> cursor{0};
+  const bool hybrid = workers > 0 && c->pool;
+  if (st == EXSUM_OK && hybrid) c->pool->start(h_x, n, base_index, &cursor, kHostGrain);
+  uint64_t dev_terms = 0;
+  if (st == EXSUM_OK) dev_terms = feed_device(c, h_x, n, base_index, &cursor, pinned, hybrid, &st);
   if (st == EXSUM_OK)
     st = exsum_cuda_finalize(c->d_result, c->d_partial, c->ws, c->ws_bytes, c->compute);
-  if (st == EXSUM_OK && h_result &&
-      cudaMemcpyAsync(h_result, c->d_result, sizeof(double), cudaMemcpyDeviceToHost,
+  if (st == EXSUM_OK &&
+      cudaMemcpyAsync(c->h_partial, c->d_partial, sizeof(exsum_partial), cudaMemcpyDeviceToHost,
                       c->compute) != cudaSuccess)
     st = EXSUM_ECUDA;
-  if (st == EXSUM_OK && h_partial &&
-      cudaMemcpyAsync(h_partial, c->d_partial, sizeof(exsum_partial), cudaMemcpyDeviceToHost,
-                      c->compute) != cudaSuccess)
-    st = EXSUM_ECUDA;
-  if (cudaStreamSynchronize(c->compute) != cudaSuccess) st = EXSUM_ECUDA;
+  if (cudaStreamSynchronize(c->compute) != cudaSuccess && st == EXSUM_OK) st = EXSUM_ECUDA;
+  if (hybrid) c->pool->join_helpers();  // workers finish the array even if the device failed
+  if (st != EXSUM_OK) {
+    reset_after_error(c);
+  } else {
+    exsum_partial merged;
+    if (hybrid) {
+      auto &parts = c->pool->parts();
+      parts[0] = *c->h_partial;
+      exsum_partial_merge(parts.data(), parts.size(), &merged, nullptr);
+    } else {
+      merged = *c->h_partial;
+    }
+    if (h_partial) *h_partial = merged;
+    if (h_result) exsum_partial_round(&merged, h_result);
+    c->last_device_terms = dev_terms;
+    c->last_host_terms = n - dev_terms;
+  }
   cudaSetDevice(prev);
   return st;
 }
@@ -155,7 +287,8 @@ int exsum_context_sum_file(exsum_context *c, const char *path, int format, doubl
     return st;
   }
   if (format != EXSUM_FORMAT_BIN) return EXSUM_EINVAL;
-  // bin: validate like read_values (io.cpp:94-99), then stream
+  // bin: validate like read_values (io.cpp:94-99), then stream disk -> pinned
+  // bounce -> device (the disk, not the cores, bounds this path: device only)
   double *probe = nullptr;
   size_t dummy = 0;
   const int fd = open(path, O_RDONLY);
@@ -165,27 +298,21 @@ int exsum_context_sum_file(exsum_context *c, const char *path, int format, doubl
     close(fd);
     return exsum_read_values(path, format, &probe, &dummy);
   }
+  std::lock_guard<std::mutex> lk(c->busy);
   int prev = 0;
   cudaGetDevice(&prev);
   if (cudaSetDevice(c->device) != cudaSuccess) {
     close(fd);
     return EXSUM_ECUDA;
   }
-  int st = EXSUM_OK;
-  for (int i = 0; i < 2 && st == EXSUM_OK; ++i) {
-    if (!c->host[i] &&
-        (cudaMallocHost(&c->host[i], c->stage_elems * sizeof(double)) != cudaSuccess ||
-         cudaEventCreateWithFlags(&c->h2d[i], cudaEventDisableTiming) != cudaSuccess))
-      st = EXSUM_ECUDA;
-  }
+  int st = ensure_bounce(c);
   const size_t n = static_cast<size_t>(size) / 8;
   size_t off = 0;
-  int i = 0;
-  while (off < n && st == EXSUM_OK) {
+  for (int i = 0; off < n && st == EXSUM_OK; ++i) {
     const size_t len = (n - off < c->stage_elems) ? n - off : c->stage_elems;
-    const int b = i & 1;
-    // the host buffer is free once its previous host->device copy completed
-    if (i >= 2 && cudaEventSynchronize(c->h2d[b]) != cudaSuccess) {
+    const int b = i % kSlots;
+    // the bounce buffer and stage slot are free once chunk i - kSlots was consumed
+    if (i >= kSlots && cudaEventSynchronize(c->consumed[b]) != cudaSuccess) {
       st = EXSUM_ECUDA;
       break;
     }
@@ -200,10 +327,8 @@ int exsum_context_sum_file(exsum_context *c, const char *path, int format, doubl
       st = EXSUM_EIO;
       break;
     }
-    if (cudaStreamWaitEvent(c->copy, c->consumed[b], 0) != cudaSuccess ||
-        cudaMemcpyAsync(c->stage[b], c->host[b], len * sizeof(double), cudaMemcpyHostToDevice,
+    if (cudaMemcpyAsync(c->stage[b], c->host[b], len * sizeof(double), cudaMemcpyHostToDevice,
                         c->copy) != cudaSuccess ||
-        cudaEventRecord(c->h2d[b], c->copy) != cudaSuccess ||
         cudaEventRecord(c->copied[b], c->copy) != cudaSuccess ||
         cudaStreamWaitEvent(c->compute, c->copied[b], 0) != cudaSuccess) {
       st = EXSUM_ECUDA;
@@ -213,26 +338,29 @@ int exsum_context_sum_file(exsum_context *c, const char *path, int format, doubl
     if (st == EXSUM_OK && cudaEventRecord(c->consumed[b], c->compute) != cudaSuccess)
       st = EXSUM_ECUDA;
     off += len;
-    ++i;
   }
   close(fd);
   if (st == EXSUM_OK)
     st = exsum_cuda_finalize(c->d_result, c->d_partial, c->ws, c->ws_bytes, c->compute);
-  if (st == EXSUM_OK && h_result &&
-      cudaMemcpyAsync(h_result, c->d_result, sizeof(double), cudaMemcpyDeviceToHost,
-                      c->compute) != cudaSuccess)
-    st = EXSUM_ECUDA;
-  if (st == EXSUM_OK && h_partial &&
-      cudaMemcpyAsync(h_partial, c->d_partial, sizeof(exsum_partial), cudaMemcpyDeviceToHost,
+  if (st == EXSUM_OK &&
+      cudaMemcpyAsync(c->h_partial, c->d_partial, sizeof(exsum_partial), cudaMemcpyDeviceToHost,
                       c->compute) != cudaSuccess)
     st = EXSUM_ECUDA;
   if (cudaStreamSynchronize(c->compute) != cudaSuccess && st == EXSUM_OK) st = EXSUM_ECUDA;
   if (cudaStreamSynchronize(c->copy) != cudaSuccess && st == EXSUM_OK) st = EXSUM_ECUDA;
+  if (st != EXSUM_OK) {
+    reset_after_error(c);  // EIO mid-file leaves chunks in the workspace otherwise
+  } else {
+    if (h_partial) *h_partial = *c->h_partial;
+    if (h_result) exsum_partial_round(c->h_partial, h_result);
+    c->last_device_terms = n;
+    c->last_host_terms = 0;
+    if (n_out) *n_out = n;
+  }
   cudaSetDevice(prev);
-  if (st == EXSUM_OK && n_out) *n_out = n;
   return st;
 }
 
-const char *exsum_version(void) { return "exsum_b200 0.1.0 sm_100a"; }
+const char *exsum_version(void) { return "exsum_b200 0.2.0 sm_100a"; }
 
 }  // extern "C"

@@ -1,0 +1,355 @@
+// host_sum.cpp — the library's multithreaded HOST exact sum (the CPU side of a
+// hybrid host+device sum of a host-resident array).
+//
+// Why it exists: a reference caller holds its values in host memory
+// (exact_sum(std::span<const double>), vector_ops.cpp:121-130).  Shipping them
+// to the B200 is capped by PCIe (~55 GB/s H2D on the box), below the 16-thread
+// reference (~93 GB/s).  exsum_context_sum therefore streams part of the array
+// to the device while these host workers sum the rest, and merges the exact
+// partial records (exsum_partial, global Inf/NaN indices) — bits identical to
+// exact_sum whatever the split.
+//
+// The per-term kernel is the paper's large superaccumulator (Neal 2015, §4;
+// large_accumulator.hpp:47-59) re-designed for a modern out-of-order core:
+//
+//   reference: bins of raw bit patterns + an int16 countdown per bin; every
+//              add loads, decrements, tests and stores the count (the count
+//              both limits overflow and later recovers the implicit ones and
+//              strips the exponent bits, large_accumulator.cpp:77-96).
+//   here:      bins of SIGNIFICANDS (mantissa | implicit bit, exponent and
+//              sign dropped: the bin index carries them), so no count is
+//              needed to decode a bin; overflow is caught by the carry flag
+//              of the 64-bit add itself (one add < 2^53, so a bin wraps at
+//              most once per add and after >= 2048 adds) and the wrapped bin is
+//              transferred with its carry bit 2^64 — exact, no countdown.
+//   per term:  load, shift, and, or, add-to-memory, never-taken jc.
+//
+// Zeros, denormals, Inf and NaN are screened eight terms at a time (one
+// exponent-field test per group); a group containing any takes a careful
+// per-term path (denormals without the implicit bit, specials recorded by first
+// global index, exactly like the device kernels' side channel).
+//
+// Bins drain into a 67-chunk small superaccumulator (chunk i weighs
+// 2^(32 i - 1075), small_accumulator.hpp:27-35) as three 32-bit pieces, the
+// reference's transfer geometry (large_accumulator.cpp:81-109) applied to a
+// 65-bit significand sum; exsum_core.h canonicalises and rounds.
+
+#include <immintrin.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <thread>
+#include <vector>
+
+#include "exsum_b200.h"
+#include "exsum_core.h"
+#include "host_sum.h"
+
+using namespace exsum_b200;
+
+namespace exsum_host {
+
+namespace {
+
+constexpr uint64_t kImplicit = uint64_t{1} << kMantBits;
+constexpr uint64_t kExpField = uint64_t{0x7FF} << kMantBits;
+
+}  // namespace
+
+void Acc::reset() {
+  std::memset(bin, 0, sizeof bin);
+  std::memset(chunk, 0, sizeof chunk);
+  transfers = 0;
+  P = M = N = kNoIndex;
+  payload = 0;
+  terms = 0;
+}
+
+// value = (carry * 2^64 + v) * 2^(e' - 1075), e' = max(e, 1), sign from ix.
+// Placed at chunk e' >> 5 shifted by e' & 31: at most 65 + 31 = 96 bits, three
+// 32-bit pieces into chunks base .. base + 2 (base + 2 <= 65 < 67).
+__attribute__((noinline)) void Acc::transfer(uint32_t ix, uint64_t v, uint64_t carry) {
+  const uint32_t e = ix & 0x7FFu;
+  const uint32_t ep = e ? e : 1u;
+  const uint32_t sh = ep & 31u, base = ep >> 5;
+  const unsigned __int128 w = ((static_cast<unsigned __int128>(carry) << 64) | v) << sh;
+  const int64_t p0 = static_cast<int64_t>(static_cast<uint64_t>(w) & 0xFFFFFFFFull);
+  const int64_t p1 = static_cast<int64_t>(static_cast<uint64_t>(w >> 32) & 0xFFFFFFFFull);
+  const int64_t p2 = static_cast<int64_t>(static_cast<uint64_t>(w >> 64));
+  if (ix >> 11) {
+    chunk[base] -= p0;
+    chunk[base + 1] -= p1;
+    chunk[base + 2] -= p2;
+  } else {
+    chunk[base] += p0;
+    chunk[base + 1] += p1;
+    chunk[base + 2] += p2;
+  }
+  // each transfer moves < 2^32 into a chunk: canonicalise long before 2^62
+  if (++transfers >= (1u << 20)) {
+    exsum_canonicalize(chunk);
+    transfers = 0;
+  }
+}
+
+inline void Acc::add_sig(uint32_t ix, uint64_t sig) {
+  uint64_t s;
+  if (__builtin_expect(__builtin_add_overflow(bin[0][ix], sig, &s), 0)) {
+    transfer(ix, s, 1);
+    s = 0;
+  }
+  bin[0][ix] = s;
+}
+
+// The block's zeros, denormals, Inf and NaN (exponent field 0 or 0x7FF), after
+// the blind pass put them into the sentinel bins: denormals go to the bin of
+// exponent 1 (same weight, no implicit bit), specials to the first-index record.
+// Groups of eight are screened with one vector test (1% denormals -> ~8% of
+// groups need the per-term look).
+namespace {
+
+// flags[g] = 1 iff group g (terms 8g .. 8g+7) holds an exponent field of 0 or 0x7FF:
+// ((b + 2^52) & exp) < 2^53  <=>  e in {0x7FF, 0}.
+__attribute__((target("avx512f"))) void odd_groups_avx512(const uint64_t *b, size_t ngroups,
+                                                           uint8_t *flags) {
+  const __m512i one = _mm512_set1_epi64(static_cast<long long>(kImplicit));
+  const __m512i ef = _mm512_set1_epi64(static_cast<long long>(kExpField));
+  const __m512i lim = _mm512_set1_epi64(static_cast<long long>((kImplicit << 1) - 1));
+  for (size_t g = 0; g < ngroups; ++g) {
+    const __m512i v = _mm512_loadu_si512(b + 8 * g);
+    const __m512i t = _mm512_and_si512(_mm512_add_epi64(v, one), ef);
+    flags[g] = _mm512_cmple_epu64_mask(t, lim) != 0;
+  }
+}
+
+void odd_groups_scalar(const uint64_t *b, size_t ngroups, uint8_t *flags) {
+  for (size_t g = 0; g < ngroups; ++g) {
+    bool odd = false;
+    for (int k = 0; k < 8; ++k) odd |= ((b[8 * g + k] + kImplicit) & kExpField) < (kImplicit << 1);
+    flags[g] = odd;
+  }
+}
+
+const bool kHaveAvx512 = __builtin_cpu_supports("avx512f");
+
+}  // namespace
+
+__attribute__((noinline)) void Acc::rescan(const uint64_t *b, size_t n, uint64_t gbase) {
+  for (int c = 0; c < kCopies; ++c)
+    bin[c][0] = bin[c][0x800] = bin[c][0x7FF] = bin[c][0xFFF] = 0;
+  uint8_t flags[kBlock / 8];
+  const size_t ng = n / 8;
+  if (kHaveAvx512)
+    odd_groups_avx512(b, ng, flags);
+  else
+    odd_groups_scalar(b, ng, flags);
+  for (size_t k = 0; k < n; ++k) {
+    if (k < 8 * ng && !flags[k / 8]) {
+      k |= 7;  // skip the rest of a clean group
+      continue;
+    }
+    const uint64_t v = b[k];
+    if (((v + kImplicit) & kExpField) >= (kImplicit << 1)) continue;  // normal
+    const uint64_t m = v & kMantMask;
+    if ((v & kExpField) == 0) {
+      if (m) add_sig(static_cast<uint32_t>(v >> kMantBits) | 1u, m);
+      continue;
+    }
+    const uint64_t gi = gbase + k;
+    if (m) {
+      if (gi < N) {
+        N = gi;
+        payload = v;
+      }
+    } else if (v >> 63) {
+      if (gi < M) M = gi;
+    } else if (gi < P) {
+      P = gi;
+    }
+  }
+}
+
+// Blind pass: every term's significand (mantissa | implicit bit) is added to
+// bin copy (k mod kCopies) of its sign+exponent index — no per-term test for
+// zeros, denormals or specials.  Those all have exponent field 0 or 0x7FF, so
+// they can only land in the four sentinel indices 0x000, 0x800, 0x7FF, 0xFFF,
+// which hold nothing else; a block of <= 2^10 terms cannot wrap a sentinel
+// bin.  After each block one test of the sentinels routes the rare block that
+// touched them through rescan().  The copies break the store-to-load chain
+// when consecutive terms share an exponent (U[0,1): half the terms in one bin).
+void Acc::add(const double *x, size_t n, uint64_t gbase) {
+  const uint64_t *b = reinterpret_cast<const uint64_t *>(x);
+  size_t i = 0;
+  while (i < n) {
+    const size_t len = n - i < kBlock ? n - i : kBlock;
+    const uint64_t *blk = b + i;
+    size_t k = 0;
+    for (; k + kCopies <= len; k += kCopies) {
+#pragma GCC unroll 8
+      for (int c = 0; c < kCopies; ++c) {
+        const uint64_t v = blk[k + c];
+        const uint64_t ix = v >> kMantBits;
+        uint64_t s;
+        if (__builtin_expect(
+                __builtin_add_overflow(bin[c][ix], (v & kMantMask) | kImplicit, &s), 0)) {
+          transfer(static_cast<uint32_t>(ix), s, 1);
+          s = 0;
+        }
+        bin[c][ix] = s;
+      }
+    }
+    for (; k < len; ++k) {
+      const uint64_t v = blk[k];
+      const uint64_t ix = v >> kMantBits;
+      uint64_t s;
+      if (__builtin_add_overflow(bin[0][ix], (v & kMantMask) | kImplicit, &s)) {
+        transfer(static_cast<uint32_t>(ix), s, 1);
+        s = 0;
+      }
+      bin[0][ix] = s;
+    }
+    uint64_t sentinel = 0;
+    for (int c = 0; c < kCopies; ++c)
+      sentinel |= bin[c][0] | bin[c][0x800] | bin[c][0x7FF] | bin[c][0xFFF];
+    if (__builtin_expect(sentinel != 0, 0)) rescan(blk, len, gbase + i);
+    i += len;
+  }
+  terms += n;
+}
+
+void Acc::finish(exsum_partial *out) {
+  for (int c = 0; c < kCopies; ++c)
+    for (uint32_t ix = 0; ix < 4096; ++ix)
+      if (bin[c][ix]) {
+        transfer(ix, bin[c][ix], 0);
+        bin[c][ix] = 0;
+      }
+  std::memset(out, 0, sizeof *out);
+  std::memcpy(out->acc.chunk, chunk, sizeof chunk);
+  exsum_canonicalize(out->acc.chunk);
+  exsum_resolve_specials(P, M, N, payload, &out->acc.inf_bits, &out->acc.nan_bits);
+  out->acc.adds_until_propagate = kCarryTerms;
+  out->first_pos_inf = P;
+  out->first_neg_inf = M;
+  out->first_nan = N;
+  out->nan_payload = payload;
+}
+
+int default_threads() {
+  const unsigned hc = std::thread::hardware_concurrency();
+  return hc ? static_cast<int>(hc) : 1;
+}
+
+// ------------------------------------------------------------------ Pool
+
+Pool::Pool(int nthreads) {
+  if (nthreads < 1) nthreads = 1;
+  accs_.resize(static_cast<size_t>(nthreads));
+  for (auto &a : accs_) a = new (std::nothrow) Acc;
+  for (int t = 1; t < nthreads; ++t) threads_.emplace_back([this, t] { worker(t); });
+}
+
+Pool::~Pool() {
+  {
+    std::lock_guard<std::mutex> lk(m_);
+    quit_ = true;
+    ++gen_;
+  }
+  cv_.notify_all();
+  for (auto &th : threads_) th.join();
+  for (auto *a : accs_) delete a;
+}
+
+bool Pool::ok() const {
+  for (auto *a : accs_)
+    if (!a) return false;
+  return true;
+}
+
+void Pool::run_share(int t) {
+  Acc *a = accs_[static_cast<size_t>(t)];
+  a->reset();
+  for (;;) {
+    const size_t begin = job_.cursor->fetch_add(job_.grain, std::memory_order_relaxed);
+    if (begin >= job_.n) break;
+    const size_t len = job_.n - begin < job_.grain ? job_.n - begin : job_.grain;
+    a->add(job_.x + begin, len, job_.base + begin);
+  }
+  a->finish(&parts_[static_cast<size_t>(t)]);
+}
+
+void Pool::worker(int t) {
+  uint64_t seen = 0;
+  for (;;) {
+    {
+      std::unique_lock<std::mutex> lk(m_);
+      cv_.wait(lk, [&] { return gen_ != seen; });
+      seen = gen_;
+      if (quit_) return;
+    }
+    run_share(t);
+    if (pending_.fetch_sub(1, std::memory_order_acq_rel) == 1) {
+      std::lock_guard<std::mutex> lk(m_);
+      done_cv_.notify_all();
+    }
+  }
+}
+
+void Pool::start(const double *x, size_t n, uint64_t base, std::atomic<size_t> *cursor,
+                 size_t grain) {
+  exsum_partial empty{};
+  empty.acc.adds_until_propagate = kCarryTerms;
+  empty.first_pos_inf = empty.first_neg_inf = empty.first_nan = kNoIndex;
+  parts_.assign(accs_.size(), empty);
+  job_ = Job{x, n, base, cursor, grain ? grain : (size_t{1} << 18)};
+  pending_.store(static_cast<int>(threads_.size()), std::memory_order_relaxed);
+  {
+    std::lock_guard<std::mutex> lk(m_);
+    ++gen_;
+  }
+  cv_.notify_all();
+}
+
+void Pool::join_helpers() {
+  std::unique_lock<std::mutex> lk(m_);
+  done_cv_.wait(lk, [&] { return pending_.load(std::memory_order_acquire) == 0; });
+}
+
+void Pool::sum(const double *x, size_t n, uint64_t base, exsum_partial *out) {
+  std::atomic<size_t> cursor{0};
+  start(x, n, base, &cursor, 0);
+  run_share(0);  // the calling thread is worker 0
+  join_helpers();
+  exsum_partial_merge(parts_.data(), parts_.size(), out, nullptr);
+}
+
+}  // namespace exsum_host
+
+// ================================================================== C ABI
+
+extern "C" int exsum_host_sum(const double *x, size_t n, uint64_t base_index, int threads,
+                              double *result, exsum_partial *partial) {
+  if ((n && !x) || (!result && !partial)) return EXSUM_EINVAL;
+  if (threads <= 0) threads = exsum_host::default_threads();
+  // no more threads than 1 Mi-term shares: thread start-up would dominate
+  const size_t cap = n >> 20;
+  if (static_cast<size_t>(threads) > cap) threads = cap ? static_cast<int>(cap) : 1;
+  exsum_partial rec;
+  if (threads == 1) {
+    exsum_host::Acc *a = new (std::nothrow) exsum_host::Acc;
+    if (!a) return EXSUM_ENOMEM;
+    a->reset();
+    a->add(x, n, base_index);
+    a->finish(&rec);
+    delete a;
+  } else {
+    exsum_host::Pool pool(threads);
+    if (!pool.ok()) return EXSUM_ENOMEM;
+    pool.sum(x, n, base_index, &rec);
+  }
+  if (partial) *partial = rec;
+  if (result) exsum_partial_round(&rec, result);
+  return EXSUM_OK;
+}

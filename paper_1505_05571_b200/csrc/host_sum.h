@@ -1,0 +1,94 @@
+// host_sum.h — the library's host superaccumulator workers (see host_sum.cpp).
+#ifndef EXSUM_HOST_SUM_H_
+#define EXSUM_HOST_SUM_H_
+
+#include <atomic>
+#include <condition_variable>
+#include <cstddef>
+#include <cstdint>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "exsum_b200.h"
+
+namespace exsum_host {
+
+// One worker's exact accumulator: 4096 significand bins (index = sign+exponent,
+// as large_accumulator.hpp:99-103) over a 67-chunk small superaccumulator, plus
+// the first global index of +Inf / -Inf / NaN.
+#ifndef EXSUM_HOST_COPIES
+#define EXSUM_HOST_COPIES 2
+#endif
+struct alignas(64) Acc {
+  static constexpr int kCopies = EXSUM_HOST_COPIES;
+  static constexpr size_t kBlock = 512;  // terms per blind pass (< 2^10: sentinels cannot wrap)
+  uint64_t bin[kCopies][4096];
+  int64_t chunk[67];
+  uint32_t transfers;
+  uint64_t P, M, N, payload;
+  uint64_t terms;
+
+  void reset();
+  // x[0..n) with global indices gbase .. gbase + n - 1
+  void add(const double *x, size_t n, uint64_t gbase);
+  // drain the bins; the canonical record with index-resolved Inf/NaN
+  void finish(exsum_partial *out);
+
+ private:
+  void transfer(uint32_t ix, uint64_t v, uint64_t carry);
+  void add_sig(uint32_t ix, uint64_t sig);
+  void rescan(const uint64_t *b, size_t n, uint64_t gbase);
+};
+
+int default_threads();
+
+// Persistent host workers.  A job is a host array and a shared element cursor:
+// every worker (the caller is worker 0 in sum(); in the hybrid context sum the
+// caller drives the device instead) claims `grain` terms at a time until the
+// cursor passes n, so the device feeder and the host workers split the array
+// dynamically.  Each worker's record lands in parts()[t].
+class Pool {
+ public:
+  explicit Pool(int nthreads);  // nthreads - 1 helper threads + the caller's slot
+  ~Pool();
+  Pool(const Pool &) = delete;
+  Pool &operator=(const Pool &) = delete;
+
+  bool ok() const;
+  int size() const { return static_cast<int>(accs_.size()); }
+  // Whole array on the pool, caller included; merged record in *out.
+  void sum(const double *x, size_t n, uint64_t base, exsum_partial *out);
+  // Hybrid: helpers start on the shared cursor; the caller does other work,
+  // may call run_share(0) itself, then join_helpers().
+  void start(const double *x, size_t n, uint64_t base, std::atomic<size_t> *cursor,
+             size_t grain);
+  void run_share(int t);
+  void join_helpers();
+  std::vector<exsum_partial> &parts() { return parts_; }
+  uint64_t terms(int t) const { return accs_[static_cast<size_t>(t)]->terms; }
+
+ private:
+  struct Job {
+    const double *x = nullptr;
+    size_t n = 0;
+    uint64_t base = 0;
+    std::atomic<size_t> *cursor = nullptr;
+    size_t grain = 0;
+  };
+  void worker(int t);
+
+  std::vector<Acc *> accs_;
+  std::vector<exsum_partial> parts_;
+  std::vector<std::thread> threads_;
+  std::mutex m_;
+  std::condition_variable cv_, done_cv_;
+  uint64_t gen_ = 0;
+  bool quit_ = false;
+  std::atomic<int> pending_{0};
+  Job job_;
+};
+
+}  // namespace exsum_host
+
+#endif  // EXSUM_HOST_SUM_H_

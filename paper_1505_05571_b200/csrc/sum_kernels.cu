@@ -913,6 +913,33 @@ __device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v)
   return v;
 }
 
+// Warp-parallel carry propagation of a 67-chunk row held as v[r] = chunk
+// 32 r + lane: repeated shuffle passes until no lane holds a carry (two or three
+// passes for accumulated chunk sums).  On return chunks 0..65 are in [0, 2^32)
+// and chunk 66 holds the signed rest; the value is unchanged.
+__device__ __forceinline__ void warp_carry(long long (&v)[3], int lane) {
+  const unsigned FULL = 0xffffffffu;
+  while (true) {
+    long long c[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) c[r] = (32 * r + lane < kChunks - 1) ? (v[r] >> 32) : 0;
+    if (!__any_sync(FULL, (c[0] | c[1] | c[2]) != 0)) break;
+    long long in[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const long long up = __shfl_up_sync(FULL, c[r], 1);
+      const long long wrap = r ? __shfl_sync(FULL, c[r - 1], 31) : 0;
+      in[r] = lane ? up : wrap;
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int idx = 32 * r + lane;
+      if (idx < kChunks - 1) v[r] &= 0xFFFFFFFFll;
+      if (idx < kChunks) v[r] += in[r];
+    }
+  }
+}
+
 // Warp-parallel finalisation (all 32 lanes of one warp): the canonical form and
 // rounding of exsum_core.h (SmallAccumulator::carry_propagate + round,
 // small_accumulator.cpp:244-348) without a 67-step serial chain:
@@ -943,25 +970,7 @@ __device__ void warp_emit_v(long long v0, long long v1, long long v2, unsigned l
   const unsigned FULL = 0xffffffffu;
   long long v[3] = {v0, v1, v2};
   // 1. carries: chunk i keeps its low 32 bits, passes the rest to i + 1; chunk 66 keeps all.
-  while (true) {
-    long long c[3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) c[r] = (32 * r + lane < kChunks - 1) ? (v[r] >> 32) : 0;
-    if (!__any_sync(FULL, (c[0] | c[1] | c[2]) != 0)) break;
-    long long in[3];
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const long long up = __shfl_up_sync(FULL, c[r], 1);
-      const long long wrap = r ? __shfl_sync(FULL, c[r - 1], 31) : 0;
-      in[r] = lane ? up : wrap;
-    }
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const int idx = 32 * r + lane;
-      if (idx < kChunks - 1) v[r] &= 0xFFFFFFFFll;
-      if (idx < kChunks) v[r] += in[r];
-    }
-  }
+  warp_carry(v, lane);
   const long long d66 = __shfl_sync(FULL, v[2], 2);
   // 2. canonical top.
   auto top_of = [&](unsigned b0, unsigned b1, unsigned b2) -> int {
@@ -1109,6 +1118,8 @@ struct GroupArgs {  // grid split into independent sums (emulated ranks); groups
 struct P2PArgs {
   int nranks;  // 0: no exchange
   int rank;    // this process's rank; group g of an emulation is rank g
+  int publish_only;  // 1: publish the record and flags, skip the wait/merge (exsum_p2p_collect
+                     // finishes later) — lets tests run ranks one after another
   unsigned long long epoch;
   unsigned char *mailbox[kMaxRanks];  // rank r's mailbox, mapped into this process
 };
@@ -1146,12 +1157,11 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 
 // Warp 0 of a rank's last CTA: publish this rank's record (own = its slot in
-// this rank's own mailbox, already written by warp_emit), wait for all ranks,
-// merge into row/P/M/N/payload for the final warp_emit.  Returns false on a
-// timeout (a peer never published), after flagging the mailbox's error word.
-__device__ bool p2p_exchange(const P2PArgs &p2p, int me, long long *row, unsigned long long &P,
-                             unsigned long long &M, unsigned long long &N,
-                             unsigned long long &payload, int lane) {
+// this rank's own mailbox, already written by warp_emit) to every rank, then
+// (p2p_collect) wait for all ranks and merge into row/P/M/N/payload for the
+// final warp_emit.  p2p_collect returns false on a timeout (a peer never
+// published), after flagging the mailbox's error word.
+__device__ void p2p_publish(const P2PArgs &p2p, int me, int lane) {
   const int R = p2p.nranks;
   const int set = static_cast<int>(p2p.epoch & 1);
   const unsigned long long *own = reinterpret_cast<const unsigned long long *>(
@@ -1169,6 +1179,14 @@ __device__ bool p2p_exchange(const P2PArgs &p2p, int me, long long *row, unsigne
   __syncwarp();
   // 2. ... before this rank's flag in every mailbox
   if (lane < R) st_release_sys(p2p_flag(p2p.mailbox[lane], R, set, me), p2p.epoch);
+  __syncwarp();
+}
+
+__device__ bool p2p_collect(const P2PArgs &p2p, int me, long long *row, unsigned long long &P,
+                            unsigned long long &M, unsigned long long &N,
+                            unsigned long long &payload, int lane) {
+  const int R = p2p.nranks;
+  const int set = static_cast<int>(p2p.epoch & 1);
   // 3. wait for every rank's flag in the own mailbox (bounded)
   bool ok = true;
   if (lane < R) {
@@ -1328,14 +1346,29 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
     if (!finalize && lane == 0) ws->nan_payload = payload;  // first NaN so far is in this launch
   }
   if (lane == 0) ws->done = 0;
-  if (!finalize) return;
+  if (!finalize) {
+    // Incremental sum (exsum_cuda_accumulate): store the workspace back carried,
+    // so every chunk starts the next launch below 2^32 (the top one: the signed
+    // rest, |c| <= |sum| / 2^1037).  One launch adds < 2^50 per chunk, so any
+    // number of launches stays inside warp_emit's |c| < 2^62 — the device form
+    // of the reference's carry budget (small_accumulator.cpp:174-189), which
+    // lets LargeAccumulator::add(span) run for ever (large_accumulator.cpp:28-32).
+    long long v[3] = {scratch[lane], scratch[lane + 32], lane < 3 ? scratch[lane + 64] : 0};
+    warp_carry(v, lane);
+    ws->chunk[lane] = static_cast<unsigned long long>(v[0]);
+    ws->chunk[lane + 32] = static_cast<unsigned long long>(v[1]);
+    if (lane < 3) ws->chunk[lane + 64] = static_cast<unsigned long long>(v[2]);
+    return;
+  }
   if (p2p.nranks > 0) {
     // this rank's canonical record into its own mailbox slot, then exchange
     const int me = p2p.rank + g;
     warp_emit(scratch, ~s_spec[0], ~s_spec[1], Nf, payload, nullptr,
               p2p_record(p2p.mailbox[me], p2p.nranks, static_cast<int>(p2p.epoch & 1), me), lane);
+    p2p_publish(p2p, me, lane);
+    if (p2p.publish_only) return;
     unsigned long long P = 0, M = 0, N = 0, pay = 0;
-    if (!p2p_exchange(p2p, me, scratch, P, M, N, pay, lane)) {
+    if (!p2p_collect(p2p, me, scratch, P, M, N, pay, lane)) {
       if (lane == 0 && result) *result = __longlong_as_double(0x7FF80000DEAD0000ll);
       return;
     }
@@ -1344,6 +1377,21 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
   }
   warp_emit(scratch, ~s_spec[0], ~s_spec[1], Nf, payload, result, partial, lane);
   EXSUM_STAMP(3);
+}
+
+// The wait + merge half of exsum_p2p_sum for a rank whose sum kernel ran with
+// publish_only: one warp, no data.
+__global__ void exsum_p2p_collect_kernel(const __grid_constant__ P2PArgs p2p, double *result,
+                                         exsum_partial *partial) {
+  __shared__ long long row[kChunks];
+  const int lane = threadIdx.x;
+  unsigned long long P = 0, M = 0, N = 0, pay = 0;
+  if (!p2p_collect(p2p, p2p.rank, row, P, M, N, pay, lane)) {
+    if (lane == 0 && result) *result = __longlong_as_double(0x7FF80000DEAD0000ll);
+    return;
+  }
+  __syncwarp();
+  warp_emit(row, P, M, N, pay, result, partial, lane);
 }
 
 // Finalise a workspace filled by exsum_cuda_accumulate launches.
@@ -1794,12 +1842,30 @@ int exsum_p2p_sum(const double *d_shard, size_t n, uint64_t base_index, int rank
   X.nranks = nranks;
   X.rank = rank;
   X.epoch = epoch;
+  X.publish_only = (flags & EXSUM_P2P_PUBLISH_ONLY) ? 1 : 0;
   for (int r = 0; r < nranks; ++r) {
     if (!mailboxes[r]) return EXSUM_EINVAL;
     X.mailbox[r] = static_cast<unsigned char *>(mailboxes[r]);
   }
   return sum_launch(d_shard, n, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial,
-                    flags, kSum, nullptr, &X);
+                    flags & ~EXSUM_P2P_PUBLISH_ONLY, kSum, nullptr, &X);
+}
+
+int exsum_p2p_collect(int rank, int nranks, void *const *mailboxes, uint64_t epoch,
+                      double *d_result, exsum_partial *d_partial, void *stream) {
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || !mailboxes || epoch == 0)
+    return EXSUM_EINVAL;
+  P2PArgs X = {};
+  X.nranks = nranks;
+  X.rank = rank;
+  X.epoch = epoch;
+  for (int r = 0; r < nranks; ++r) {
+    if (!mailboxes[r]) return EXSUM_EINVAL;
+    X.mailbox[r] = static_cast<unsigned char *>(mailboxes[r]);
+  }
+  exsum_p2p_collect_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(X, d_result,
+                                                                          d_partial);
+  return cudaGetLastError() == cudaSuccess ? EXSUM_OK : EXSUM_ECUDA;
 }
 
 int exsum_p2p_emulate_sum(const double *d_x, const uint64_t *bounds, int nranks, uint64_t epoch,

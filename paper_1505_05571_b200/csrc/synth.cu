@@ -4,9 +4,10 @@
 // PAPER.md:817-826); the configs here are BASELINE.json's.  Each value is a pure
 // function of (config, seed, global index, n_total): shards of a multi-GPU run
 // generate their own slices and the host can regenerate any slice bit-for-bit.
-// Configs 1-4 use only integer arithmetic and correctly rounded IEEE +,*
-// (no FMA contraction), so host and device produce identical bits.  Config 5
-// (normal * 10^k with specials) is generated on the device only.
+// Every config uses only integer arithmetic and correctly rounded IEEE
+// +, -, *, /, sqrt in a fixed order (no FMA contraction, no libm calls on the
+// value path), so host and device produce identical bits; the reference arm of
+// bench.py regenerates the same arrays from oracle/port's C restatement.
 //
 //   1: U[-1,1)                    2: U[0,1)
 //   3: random sign/mantissa, exponent uniform 1..2046 (p=0.99) or 0 (denormal
@@ -14,7 +15,8 @@
 //   4: floor(0.45 n) pairs (x,-x), x = +-10^u, u ~ U[-20,20], then the rest
 //      U[-1e-10,1e-10]; physical order = keyed Feistel bijection of the index
 //   5: N(0,1) * 10^k, k uniform in [-300,300]; P=1e-4 special, split evenly
-//      between +Inf, -Inf and the canonical quiet NaN
+//      between +Inf, -Inf and the canonical quiet NaN (Box-Muller with
+//      fixed-sequence ln / cos, see ln_det, cos2pi_det)
 
 #include <cuda_runtime.h>
 #include <math.h>
@@ -29,9 +31,13 @@
 #if defined(__CUDA_ARCH__)
 #define SYN_ADD(a, b) __dadd_rn((a), (b))
 #define SYN_MUL(a, b) __dmul_rn((a), (b))
+#define SYN_DIV(a, b) __ddiv_rn((a), (b))
+#define SYN_SQRT(a) __dsqrt_rn(a)
 #else
 #define SYN_ADD(a, b) ((a) + (b))
 #define SYN_MUL(a, b) ((a) * (b))
+#define SYN_DIV(a, b) ((a) / (b))
+#define SYN_SQRT(a) sqrt(a)
 #endif
 
 namespace {
@@ -127,6 +133,74 @@ __host__ __device__ __forceinline__ double config4_logical(uint64_t seed, uint64
   return SYN_MUL(SYN_ADD(SYN_MUL(u, 2.0), -1.0), 1e-10);
 }
 
+
+// ln(u) for a normal u > 0: u = m 2^e with m in [sqrt(1/2), sqrt(2)), then
+// ln m = 2 atanh(s), s = (m-1)/(m+1), |s| < 0.172, series to s^21.
+__host__ __device__ __forceinline__ double ln_det(double u) {
+  const uint64_t b = double_to_bits(u);
+  int e = static_cast<int>((b >> 52) & 0x7FF) - 1023;
+  double m = bits_to_double((b & 0x000FFFFFFFFFFFFFull) | 0x3FF0000000000000ull);
+  if (m > 1.4142135623730951) {
+    m = SYN_MUL(m, 0.5);
+    ++e;
+  }
+  const double s = SYN_DIV(SYN_ADD(m, -1.0), SYN_ADD(m, 1.0));
+  const double s2 = SYN_MUL(s, s);
+  double p = 1.0 / 21.0;
+  const double inv[10] = {1.0 / 19.0, 1.0 / 17.0, 1.0 / 15.0, 1.0 / 13.0, 1.0 / 11.0,
+                          1.0 / 9.0,  1.0 / 7.0,  1.0 / 5.0,  1.0 / 3.0,  1.0};
+  for (int i = 0; i < 10; ++i) p = SYN_ADD(SYN_MUL(p, s2), inv[i]);
+  return SYN_ADD(SYN_MUL(static_cast<double>(e), 0.6931471805599453),
+                 SYN_MUL(SYN_MUL(s, p), 2.0));
+}
+
+// cos(2 pi u) for u in [0, 1): quadrant from 4u, Taylor cos/sin on [0, pi/2].
+__host__ __device__ __forceinline__ double cos2pi_det(double u) {
+  const double t = SYN_MUL(u, 4.0);  // exact
+  const int q = static_cast<int>(t);
+  const double a = SYN_MUL(SYN_ADD(t, -static_cast<double>(q)), 1.5707963267948966);
+  const double a2 = SYN_MUL(a, a);
+  // cos: sum (-1)^k a^2k / (2k)!, k <= 10; sin: a * sum (-1)^k a^2k / (2k+1)!, k <= 10
+  const double ci[11] = {1.0 / 2432902008176640000.0, -1.0 / 6402373705728000.0,
+                         1.0 / 20922789888000.0,      -1.0 / 87178291200.0,
+                         1.0 / 479001600.0,           -1.0 / 3628800.0,
+                         1.0 / 40320.0,               -1.0 / 720.0,
+                         1.0 / 24.0,                  -0.5,
+                         1.0};
+  const double si[11] = {1.0 / 51090942171709440000.0, -1.0 / 121645100408832000.0,
+                         1.0 / 355687428096000.0,      -1.0 / 1307674368000.0,
+                         1.0 / 6227020800.0,           -1.0 / 39916800.0,
+                         1.0 / 362880.0,               -1.0 / 5040.0,
+                         1.0 / 120.0,                  -1.0 / 6.0,
+                         1.0};
+  double c = ci[0], s = si[0];
+  for (int i = 1; i < 11; ++i) {
+    c = SYN_ADD(SYN_MUL(c, a2), ci[i]);
+    s = SYN_ADD(SYN_MUL(s, a2), si[i]);
+  }
+  s = SYN_MUL(s, a);
+  return q == 0 ? c : q == 1 ? -s : q == 2 ? -c : s;
+}
+
+// Config 5 value at global index i: P = 1e-4 special (+Inf, -Inf, canonical
+// qNaN equally), else Box-Muller N(0,1) times 10^k, k uniform in [-300, 300];
+// pow10[k + 300] is the correctly rounded 10^k.
+__host__ __device__ __forceinline__ double config5_value(uint64_t seed, uint64_t i,
+                                                         const double *pow10) {
+  const uint64_t h = draw(seed, 51, i);
+  if ((h >> 11) < 900719925474ull) {  // 1e-4 * 2^53
+    const uint64_t kind = draw(seed, 52, i) % 3;
+    return bits_to_double(kind == 0 ? 0x7FF0000000000000ull
+                                    : kind == 1 ? 0xFFF0000000000000ull : 0x7FF8000000000000ull);
+  }
+  const double u1 = SYN_MUL(static_cast<double>((draw(seed, 53, i) >> 11) + 1), 0x1.0p-53);
+  const double u2 = unit(draw(seed, 54, i));
+  const double r = SYN_SQRT(SYN_MUL(ln_det(u1), -2.0));
+  const double z = SYN_MUL(r, cos2pi_det(u2));
+  const int k = static_cast<int>(draw(seed, 55, i) % 601);
+  return SYN_MUL(z, pow10[k]);
+}
+
 __host__ __device__ __forceinline__ double gen_value(int config, uint64_t seed, uint64_t n,
                                                      uint64_t i) {
   switch (config) {
@@ -168,23 +242,22 @@ __constant__ double c_pow10[601];
 __global__ void gen5_kernel(uint64_t seed, uint64_t first, uint64_t count, double *out) {
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < count;
-       t += stride) {
-    const uint64_t i = first + t;
-    const uint64_t h = draw(seed, 51, i);
-    double v;
-    if ((h >> 11) < 900719925474ull) {  // 1e-4 * 2^53
-      const uint64_t kind = draw(seed, 52, i) % 3;
-      v = bits_to_double(kind == 0 ? 0x7FF0000000000000ull
-                                   : kind == 1 ? 0xFFF0000000000000ull : 0x7FF8000000000000ull);
-    } else {
-      const double u1 = (static_cast<double>(draw(seed, 53, i) >> 11) + 1.0) * 0x1.0p-53;
-      const double u2 = unit(draw(seed, 54, i));
-      const double z = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
-      const int k = static_cast<int>(draw(seed, 55, i) % 601);
-      v = z * c_pow10[k];
+       t += stride)
+    out[t] = config5_value(seed, first + t, c_pow10);
+}
+
+// 10^k, k in [-300, 300], correctly rounded (strtod), host copy.
+const double *pow10_table() {
+  static double p[601];
+  static std::once_flag once;
+  std::call_once(once, [] {
+    char buf[16];
+    for (int k = -300; k <= 300; ++k) {
+      snprintf(buf, sizeof buf, "1e%d", k);
+      p[k + 300] = strtod(buf, nullptr);
     }
-    out[t] = v;
-  }
+  });
+  return p;
 }
 
 unsigned gen_grid(uint64_t count) {
@@ -232,6 +305,15 @@ int exsum_host_gen_offsets(uint64_t seed, size_t nseg, uint64_t lo, uint64_t hi,
   return EXSUM_OK;
 }
 
+int exsum_host_gen_segmented(uint64_t seed, uint64_t first, size_t count, double *out) {
+  if (count && !out) return EXSUM_EINVAL;
+  const double *p = pow10_table();
+#pragma omp parallel for schedule(static)
+  for (long long t = 0; t < static_cast<long long>(count); ++t)
+    out[t] = config5_value(seed, first + static_cast<uint64_t>(t), p);
+  return EXSUM_OK;
+}
+
 int exsum_cuda_gen_segmented(uint64_t seed, uint64_t first, size_t count, double *d_out,
                              void *stream) {
   if (count && !d_out) return EXSUM_EINVAL;
@@ -243,13 +325,8 @@ int exsum_cuda_gen_segmented(uint64_t seed, uint64_t first, size_t count, double
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return EXSUM_ECUDA;
     std::lock_guard<std::mutex> lock(m);
     if (!ready[dev]) {
-      double p[601];
-      char buf[16];
-      for (int k = -300; k <= 300; ++k) {
-        snprintf(buf, sizeof buf, "1e%d", k);
-        p[k + 300] = strtod(buf, nullptr);  // correctly rounded
-      }
-      if (cudaMemcpyToSymbol(c_pow10, p, sizeof p) != cudaSuccess) return EXSUM_ECUDA;
+      if (cudaMemcpyToSymbol(c_pow10, pow10_table(), 601 * sizeof(double)) != cudaSuccess)
+        return EXSUM_ECUDA;
       ready[dev] = true;
     }
   }

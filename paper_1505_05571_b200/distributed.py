@@ -27,7 +27,7 @@ from ._lib import ExsumPartial
 from .ops import PARTIAL_BYTES, exact_sum_tensor, merge_partials, partial_from_tensor
 
 __all__ = ["shard_bounds", "exchange_partials", "merge_records", "parallel_exact_sum",
-           "NcclCommunicator", "nccl_exact_sum", "P2PGroup", "p2p_exact_sum"]
+           "NcclCommunicator", "nccl_exact_sum", "P2PGroup", "p2p_exact_sum", "p2p_collect"]
 
 
 def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -138,9 +138,10 @@ def nccl_exact_sum(shard: torch.Tensor, comm: NcclCommunicator, *, base_index: i
     if result is None:
         result = torch.empty(1, dtype=torch.float64, device=x.device)
     stream = torch.cuda.current_stream(x.device).cuda_stream
-    _lib.call("exsum_nccl_sum", x.data_ptr() if x.numel() else None, x.numel(), base_index,
-              comm.comm, result.data_ptr(), record.data_ptr() if record is not None else None,
-              comm.workspace.data_ptr(), comm.workspace.numel(), stream, 1 if overlap else 0)
+    with torch.cuda.device(x.device):
+        _lib.call("exsum_nccl_sum", x.data_ptr() if x.numel() else None, x.numel(), base_index,
+                  comm.comm, result.data_ptr(), record.data_ptr() if record is not None else None,
+                  comm.workspace.data_ptr(), comm.workspace.numel(), stream, 1 if overlap else 0)
     return result
 
 
@@ -220,9 +221,12 @@ class P2PGroup:
 
 def p2p_exact_sum(shard: torch.Tensor, grp: P2PGroup, *, base_index: int,
                   result: torch.Tensor | None = None,
-                  record: torch.Tensor | None = None, overlap: bool = False) -> torch.Tensor:
+                  record: torch.Tensor | None = None, overlap: bool = False,
+                  publish_only: bool = False) -> torch.Tensor:
     """exsum_p2p_sum: one launch per rank — shard sum, record exchange over
-    peer memory, merge.  Every rank gets the full array's exact sum."""
+    peer memory, merge.  Every rank gets the full array's exact sum.
+    ``publish_only``: sum and publish this rank's record, return without the
+    wait/merge — finish with p2p_collect (ranks run one after another)."""
     if not shard.is_cuda or shard.dtype != torch.float64:
         raise ValueError("p2p_exact_sum: shard must be a CUDA float64 tensor")
     x = shard.contiguous()
@@ -230,9 +234,23 @@ def p2p_exact_sum(shard: torch.Tensor, grp: P2PGroup, *, base_index: int,
         result = torch.empty(1, dtype=torch.float64, device=x.device)
     grp.epoch += 1
     ptrs = (C.c_void_p * grp.world)(*grp.ptrs)
-    _lib.call("exsum_p2p_sum", x.data_ptr() if x.numel() else None, x.numel(), base_index,
-              grp.rank, grp.world, ptrs, grp.epoch, result.data_ptr(),
-              record.data_ptr() if record is not None else None, grp.workspace.data_ptr(),
-              grp.workspace.numel(), torch.cuda.current_stream(x.device).cuda_stream,
-              1 if overlap else 0)
+    flags = (1 if overlap else 0) | (2 if publish_only else 0)
+    with torch.cuda.device(x.device):
+        _lib.call("exsum_p2p_sum", x.data_ptr() if x.numel() else None, x.numel(), base_index,
+                  grp.rank, grp.world, ptrs, grp.epoch, result.data_ptr(),
+                  record.data_ptr() if record is not None else None, grp.workspace.data_ptr(),
+                  grp.workspace.numel(), torch.cuda.current_stream(x.device).cuda_stream, flags)
+    return result
+
+
+def p2p_collect(grp: P2PGroup, *, result: torch.Tensor | None = None,
+                record: torch.Tensor | None = None) -> torch.Tensor:
+    """exsum_p2p_collect: the wait + merge of this rank's last publish_only call."""
+    if result is None:
+        result = torch.empty(1, dtype=torch.float64, device=grp.device)
+    ptrs = (C.c_void_p * grp.world)(*grp.ptrs)
+    with torch.cuda.device(grp.device):
+        _lib.call("exsum_p2p_collect", grp.rank, grp.world, ptrs, grp.epoch, result.data_ptr(),
+                  record.data_ptr() if record is not None else None,
+                  torch.cuda.current_stream(grp.device).cuda_stream)
     return result

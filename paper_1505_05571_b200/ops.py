@@ -125,9 +125,10 @@ def exact_sum_tensor(x: torch.Tensor, *, base_index: int = 0, result: torch.Tens
         result = torch.empty(1, dtype=torch.float64, device=dev)
     if partial is None:
         partial = torch.empty(PARTIAL_BYTES, dtype=torch.uint8, device=dev)
-    _lib.call("exsum_cuda_sum_ex", x.data_ptr(), x.numel(), base_index, result.data_ptr(),
-              partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev),
-              1 if overlap else 0)
+    with torch.cuda.device(dev):
+        _lib.call("exsum_cuda_sum_ex", x.data_ptr(), x.numel(), base_index, result.data_ptr(),
+                  partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev),
+                  1 if overlap else 0)
     return result, partial
 
 
@@ -143,8 +144,9 @@ def exact_sqnorm_tensor(x: torch.Tensor, *, base_index: int = 0,
     ws = workspace or _workspace(dev)
     result = torch.empty(1, dtype=torch.float64, device=dev) if result is None else result
     partial = torch.empty(PARTIAL_BYTES, dtype=torch.uint8, device=dev) if partial is None else partial
-    _lib.call("exsum_cuda_sqnorm", x.data_ptr(), x.numel(), base_index, result.data_ptr(),
-              partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev))
+    with torch.cuda.device(dev):
+        _lib.call("exsum_cuda_sqnorm", x.data_ptr(), x.numel(), base_index, result.data_ptr(),
+                  partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev))
     return result, partial
 
 
@@ -163,8 +165,9 @@ def exact_dot_tensor(a: torch.Tensor, b: torch.Tensor, *, base_index: int = 0,
     ws = workspace or _workspace(dev)
     result = torch.empty(1, dtype=torch.float64, device=dev) if result is None else result
     partial = torch.empty(PARTIAL_BYTES, dtype=torch.uint8, device=dev) if partial is None else partial
-    _lib.call("exsum_cuda_dot", a.data_ptr(), a.numel(), b.data_ptr(), b.numel(), base_index,
-              result.data_ptr(), partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev))
+    with torch.cuda.device(dev):
+        _lib.call("exsum_cuda_dot", a.data_ptr(), a.numel(), b.data_ptr(), b.numel(), base_index,
+                  result.data_ptr(), partial.data_ptr(), ws.ptr, WORKSPACE_BYTES, _stream_handle(dev))
     return result, partial
 
 
@@ -223,13 +226,22 @@ def exact_sum_file(path, fmt: str = "bin", *, device: int = 0) -> float:
 
 
 class HostContext:
-    """exsum_context: device workspace + staging ring for host-resident arrays."""
+    """exsum_context: the exact sum of host-resident arrays on the device and the
+    host cores together (device staging ring + host worker pool).
 
-    def __init__(self, device: int = 0, staging_bytes: int = 256 << 20):
+    ``host_threads``: host workers beside the device (-1: every hardware thread,
+    the library default; 0: device only).  One sum at a time per context — the
+    C library serialises calls on a context, and this wrapper also holds a lock
+    so Python threads sharing a context cannot interleave.
+    """
+
+    def __init__(self, device: int = 0, staging_bytes: int = 192 << 20, host_threads: int = -1):
         self.device = device
+        self._lock = threading.Lock()
         self._h = lib.exsum_context_create(device, staging_bytes)
         if not self._h:
             raise _lib.ExsumError("exsum_context_create", _lib.EXSUM_ECUDA)
+        self.set_host_threads(host_threads)
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -237,29 +249,45 @@ class HostContext:
             lib.exsum_context_free(h)
             self._h = None
 
+    def set_host_threads(self, threads: int) -> None:
+        with self._lock:
+            _lib.call("exsum_context_set_host_threads", self._h, int(threads))
+
+    def last_split(self) -> tuple[int, int]:
+        """(device terms, host terms) of the last sum."""
+        d, h = C.c_uint64(), C.c_uint64()
+        _lib.call("exsum_context_last_split", self._h, C.byref(d), C.byref(h))
+        return d.value, h.value
+
     def sum(self, values, want_partial: bool = False, base_index: int = 0):
         """exact_sum of a host array (exsum_context_sum_at); base_index = global
-        index of values[0] for the record's Inf/NaN indices."""
+        index of values[0] for the record's Inf/NaN indices.  The array is
+        flattened (all elements are summed)."""
         a = values.numpy() if isinstance(values, torch.Tensor) else values
         a = np.ascontiguousarray(a, dtype=np.float64).reshape(-1)
         out = C.c_double()
         part = ExsumPartial()
-        _lib.call("exsum_context_sum_at", self._h, a.ctypes.data, a.size, base_index,
-                  C.byref(out), C.byref(part) if want_partial else None)
+        with self._lock:
+            _lib.call("exsum_context_sum_at", self._h, a.ctypes.data, a.size, base_index,
+                      C.byref(out), C.byref(part) if want_partial else None)
         return (out.value, part) if want_partial else out.value
 
-    def sum_ptr(self, ptr: int, n: int) -> float:
+    def sum_ptr(self, ptr: int, n: int, want_partial: bool = False, base_index: int = 0):
         out = C.c_double()
-        _lib.call("exsum_context_sum", self._h, ptr, n, C.byref(out), None)
-        return out.value
+        part = ExsumPartial()
+        with self._lock:
+            _lib.call("exsum_context_sum_at", self._h, ptr, n, base_index, C.byref(out),
+                      C.byref(part) if want_partial else None)
+        return (out.value, part) if want_partial else out.value
 
     def sum_file(self, path, fmt: str = "bin", want_partial: bool = False):
         """exact_sum(read_values(path, fmt)) — a bin file streams from disk through
         pinned buffers into the device accumulate.  Returns (result, n[, partial])."""
         out, n = C.c_double(), C.c_uint64()
         part = ExsumPartial()
-        _lib.call("exsum_context_sum_file", self._h, str(path).encode(), _format(fmt),
-                  C.byref(out), C.byref(part) if want_partial else None, C.byref(n))
+        with self._lock:
+            _lib.call("exsum_context_sum_file", self._h, str(path).encode(), _format(fmt),
+                      C.byref(out), C.byref(part) if want_partial else None, C.byref(n))
         return (out.value, n.value, part) if want_partial else (out.value, n.value)
 
 
@@ -301,7 +329,7 @@ def exact_mean(values, method: str = "large") -> float:
     (SmallAccumulator::mean, small_accumulator.cpp:350-421).
     """
     _check_method(method)
-    n = values.numel() if isinstance(values, torch.Tensor) else len(values)
+    n = values.numel() if isinstance(values, torch.Tensor) else int(np.asarray(values).size)
     if n == 0:
         raise ValueError("exact_mean: empty input")
     if isinstance(values, torch.Tensor) and values.is_cuda:
@@ -341,9 +369,10 @@ def exact_sum_segmented(x: torch.Tensor, offsets: torch.Tensor, *,
     if nseg <= 0:
         return (out, parts) if partials else out
     ws = workspace or _segmented_workspace(dev, nseg)
-    _lib.call("exsum_cuda_sum_segmented", x.data_ptr(), offsets.data_ptr(), nseg,
-              out.data_ptr(), parts.data_ptr() if partials else None, ws.ptr,
-              ws.nbytes if longest_first else WORKSPACE_BYTES, _stream_handle(dev))
+    with torch.cuda.device(dev):
+        _lib.call("exsum_cuda_sum_segmented", x.data_ptr(), offsets.data_ptr(), nseg,
+                  out.data_ptr(), parts.data_ptr() if partials else None, ws.ptr,
+                  ws.nbytes if longest_first else WORKSPACE_BYTES, _stream_handle(dev))
     return (out, parts) if partials else out
 
 
@@ -359,8 +388,9 @@ def merge_partials(parts: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
     dev = parts.device
     result = torch.empty(1, dtype=torch.float64, device=dev)
     out = torch.empty(PARTIAL_BYTES, dtype=torch.uint8, device=dev)
-    _lib.call("exsum_cuda_merge", parts.data_ptr(), parts.shape[0], result.data_ptr(),
-              out.data_ptr(), _stream_handle(dev))
+    with torch.cuda.device(dev):
+        _lib.call("exsum_cuda_merge", parts.data_ptr(), parts.shape[0], result.data_ptr(),
+                  out.data_ptr(), _stream_handle(dev))
     return result, out
 
 

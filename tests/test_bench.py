@@ -26,11 +26,30 @@ def test_reference_arm_line():
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] == line["value"]
     assert line["e2e"] == {"value": line["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
-    assert line["config"]["workload"].startswith("config2")
+    assert line["config"]["workload"].startswith("config4")  # the default workload
+    assert line["config"]["n_total"] == 200_000
+
+
+def test_reference_arm_does_not_load_the_product():
+    """The reference arm must time the reference only: its inputs come from
+    oracle/port, so libexsum_b200.so is never mapped into that process."""
+    from oracle import ref as R
+    if not R.available():
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    code = ("import sys, runpy; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', "
+            "'--warmup', '3', '--n', '{n}', '--config', '{c}']; "
+            "runpy.run_path('bench.py', run_name='__main__'); "
+            "maps = open('/proc/self/maps').read(); "
+            "print('PRODUCT_LOADED' if 'libexsum_b200' in maps else 'CLEAN')")
+    for c, n in ((2, "1e5"), (4, "1e5"), (5, "64")):
+        out = subprocess.run([sys.executable, "-c", code.format(c=c, n=n)], capture_output=True,
+                             text=True, timeout=600, cwd=ROOT)
+        assert out.returncode == 0, out.stderr[-2000:]
+        assert out.stdout.strip().splitlines()[-1] == "CLEAN", c
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("config", [2, 5])
+@pytest.mark.parametrize("config", [2, 4, 5])
 def test_device_arm_line(config):
     """bench.py's own arm at a reduced size: every contract key, a bit-exact
     result and a positive roofline fraction."""
@@ -39,7 +58,7 @@ def test_device_arm_line(config):
         pytest.skip("no CUDA device")
     args = [sys.executable, str(ROOT / "bench.py"), "--config", str(config), "--steps", "5",
             "--warmup", "3"]
-    args += ["--n", "1e7"] if config == 2 else ["--no-cpu-baseline"]
+    args += {2: ["--n", "1e7"], 4: ["--n", "3e7"], 5: ["--no-cpu-baseline", "--n", "4096"]}[config]
     out = subprocess.run(args, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     line = json.loads(out.stdout.strip().splitlines()[-1])
@@ -52,6 +71,11 @@ def test_device_arm_line(config):
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 2
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["value"] > 0
     assert "workload" in line["config"]
-    if config == 2:  # the CPU leg also checks the device result against the reference
+    # the reference arm on the same arguments reports the identical config dict
+    ref = subprocess.run([a for a in args if a != "--no-cpu-baseline"] + ["--impl", "reference"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert ref.returncode == 0, ref.stderr[-2000:]
+    assert json.loads(ref.stdout.strip().splitlines()[-1])["config"] == line["config"]
+    if config in (2, 4):  # the CPU leg also checks the device result against the reference
         assert line["bit_exact_vs_oracle"] is True
         assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] > 0
