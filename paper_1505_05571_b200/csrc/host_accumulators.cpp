@@ -243,6 +243,13 @@ int exsum_small_add(exsum_small *acc, double v) {
   return EXSUM_OK;
 }
 
+// add(span) (small_accumulator.cpp:174-189): the same runs between
+// propagations, but each run is summed branch-free (sign applied as
+// (v ^ s) - s, no mispredicted sign branch on mixed-sign data) into two local
+// chunk arrays taken alternately (no store-to-load chain through the same
+// chunk on consecutive terms), then added to the accumulator.  Integer adds
+// are associative and a run stays within the 2047-add budget, so the chunk
+// values after every call equal the reference's sequential adds exactly.
 int exsum_small_add_array(exsum_small *acc, const double *x, size_t n) {
   if (!acc || (n && !x)) return EXSUM_EINVAL;
   size_t i = 0;
@@ -250,7 +257,31 @@ int exsum_small_add_array(exsum_small *acc, const double *x, size_t n) {
     if (acc->adds_until_propagate <= 0) small_propagate(acc);
     size_t run = static_cast<size_t>(acc->adds_until_propagate);
     if (run > n - i) run = n - i;
-    for (size_t j = 0; j < run; ++j) small_add_term(acc, bits_of(x[i + j]));
+    int64_t c[2][kChunks + 1] = {};
+    for (size_t j = 0; j < run; ++j) {
+      const uint64_t bits = bits_of(x[i + j]);
+      const uint32_t e = static_cast<uint32_t>(bits >> kMantBits) & 0x7FFu;
+      uint64_t m = bits & kMantMask;
+      uint32_t ee = e;
+      if (__builtin_expect(e - 1u >= 0x7FEu, 0)) {  // e == 0 or e == 0x7FF
+        if (e == 0x7FFu) {
+          small_special(acc, bits);
+          continue;
+        }
+        if (m == 0) continue;
+        ee = 1;
+      } else {
+        m |= uint64_t{1} << kMantBits;
+      }
+      const uint32_t sh = ee & 31u, ix = ee >> 5;
+      const int64_t s = static_cast<int64_t>(bits) >> 63;  // 0 or -1
+      const int64_t low = static_cast<int64_t>((m << sh) & 0xFFFFFFFFull);
+      const int64_t high = static_cast<int64_t>(m >> (32u - sh));
+      int64_t *cj = c[j & 1];
+      cj[ix] += (low ^ s) - s;
+      cj[ix + 1] += (high ^ s) - s;
+    }
+    for (int k = 0; k < kChunks; ++k) acc->chunk[k] += c[0][k] + c[1][k];
     acc->adds_until_propagate -= static_cast<int32_t>(run);  // budget per element
     i += run;
   }

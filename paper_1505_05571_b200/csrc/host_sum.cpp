@@ -24,10 +24,10 @@
 //              transferred with its carry bit 2^64 — exact, no countdown.
 //   per term:  load, shift, and, or, add-to-memory, never-taken jc.
 //
-// Zeros, denormals, Inf and NaN are screened eight terms at a time (one
-// exponent-field test per group); a group containing any takes a careful
-// per-term path (denormals without the implicit bit, specials recorded by first
-// global index, exactly like the device kernels' side channel).
+// Zeros and denormals go through the same blind add (their wrongly added
+// implicit bits are removed by one counted correction per block); Inf and NaN
+// land in two sentinel bins that send their block through a per-term pass
+// (first global index, exactly like the device kernels' side channel).
 //
 // Bins drain into a 67-chunk small superaccumulator (chunk i weighs
 // 2^(32 i - 1075), small_accumulator.hpp:27-35) as three 32-bit pieces, the
@@ -94,71 +94,53 @@ __attribute__((noinline)) void Acc::transfer(uint32_t ix, uint64_t v, uint64_t c
   }
 }
 
-inline void Acc::add_sig(uint32_t ix, uint64_t sig) {
-  uint64_t s;
-  if (__builtin_expect(__builtin_add_overflow(bin[0][ix], sig, &s), 0)) {
-    transfer(ix, s, 1);
-    s = 0;
-  }
-  bin[0][ix] = s;
-}
-
-// The block's zeros, denormals, Inf and NaN (exponent field 0 or 0x7FF), after
-// the blind pass put them into the sentinel bins: denormals go to the bin of
-// exponent 1 (same weight, no implicit bit), specials to the first-index record.
-// Groups of eight are screened with one vector test (1% denormals -> ~8% of
-// groups need the per-term look).
 namespace {
 
-// flags[g] = 1 iff group g (terms 8g .. 8g+7) holds an exponent field of 0 or 0x7FF:
-// ((b + 2^52) & exp) < 2^53  <=>  e in {0x7FF, 0}.
-__attribute__((target("avx512f"))) void odd_groups_avx512(const uint64_t *b, size_t ngroups,
-                                                           uint8_t *flags) {
-  const __m512i one = _mm512_set1_epi64(static_cast<long long>(kImplicit));
+// Zero-exponent terms (+-0, denormals) of a block, per sign: they were added
+// blindly with an implicit 2^52 each.
+struct ZeroExp {
+  uint64_t pos, neg;
+};
+
+__attribute__((target("avx512f,avx512vpopcntdq"))) ZeroExp zero_exp_avx512(const uint64_t *b,
+                                                                            size_t n) {
   const __m512i ef = _mm512_set1_epi64(static_cast<long long>(kExpField));
-  const __m512i lim = _mm512_set1_epi64(static_cast<long long>((kImplicit << 1) - 1));
-  for (size_t g = 0; g < ngroups; ++g) {
-    const __m512i v = _mm512_loadu_si512(b + 8 * g);
-    const __m512i t = _mm512_and_si512(_mm512_add_epi64(v, one), ef);
-    flags[g] = _mm512_cmple_epu64_mask(t, lim) != 0;
+  const __m512i sg = _mm512_set1_epi64(static_cast<long long>(kSignMask));
+  uint64_t pos = 0, neg = 0;
+  size_t k = 0;
+  for (; k + 8 <= n; k += 8) {
+    const __m512i v = _mm512_loadu_si512(b + k);
+    const __mmask8 z = _mm512_testn_epi64_mask(v, ef);  // exponent field == 0
+    const __mmask8 s = _mm512_test_epi64_mask(v, sg);
+    pos += static_cast<uint64_t>(__builtin_popcount(z & static_cast<__mmask8>(~s)));
+    neg += static_cast<uint64_t>(__builtin_popcount(z & s));
   }
+  for (; k < n; ++k)
+    if ((b[k] & kExpField) == 0) (b[k] >> 63 ? neg : pos) += 1;
+  return {pos, neg};
 }
 
-void odd_groups_scalar(const uint64_t *b, size_t ngroups, uint8_t *flags) {
-  for (size_t g = 0; g < ngroups; ++g) {
-    bool odd = false;
-    for (int k = 0; k < 8; ++k) odd |= ((b[8 * g + k] + kImplicit) & kExpField) < (kImplicit << 1);
-    flags[g] = odd;
-  }
+ZeroExp zero_exp_scalar(const uint64_t *b, size_t n) {
+  uint64_t pos = 0, neg = 0;
+  for (size_t k = 0; k < n; ++k)
+    if ((b[k] & kExpField) == 0) (b[k] >> 63 ? neg : pos) += 1;
+  return {pos, neg};
 }
 
-const bool kHaveAvx512 = __builtin_cpu_supports("avx512f");
+const bool kHaveAvx512 =
+    __builtin_cpu_supports("avx512f") && __builtin_cpu_supports("avx512vpopcntdq");
 
 }  // namespace
 
-__attribute__((noinline)) void Acc::rescan(const uint64_t *b, size_t n, uint64_t gbase) {
-  for (int c = 0; c < kCopies; ++c)
-    bin[c][0] = bin[c][0x800] = bin[c][0x7FF] = bin[c][0xFFF] = 0;
-  uint8_t flags[kBlock / 8];
-  const size_t ng = n / 8;
-  if (kHaveAvx512)
-    odd_groups_avx512(b, ng, flags);
-  else
-    odd_groups_scalar(b, ng, flags);
+// The block's Inf and NaN (exponent field 0x7FF) after the blind pass put them
+// into the sentinel bins 0x7FF / 0xFFF: clear those, record first indices.
+__attribute__((noinline)) void Acc::specials(const uint64_t *b, size_t n, uint64_t gbase) {
+  for (int c = 0; c < kCopies; ++c) bin[c][0x7FF] = bin[c][0xFFF] = 0;
   for (size_t k = 0; k < n; ++k) {
-    if (k < 8 * ng && !flags[k / 8]) {
-      k |= 7;  // skip the rest of a clean group
-      continue;
-    }
     const uint64_t v = b[k];
-    if (((v + kImplicit) & kExpField) >= (kImplicit << 1)) continue;  // normal
-    const uint64_t m = v & kMantMask;
-    if ((v & kExpField) == 0) {
-      if (m) add_sig(static_cast<uint32_t>(v >> kMantBits) | 1u, m);
-      continue;
-    }
+    if ((v & kExpField) != kExpField) continue;
     const uint64_t gi = gbase + k;
-    if (m) {
+    if (v & kMantMask) {
       if (gi < N) {
         N = gi;
         payload = v;
@@ -171,25 +153,49 @@ __attribute__((noinline)) void Acc::rescan(const uint64_t *b, size_t n, uint64_t
   }
 }
 
+// Implicit bits wrongly added for the block's zero-exponent terms: remove them
+// exactly as a transfer of -k 2^52 at exponent 1 (the weight of bins 0x000 /
+// 0x800 and of denormals), whatever the bins did meanwhile (carries included).
+__attribute__((noinline)) void Acc::zero_exponents(const uint64_t *b, size_t n) {
+  const ZeroExp z = kHaveAvx512 ? zero_exp_avx512(b, n) : zero_exp_scalar(b, n);
+  if (z.pos) transfer(0x800u, z.pos << kMantBits, 0);  // minus k 2^52 of positive terms
+  if (z.neg) transfer(0x000u, z.neg << kMantBits, 0);  // plus k 2^52 of negative terms
+}
+
+#ifndef EXSUM_HOST_PREFETCH
+#define EXSUM_HOST_PREFETCH 0  // software prefetch distance in terms (0: hardware only)
+#endif
+
 // Blind pass: every term's significand (mantissa | implicit bit) is added to
 // bin copy (k mod kCopies) of its sign+exponent index — no per-term test for
-// zeros, denormals or specials.  Those all have exponent field 0 or 0x7FF, so
-// they can only land in the four sentinel indices 0x000, 0x800, 0x7FF, 0xFFF,
-// which hold nothing else; a block of <= 2^10 terms cannot wrap a sentinel
-// bin.  After each block one test of the sentinels routes the rare block that
-// touched them through rescan().  The copies break the store-to-load chain
-// when consecutive terms share an exponent (U[0,1): half the terms in one bin).
+// zeros, denormals or specials.  Afterwards, once per block:
+//   * bins 0x000 / 0x800 changed -> the block held zero-exponent terms: the
+//     wrongly added implicit bits are removed by a counted correction
+//     (zero_exponents; the denormals' mantissas are already in the right bin);
+//   * sentinel bins 0x7FF / 0xFFF nonzero -> Inf/NaN in the block (specials);
+//     they hold nothing else, and a block of <= 2^10 terms cannot wrap them.
+// The copies break the store-to-load chain when consecutive terms share an
+// exponent (U[0,1): half the terms in one bin).
 void Acc::add(const double *x, size_t n, uint64_t gbase) {
   const uint64_t *b = reinterpret_cast<const uint64_t *>(x);
   size_t i = 0;
   while (i < n) {
     const size_t len = n - i < kBlock ? n - i : kBlock;
     const uint64_t *blk = b + i;
+    uint64_t z0[kCopies], z8[kCopies];
+    for (int c = 0; c < kCopies; ++c) {
+      z0[c] = bin[c][0];
+      z8[c] = bin[c][0x800];
+    }
     size_t k = 0;
-    for (; k + kCopies <= len; k += kCopies) {
+    for (; k + 8 <= len; k += 8) {
+#if EXSUM_HOST_PREFETCH
+      __builtin_prefetch(blk + k + EXSUM_HOST_PREFETCH, 0, 0);
+#endif
 #pragma GCC unroll 8
-      for (int c = 0; c < kCopies; ++c) {
-        const uint64_t v = blk[k + c];
+      for (int j = 0; j < 8; ++j) {
+        const int c = j % kCopies;
+        const uint64_t v = blk[k + j];
         const uint64_t ix = v >> kMantBits;
         uint64_t s;
         if (__builtin_expect(
@@ -210,10 +216,13 @@ void Acc::add(const double *x, size_t n, uint64_t gbase) {
       }
       bin[0][ix] = s;
     }
-    uint64_t sentinel = 0;
-    for (int c = 0; c < kCopies; ++c)
-      sentinel |= bin[c][0] | bin[c][0x800] | bin[c][0x7FF] | bin[c][0xFFF];
-    if (__builtin_expect(sentinel != 0, 0)) rescan(blk, len, gbase + i);
+    uint64_t zchg = 0, sentinel = 0;
+    for (int c = 0; c < kCopies; ++c) {
+      zchg |= (bin[c][0] ^ z0[c]) | (bin[c][0x800] ^ z8[c]);
+      sentinel |= bin[c][0x7FF] | bin[c][0xFFF];
+    }
+    if (__builtin_expect(zchg != 0, 0)) zero_exponents(blk, len);
+    if (__builtin_expect(sentinel != 0, 0)) specials(blk, len, gbase + i);
     i += len;
   }
   terms += n;

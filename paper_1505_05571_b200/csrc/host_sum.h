@@ -37,8 +37,8 @@ struct alignas(64) Acc {
 
  private:
   void transfer(uint32_t ix, uint64_t v, uint64_t carry);
-  void add_sig(uint32_t ix, uint64_t sig);
-  void rescan(const uint64_t *b, size_t n, uint64_t gbase);
+  void specials(const uint64_t *b, size_t n, uint64_t gbase);
+  void zero_exponents(const uint64_t *b, size_t n);
 };
 
 int default_threads();
