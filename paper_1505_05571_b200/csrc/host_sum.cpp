@@ -163,7 +163,7 @@ __attribute__((noinline)) void Acc::zero_exponents(const uint64_t *b, size_t n) 
 }
 
 #ifndef EXSUM_HOST_PREFETCH
-#define EXSUM_HOST_PREFETCH 0  // software prefetch distance in terms (0: hardware only)
+#define EXSUM_HOST_PREFETCH 512  // software prefetch distance in terms (4 KB; 0: hardware only)
 #endif
 
 // Blind pass: every term's significand (mantissa | implicit bit) is added to

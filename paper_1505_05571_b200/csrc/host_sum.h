@@ -18,7 +18,7 @@ namespace exsum_host {
 // as large_accumulator.hpp:99-103) over a 67-chunk small superaccumulator, plus
 // the first global index of +Inf / -Inf / NaN.
 #ifndef EXSUM_HOST_COPIES
-#define EXSUM_HOST_COPIES 2
+#define EXSUM_HOST_COPIES 1
 #endif
 struct alignas(64) Acc {
   static constexpr int kCopies = EXSUM_HOST_COPIES;

@@ -105,6 +105,10 @@
 #define EXSUM_PF_PRED 1  // plain sums: the per-batch L2 prefetch predicated on lane 0 instead of a
                          // lane-0 branch
 #endif
+#ifndef EXSUM_SEG_DEFER
+#define EXSUM_SEG_DEFER 1  // segmented sums: round every segment in a second launch
+                           // (exsum_segment_emit_kernel) instead of on the streaming warp
+#endif
 #ifndef EXSUM_DEBUG_CHECKS
 #define EXSUM_DEBUG_CHECKS 0  // debug build: every streaming load checks its vector index against
                               // the range end (printf + trap on a violation)
@@ -1439,6 +1443,10 @@ struct OrderState {                    // zeroed by exsum_cuda_workspace_init
 };
 constexpr size_t kOrderStateOffset = (sizeof(Workspace) + 255) & ~size_t{255};
 constexpr size_t kOrderOffset = kOrderStateOffset + sizeof(OrderState);  // order[] in d_ws
+// deferred-rounding records (EXSUM_SEG_DEFER) after order[], 256-byte aligned
+__host__ __device__ constexpr size_t seg_records_offset(size_t nseg) {
+  return (kOrderOffset + 4 * nseg + 255) & ~size_t{255};
+}
 
 __device__ __forceinline__ int length_bucket(unsigned long long len) {
   if (len < 8) return static_cast<int>(len);
@@ -1536,7 +1544,8 @@ struct SegmentClaim {
 __global__ void __launch_bounds__(kThreads, 1)
 exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *__restrict__ offs,
                        unsigned long long nseg, Workspace *__restrict__ ws, double *out,
-                       exsum_partial *partials, const unsigned int *__restrict__ order) {
+                       exsum_partial *partials, const unsigned int *__restrict__ order,
+                       exsum_partial *raw) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -1580,9 +1589,22 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
                              N = warp_min_u64(sp.N);
     __syncwarp();
     EXSUM_SEG_PHASE(3);
-    const unsigned long long payload =
-        N != ~0ull ? __ldg(reinterpret_cast<const unsigned long long *>(x) + b + N) : 0ull;
-    warp_emit(row, P, M, N, payload, out + s, partials ? partials + s : nullptr, lane);
+    if (raw) {
+      // deferred: the raw chunk sums and first indices; exsum_segment_emit_kernel
+      // canonicalises and rounds every segment after this launch
+      long long *dst = reinterpret_cast<long long *>(raw[s].acc.chunk);
+      dst[lane] = row[lane];
+      dst[lane + 32] = row[lane + 32];
+      if (lane < 3) {
+        dst[lane + 64] = row[lane + 64];
+        reinterpret_cast<unsigned long long *>(&raw[s].first_pos_inf)[lane] =
+            lane == 0 ? P : lane == 1 ? M : N;
+      }
+    } else {
+      const unsigned long long payload =
+          N != ~0ull ? __ldg(reinterpret_cast<const unsigned long long *>(x) + b + N) : 0ull;
+      warp_emit(row, P, M, N, payload, out + s, partials ? partials + s : nullptr, lane);
+    }
     __syncwarp();
     EXSUM_SEG_PHASE(4);
   }
@@ -1600,6 +1622,30 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
       ws->seg_done = 0;
     }
   }
+}
+
+// Second half of a deferred segmented sum: one warp per segment canonicalises
+// its raw record (chunk sums |c| < 2^44, local first indices) and rounds it —
+// the per-segment warp_emit taken off the streaming warps.  raw may alias
+// partials (in place: every lane's loads precede the warp's stores).
+constexpr int kEmitWarps = 8;
+__global__ void __launch_bounds__(32 * kEmitWarps)
+exsum_segment_emit_kernel(const exsum_partial *raw, const unsigned long long *__restrict__ offs,
+                          const double *__restrict__ x, unsigned long long nseg, double *out,
+                          exsum_partial *partials) {
+  const int lane = threadIdx.x & 31;
+  const unsigned long long s =
+      static_cast<unsigned long long>(blockIdx.x) * kEmitWarps + (threadIdx.x >> 5);
+  if (s >= nseg) return;
+  const long long *c = reinterpret_cast<const long long *>(raw[s].acc.chunk);
+  const long long v0 = __ldcg(c + lane), v1 = __ldcg(c + lane + 32),
+                  v2 = lane < 3 ? __ldcg(c + lane + 64) : 0;
+  const unsigned long long *f = reinterpret_cast<const unsigned long long *>(&raw[s].first_pos_inf);
+  const unsigned long long P = __ldcg(f), M = __ldcg(f + 1), N = __ldcg(f + 2);
+  const unsigned long long payload =
+      N != ~0ull ? __ldg(reinterpret_cast<const unsigned long long *>(x) + offs[s] + N) : 0ull;
+  __syncwarp();
+  warp_emit_v(v0, v1, v2, P, M, N, payload, out + s, partials ? partials + s : nullptr, lane);
 }
 
 // ------------------------------------------------------------------------- K5
@@ -1964,15 +2010,34 @@ int exsum_cuda_sum_segmented(const double *d_x, const uint64_t *d_offsets, size_
     exsum_segment_scatter_kernel<<<og, kOrderThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         offs, nseg, st, order);
   }
+  // Deferred rounding: raw records go to d_partials when the caller wants them,
+  // else to the workspace after the claim order (when it has room).
+  exsum_partial *raw = nullptr;
+#if EXSUM_SEG_DEFER
+  if (d_partials) {
+    raw = d_partials;
+  } else if (order && ws_bytes >= exsum_cuda_segmented_workspace_bytes(nseg)) {
+    raw = reinterpret_cast<exsum_partial *>(static_cast<unsigned char *>(d_ws) +
+                                            seg_records_offset(nseg));
+  }
+#endif
   exsum_segmented_kernel<<<static_cast<unsigned>(g), kThreads, kSmem,
                            static_cast<cudaStream_t>(stream)>>>(
-      d_x, offs, nseg, static_cast<Workspace *>(d_ws), d_out, d_partials, order);
+      d_x, offs, nseg, static_cast<Workspace *>(d_ws), d_out, d_partials, order, raw);
+  if (raw)
+    exsum_segment_emit_kernel<<<static_cast<unsigned>((nseg + kEmitWarps - 1) / kEmitWarps),
+                                32 * kEmitWarps, 0, static_cast<cudaStream_t>(stream)>>>(
+        raw, offs, d_x, nseg, d_out, d_partials);
   return launch_status();
 }
 
 size_t exsum_cuda_segmented_workspace_bytes(size_t nseg) {
   if (nseg > kOrderMaxSegs) return sizeof(Workspace);
+#if EXSUM_SEG_DEFER
+  return seg_records_offset(nseg) + nseg * sizeof(exsum_partial);
+#else
   return kOrderOffset + 4 * nseg;
+#endif
 }
 
 int exsum_cuda_merge(const exsum_partial *d_parts, size_t k, double *d_result,

@@ -51,14 +51,20 @@ def test_struct_layouts():
 
 
 def test_segmented_workspace_sizes():
-    """Room for the longest-first claim order: 4 bytes per segment after the
-    base workspace and the order state; beyond 2^24 segments the kernel claims
-    in index order and needs only the base workspace."""
+    """Room for the longest-first claim order (4 bytes per segment after the
+    base workspace and the order state) and for the deferred-rounding records
+    (one 592-byte exsum_partial per segment, 256-byte aligned); beyond 2^24
+    segments the kernel claims in index order and needs only the base workspace."""
     base = lib.exsum_cuda_workspace_bytes()
     w0 = lib.exsum_cuda_segmented_workspace_bytes(0)
     assert w0 >= base
-    assert lib.exsum_cuda_segmented_workspace_bytes(65536) == w0 + 4 * 65536
-    assert lib.exsum_cuda_segmented_workspace_bytes(1 << 24) == w0 + 4 * (1 << 24)
+
+    def expect(n):
+        return ((w0 + 4 * n + 255) // 256) * 256 + 592 * n
+
+    assert w0 == expect(0)
+    assert lib.exsum_cuda_segmented_workspace_bytes(65536) == expect(65536)
+    assert lib.exsum_cuda_segmented_workspace_bytes(1 << 24) == expect(1 << 24)
     assert lib.exsum_cuda_segmented_workspace_bytes((1 << 24) + 1) == base
 
 
