@@ -5,10 +5,10 @@
 // they do for every reference caller.  The array is split DYNAMICALLY between
 //
 //   * the device feeder (the calling thread): claims chunks from a shared
-//     cursor, copies each host->device over PCIe into a 3-slot device staging
+//     cursor, copies each host->device over PCIe into a 4-slot device staging
 //     ring (copy stream) and accumulates it there (exsum_cuda_accumulate with the
-//     chunk's global base index, compute stream); at most two chunks in flight,
-//     so the DMA engine never idles and the device never hoards work;
+//     chunk's global base index, compute stream); at most three chunks in
+//     flight, so the DMA engine never idles and the device never hoards work;
 //   * the host workers (exsum_host::Pool, host_sum.cpp): claim small chunks
 //     from the same cursor and sum them with the library's own host kernel.
 //
@@ -36,8 +36,9 @@
 #include "host_sum.h"
 
 namespace {
-constexpr int kSlots = 3;     // device staging buffers
-constexpr int kInFlight = 2;  // chunks claimed by the feeder and not yet copied
+constexpr int kSlots = 4;     // device staging buffers
+constexpr int kInFlight = 3;  // chunks claimed by the feeder and not yet copied (DMA queue
+                              // depth: covers the feeder's wake-up latency among busy workers)
 constexpr size_t kHostGrain = size_t{1} << 18;  // terms per host-worker claim (2 MB)
 }  // namespace
 

@@ -235,7 +235,7 @@ class HostContext:
     so Python threads sharing a context cannot interleave.
     """
 
-    def __init__(self, device: int = 0, staging_bytes: int = 192 << 20, host_threads: int = -1):
+    def __init__(self, device: int = 0, staging_bytes: int = 256 << 20, host_threads: int = -1):
         self.device = device
         self._lock = threading.Lock()
         self._h = lib.exsum_context_create(device, staging_bytes)

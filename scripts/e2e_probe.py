@@ -26,7 +26,7 @@ def main():
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--threads", default="16,15,14,12")
-    ap.add_argument("--staging", type=int, default=192)
+    ap.add_argument("--staging", type=int, default=256)
     a = ap.parse_args()
     n = int(a.n)
     from oracle import port
