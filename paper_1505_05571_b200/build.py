@@ -25,7 +25,7 @@ CXX = "/usr/bin/g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["sum_kernels.cu", "synth.cu", "context.cu", "nccl_sum.cu"]
 CXX_SOURCES = ["host_accumulators.cpp", "io.cpp", "host_sum.cpp"]
-HEADERS = [CSRC / "exsum_core.h", CSRC / "host_sum.h", INCLUDE / "exsum_b200.h"]
+HEADERS = [CSRC / "exsum_core.h", CSRC / "host_sum.h", CSRC / "exsum_nvtx.h", INCLUDE / "exsum_b200.h"]
 
 
 def _stale(target: Path, deps: list[Path]) -> bool:
@@ -63,7 +63,7 @@ def build(verbose: bool = False, force: bool = False, defines: tuple[str, ...] =
         objs.append(obj)
         if force or _stale(obj, [CSRC / src, *HEADERS]):
             _run([CXX, *dflags, "-std=c++17", "-O3" if src == "host_sum.cpp" else "-O2", "-fPIC",
-                  "-pthread", "-Wall", "-Wextra", *common_inc,
+                  "-pthread", "-Wall", "-Wextra", *common_inc, "-I/usr/local/cuda/include",
                   "-c", str(CSRC / src), "-o", str(obj)], verbose)
     if force or _stale(lib, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs),

@@ -33,6 +33,7 @@
 #include <string>
 
 #include "exsum_b200.h"
+#include "exsum_nvtx.h"
 #include "host_sum.h"
 
 namespace {
@@ -114,6 +115,7 @@ bool is_pinned(const void *p) {
 // Returns the number of terms it took, or sets *st.
 uint64_t feed_device(exsum_context *c, const double *h_x, size_t n, uint64_t base,
                      std::atomic<size_t> *cursor, bool pinned, bool hybrid, int *st) {
+  EXSUM_NVTX("exsum_context: device feed");
   uint64_t taken = 0;
   for (int i = 0;; ++i) {
     const int b = i % kSlots;
@@ -222,6 +224,7 @@ int exsum_context_sum(exsum_context *c, const double *h_x, size_t n, double *h_r
 
 int exsum_context_sum_at(exsum_context *c, const double *h_x, size_t n, uint64_t base_index,
                          double *h_result, exsum_partial *h_partial) {
+  EXSUM_NVTX("exsum_context_sum");
   if (!c || (n && !h_x) || (!h_result && !h_partial)) return EXSUM_EINVAL;
   std::lock_guard<std::mutex> lk(c->busy);
   int prev = 0;
@@ -277,6 +280,7 @@ int exsum_context_sum_at(exsum_context *c, const double *h_x, size_t n, uint64_t
 
 int exsum_context_sum_file(exsum_context *c, const char *path, int format, double *h_result,
                            exsum_partial *h_partial, uint64_t *n_out) {
+  EXSUM_NVTX("exsum_context_sum_file");
   if (!c || !path || (!h_result && !h_partial)) return EXSUM_EINVAL;
   if (format == EXSUM_FORMAT_TEXT) {
     double *v = nullptr;

@@ -45,6 +45,7 @@
 
 #include "exsum_b200.h"
 #include "exsum_core.h"
+#include "exsum_nvtx.h"
 #include "host_sum.h"
 
 using namespace exsum_b200;
@@ -278,6 +279,7 @@ bool Pool::ok() const {
 }
 
 void Pool::run_share(int t) {
+  EXSUM_NVTX("exsum_host: worker share");
   Acc *a = accs_[static_cast<size_t>(t)];
   a->reset();
   for (;;) {
@@ -340,6 +342,7 @@ void Pool::sum(const double *x, size_t n, uint64_t base, exsum_partial *out) {
 
 extern "C" int exsum_host_sum(const double *x, size_t n, uint64_t base_index, int threads,
                               double *result, exsum_partial *partial) {
+  EXSUM_NVTX("exsum_host_sum");
   if ((n && !x) || (!result && !partial)) return EXSUM_EINVAL;
   if (threads <= 0) threads = exsum_host::default_threads();
   // no more threads than 1 Mi-term shares: thread start-up would dominate

@@ -26,6 +26,7 @@
 #include <mutex>
 
 #include "exsum_b200.h"
+#include "exsum_nvtx.h"
 
 namespace {
 
@@ -135,6 +136,7 @@ size_t exsum_nccl_workspace_bytes(int nranks) {
 int exsum_nccl_sum(const double *d_shard, size_t n, uint64_t base_index, void *comm,
                    double *d_result, exsum_partial *d_partial, void *d_ws, size_t ws_bytes,
                    void *stream, unsigned flags) {
+  EXSUM_NVTX("exsum_nccl_sum");
   if (!comm || !d_ws || (n && !d_shard)) return EXSUM_EINVAL;
   const NcclApi *api = nccl();
   if (!api) return EXSUM_ENCCL;

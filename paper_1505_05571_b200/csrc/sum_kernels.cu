@@ -62,6 +62,7 @@
 
 #include "exsum_b200.h"
 #include "exsum_core.h"
+#include "exsum_nvtx.h"
 
 #ifndef EXSUM_VEC_PER_LANE
 #define EXSUM_VEC_PER_LANE 8  // single-sum kernel: 256-bit vectors per lane per batch
@@ -1839,11 +1840,13 @@ int exsum_cuda_sum(const double *d_x, size_t n, uint64_t base_index, double *d_r
 int exsum_cuda_sum_ex(const double *d_x, size_t n, uint64_t base_index, double *d_result,
                       exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
                       unsigned flags) {
+  EXSUM_NVTX("exsum_cuda_sum");
   return sum_launch(d_x, n, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial, flags);
 }
 
 int exsum_cuda_sqnorm(const double *d_x, size_t n, uint64_t base_index, double *d_result,
                       exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream) {
+  EXSUM_NVTX("exsum_cuda_sqnorm");
   return sum_launch(d_x, n, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial, 0,
                     kSqnorm);
 }
@@ -1851,6 +1854,7 @@ int exsum_cuda_sqnorm(const double *d_x, size_t n, uint64_t base_index, double *
 int exsum_cuda_dot(const double *d_a, size_t na, const double *d_b, size_t nb,
                    uint64_t base_index, double *d_result, exsum_partial *d_partial, void *d_ws,
                    size_t ws_bytes, void *stream) {
+  EXSUM_NVTX("exsum_cuda_dot");
   if (na != nb) return EXSUM_EINVAL;  // dot: length mismatch (vector_ops.cpp:150-152)
   return sum_launch(d_a, na, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial, 0,
                     dot_op(d_a, d_b), d_b);
@@ -1882,6 +1886,7 @@ int exsum_p2p_sum(const double *d_shard, size_t n, uint64_t base_index, int rank
                   void *const *mailboxes, uint64_t epoch, double *d_result,
                   exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
                   unsigned flags) {
+  EXSUM_NVTX("exsum_p2p_sum");
   if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || !mailboxes || epoch == 0)
     return EXSUM_EINVAL;
   P2PArgs X = {};
@@ -1899,6 +1904,7 @@ int exsum_p2p_sum(const double *d_shard, size_t n, uint64_t base_index, int rank
 
 int exsum_p2p_collect(int rank, int nranks, void *const *mailboxes, uint64_t epoch,
                       double *d_result, exsum_partial *d_partial, void *stream) {
+  EXSUM_NVTX("exsum_p2p_collect");
   if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || !mailboxes || epoch == 0)
     return EXSUM_EINVAL;
   P2PArgs X = {};
@@ -1971,12 +1977,14 @@ int exsum_ipc_close(void *d_ptr) {
 
 int exsum_cuda_accumulate(const double *d_x, size_t n, uint64_t base_index, void *d_ws,
                           size_t ws_bytes, void *stream) {
+  EXSUM_NVTX("exsum_cuda_accumulate");
   if (n == 0) return (d_ws && ws_bytes >= sizeof(Workspace)) ? EXSUM_OK : EXSUM_EINVAL;
   return sum_launch(d_x, n, base_index, d_ws, ws_bytes, stream, 0, nullptr, nullptr);
 }
 
 int exsum_cuda_finalize(double *d_result, exsum_partial *d_partial, void *d_ws, size_t ws_bytes,
                         void *stream) {
+  EXSUM_NVTX("exsum_cuda_finalize");
   if (!d_ws || ws_bytes < sizeof(Workspace)) return EXSUM_EINVAL;
   exsum_finalize_kernel<<<1, 96, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<Workspace *>(d_ws), d_result, d_partial);
@@ -1986,6 +1994,7 @@ int exsum_cuda_finalize(double *d_result, exsum_partial *d_partial, void *d_ws, 
 int exsum_cuda_sum_segmented(const double *d_x, const uint64_t *d_offsets, size_t nseg,
                              double *d_out, exsum_partial *d_partials, void *d_ws,
                              size_t ws_bytes, void *stream) {
+  EXSUM_NVTX("exsum_cuda_sum_segmented");
   if (!d_ws || ws_bytes < sizeof(Workspace) || (nseg && (!d_offsets || !d_out)))
     return EXSUM_EINVAL;
   if (nseg == 0) return EXSUM_OK;
@@ -2042,6 +2051,7 @@ size_t exsum_cuda_segmented_workspace_bytes(size_t nseg) {
 
 int exsum_cuda_merge(const exsum_partial *d_parts, size_t k, double *d_result,
                      exsum_partial *d_out, void *stream) {
+  EXSUM_NVTX("exsum_cuda_merge");
   if (k && !d_parts) return EXSUM_EINVAL;
   exsum_merge_kernel<<<1, 96, 0, static_cast<cudaStream_t>(stream)>>>(d_parts, k, d_result,
                                                                       d_out);
