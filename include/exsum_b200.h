@@ -352,6 +352,13 @@ int exsum_cuda_gen_segmented(uint64_t seed, uint64_t first, size_t count, double
 /* The same config-5 values on the host (bit-identical to exsum_cuda_gen_segmented). */
 int exsum_host_gen_segmented(uint64_t seed, uint64_t first, size_t count, double *out);
 
+/* The paper's benchmark data (generate, generator.cpp:23-45): n/2 values
+ * U1 * exp(30 U2) from the minstd stream seeded with `seed`, mirrored as -v into
+ * the second half (exact sum zero), Fisher-Yates shuffled on the same stream if
+ * permute.  EXSUM_EINVAL for n == 0 or odd (the reference throws
+ * std::invalid_argument).  Bits equal the reference's with the same libm exp. */
+int exsum_generate(uint64_t n, uint64_t seed, int permute, double *out);
+
 /* Library build/version info: "exsum_b200 <version> sm_100a". */
 const char *exsum_version(void);
 

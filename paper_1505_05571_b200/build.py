@@ -24,7 +24,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CXX = "/usr/bin/g++"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["sum_kernels.cu", "synth.cu", "context.cu", "nccl_sum.cu"]
-CXX_SOURCES = ["host_accumulators.cpp", "io.cpp", "host_sum.cpp"]
+CXX_SOURCES = ["host_accumulators.cpp", "io.cpp", "host_sum.cpp", "host_tools.cpp"]
 HEADERS = [CSRC / "exsum_core.h", CSRC / "host_sum.h", CSRC / "exsum_nvtx.h", INCLUDE / "exsum_b200.h"]
 
 
