@@ -1,7 +1,8 @@
 """Summarise ncu --set full reports into profiles/ (text + JSON).
 
-usage: python scripts/ncu_summary.py <tag> <report.ncu-rep> [<tag> <report> ...]
-Writes profiles/ncu_<tag>.txt and merges profiles/ncu_summary.json.
+usage: python scripts/ncu_summary.py [--round r02] <tag>[:kernel-substring] <report.ncu-rep> ...
+Writes profiles/<round>_ncu_<tag>.txt and merges profiles/ncu_summary.json (bench.py reads
+the per-launch DRAM bytes of tags config2..config5 from it).
 """
 import csv
 import io
@@ -37,29 +38,37 @@ KEYS = [
 ]
 
 
-def raw(report):
+def raw(report, kernel=None):
     out = subprocess.run(["ncu", "-i", str(report), "--page", "raw", "--csv"], check=True,
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h, units, vals = rows[0], rows[1], rows[2]
-    return {k: (vals[h.index(k)], units[h.index(k)]) for k in KEYS if k in h}, vals[h.index("Kernel Name")] if "Kernel Name" in h else ""
+    h, units = rows[0], rows[1]
+    kn = h.index("Kernel Name") if "Kernel Name" in h else None
+    vals = rows[2]
+    if kernel and kn is not None:
+        vals = next(r for r in rows[2:] if kernel in r[kn])
+    return {k: (vals[h.index(k)], units[h.index(k)]) for k in KEYS if k in h}, vals[kn] if kn is not None else ""
 
 
 def main():
     args = sys.argv[1:]
+    rnd = "r01"
+    if args[:1] == ["--round"]:
+        rnd, args = args[1], args[2:]
     summ_path = ROOT / "profiles" / "ncu_summary.json"
     summ = json.loads(summ_path.read_text()) if summ_path.exists() else {}
-    for tag, rep in zip(args[::2], args[1::2]):
-        m, kname = raw(rep)
+    for tagk, rep in zip(args[::2], args[1::2]):
+        tag, _, kernel = tagk.partition(":")
+        m, kname = raw(rep, kernel or None)
         lines = [f"# ncu --set full --clock-control none: {tag}", f"kernel: {kname}", ""]
         lines += [f"{k:80s} {v} {u}" for k, (v, u) in m.items()]
-        (ROOT / "profiles" / f"r01_ncu_{tag}.txt").write_text("\n".join(lines) + "\n")
+        (ROOT / "profiles" / f"{rnd}_ncu_{tag}.txt").write_text("\n".join(lines) + "\n")
         f = lambda k: float(m[k][0].replace(",", "")) if k in m else None  # noqa: E731
         rd, wr = f("dram__bytes_read.sum"), f("dram__bytes_write.sum")
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         rd = rd * scale.get(m["dram__bytes_read.sum"][1], 1) if rd is not None else None
         wr = wr * scale.get(m["dram__bytes_write.sum"][1], 1) if wr is not None else None
-        summ[tag] = {"report": Path(rep).name, "dram_bytes_per_launch": (rd or 0) + (wr or 0),
+        summ[tag] = {"report": Path(rep).name, "kernel": kname[:120], "dram_bytes_per_launch": (rd or 0) + (wr or 0),
                      "dram_read_bytes": rd, "dram_write_bytes": wr,
                      "duration": m.get("gpu__time_duration.sum"),
                      "issue_active_pct": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
