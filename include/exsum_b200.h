@@ -236,6 +236,16 @@ int exsum_context_sum(exsum_context *ctx, const double *h_x, size_t n, double *h
  * partial record's Inf/NaN indices are global, ready for exsum_partial_merge). */
 int exsum_context_sum_at(exsum_context *ctx, const double *h_x, size_t n, uint64_t base_index,
                          double *h_result, exsum_partial *h_partial);
+/* One exact_sum per segment of a HOST array (host-array form of
+ * exsum_cuda_sum_segmented): segment i is h_x[h_offsets[i] .. h_offsets[i+1])
+ * (a decreasing pair is an empty segment).  The device takes groups of whole
+ * segments (≤ one staging chunk of values, ≤ 16384 segments) over PCIe while the
+ * host workers sum other segments; h_out (nseg doubles) and h_partials (nseg
+ * records, indices local to each segment; may be NULL) are bit-identical to
+ * the device path whatever the split.  Blocking. */
+int exsum_context_sum_segmented(exsum_context *ctx, const double *h_x,
+                                const uint64_t *h_offsets, size_t nseg, double *h_out,
+                                exsum_partial *h_partials);
 /* exact_sum(read_values(path, format)) without materialising the array: a bin
  * file is read chunk by chunk into pinned host buffers that feed the staging
  * ring (disk read, host->device copy and accumulate overlap); a text file is

@@ -137,6 +137,7 @@ _SIGNATURES = {
     "exsum_context_sum": (_i32, [_vp, _vp, _sz, _dp, _pp]),
     "exsum_context_sum_at": (_i32, [_vp, _vp, _sz, _u64, _dp, _pp]),
     "exsum_context_set_host_threads": (_i32, [_vp, _i32]),
+    "exsum_context_sum_segmented": (_i32, [_vp, _vp, _vp, _sz, _vp, _vp]),
     "exsum_context_last_split": (_i32, [_vp, C.POINTER(_u64), C.POINTER(_u64)]),
     "exsum_cuda_gen": (_i32, [_i32, _u64, _u64, _u64, _sz, _vp, _vp]),
     "exsum_host_gen": (_i32, [_i32, _u64, _u64, _u64, _sz, _vp]),

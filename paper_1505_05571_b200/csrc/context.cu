@@ -59,6 +59,12 @@ struct exsum_context {
   int host_threads = -1;               // < 0: all hardware threads; 0: device only
   exsum_host::Pool *pool = nullptr;
   uint64_t last_device_terms = 0, last_host_terms = 0;
+  // segmented sums of host arrays (allocated on first use)
+  void *seg_ws = nullptr;
+  size_t seg_ws_bytes = 0;
+  uint64_t *d_offs[kSlots] = {}, *h_offs[kSlots] = {};
+  double *d_out[kSlots] = {}, *h_out[kSlots] = {};
+  exsum_partial *d_parts[kSlots] = {}, *h_parts[kSlots] = {};
 };
 
 namespace {
@@ -76,6 +82,15 @@ void destroy(exsum_context *c) {
     if (c->consumed[i]) cudaEventDestroy(c->consumed[i]);
   }
   if (c->h_partial) cudaFreeHost(c->h_partial);
+  for (int i = 0; i < kSlots; ++i) {
+    if (c->d_offs[i]) cudaFree(c->d_offs[i]);
+    if (c->d_out[i]) cudaFree(c->d_out[i]);
+    if (c->d_parts[i]) cudaFree(c->d_parts[i]);
+    if (c->h_offs[i]) cudaFreeHost(c->h_offs[i]);
+    if (c->h_out[i]) cudaFreeHost(c->h_out[i]);
+    if (c->h_parts[i]) cudaFreeHost(c->h_parts[i]);
+  }
+  if (c->seg_ws) cudaFree(c->seg_ws);
   if (c->ws) cudaFree(c->ws);
   if (c->d_result) cudaFree(c->d_result);
   if (c->d_partial) cudaFree(c->d_partial);
@@ -99,7 +114,36 @@ void reset_after_error(exsum_context *c) {
   cudaStreamSynchronize(c->copy);
   cudaStreamSynchronize(c->compute);
   exsum_cuda_workspace_init(c->ws, c->ws_bytes, c->compute);
+  if (c->seg_ws) exsum_cuda_workspace_init(c->seg_ws, c->seg_ws_bytes, c->compute);
   cudaStreamSynchronize(c->compute);
+}
+
+constexpr size_t kGroupSegs = 16384;  // segments per device group (segmented sums)
+
+int ensure_segmented(exsum_context *c, bool partials) {
+  if (!c->seg_ws) {
+    c->seg_ws_bytes = exsum_cuda_segmented_workspace_bytes(kGroupSegs);
+    if (cudaMalloc(&c->seg_ws, c->seg_ws_bytes) != cudaSuccess) {
+      c->seg_ws = nullptr;
+      return EXSUM_ENOMEM;
+    }
+    if (exsum_cuda_workspace_init(c->seg_ws, c->seg_ws_bytes, c->compute) != EXSUM_OK ||
+        cudaStreamSynchronize(c->compute) != cudaSuccess)
+      return EXSUM_ECUDA;
+  }
+  for (int i = 0; i < kSlots; ++i) {
+    if (!c->d_offs[i] &&
+        (cudaMalloc(&c->d_offs[i], (kGroupSegs + 1) * 8) != cudaSuccess ||
+         cudaMalloc(&c->d_out[i], kGroupSegs * 8) != cudaSuccess ||
+         cudaMallocHost(&c->h_offs[i], (kGroupSegs + 1) * 8) != cudaSuccess ||
+         cudaMallocHost(&c->h_out[i], kGroupSegs * 8) != cudaSuccess))
+      return EXSUM_ENOMEM;
+    if (partials && !c->d_parts[i] &&
+        (cudaMalloc(&c->d_parts[i], kGroupSegs * sizeof(exsum_partial)) != cudaSuccess ||
+         cudaMallocHost(&c->h_parts[i], kGroupSegs * sizeof(exsum_partial)) != cudaSuccess))
+      return EXSUM_ENOMEM;
+  }
+  return EXSUM_OK;
 }
 
 bool is_pinned(const void *p) {
@@ -273,6 +317,165 @@ int exsum_context_sum_at(exsum_context *c, const double *h_x, size_t n, uint64_t
     if (h_result) exsum_partial_round(&merged, h_result);
     c->last_device_terms = dev_terms;
     c->last_host_terms = n - dev_terms;
+  }
+  cudaSetDevice(prev);
+  return st;
+}
+
+
+int exsum_context_sum_segmented(exsum_context *c, const double *h_x, const uint64_t *h_offsets,
+                                size_t nseg, double *h_out, exsum_partial *h_partials) {
+  EXSUM_NVTX("exsum_context_sum_segmented");
+  if (!c || (nseg && (!h_offsets || !h_out))) return EXSUM_EINVAL;
+  if (nseg == 0) return EXSUM_OK;
+  // the span of values the segments touch (offsets need not be monotonic: a
+  // decreasing pair is an empty segment)
+  uint64_t lo = h_offsets[0], hi = h_offsets[0];
+  for (size_t s = 1; s <= nseg; ++s) {
+    lo = h_offsets[s] < lo ? h_offsets[s] : lo;
+    hi = h_offsets[s] > hi ? h_offsets[s] : hi;
+  }
+  if (hi > lo && !h_x) return EXSUM_EINVAL;
+  std::lock_guard<std::mutex> lk(c->busy);
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(c->device) != cudaSuccess) return EXSUM_ECUDA;
+  const bool pinned = hi == lo || is_pinned(h_x + lo);
+  int st = ensure_segmented(c, h_partials != nullptr);
+  if (st == EXSUM_OK && !pinned) st = ensure_bounce(c);
+  int workers = c->host_threads < 0 ? exsum_host::default_threads() : c->host_threads;
+  if (hi - lo < (uint64_t{1} << 20)) workers = 0;
+  if (st == EXSUM_OK && workers > 0 && (!c->pool || c->pool->size() != workers + 1)) {
+    delete c->pool;
+    c->pool = new (std::nothrow) exsum_host::Pool(workers + 1);
+    if (!c->pool || !c->pool->ok()) {
+      delete c->pool;
+      c->pool = nullptr;
+      workers = 0;
+    }
+  }
+  const bool hybrid = workers > 0 && c->pool;
+  std::atomic<size_t> cursor{0};
+  if (st == EXSUM_OK && hybrid)
+    c->pool->start_segments(h_x, h_offsets, nseg, &cursor, 4, h_out, h_partials);
+  // device feeder: groups of whole segments, each group's value span <= one chunk
+  size_t pend0[kSlots] = {}, pend1[kSlots] = {};
+  bool pending[kSlots] = {};
+  uint64_t dev_terms = 0;
+  auto drain_slot = [&](int b) {
+    if (!pending[b]) return true;
+    if (cudaEventSynchronize(c->consumed[b]) != cudaSuccess) return false;
+    memcpy(h_out + pend0[b], c->h_out[b], (pend1[b] - pend0[b]) * 8);
+    if (h_partials)
+      memcpy(h_partials + pend0[b], c->h_parts[b], (pend1[b] - pend0[b]) * sizeof(exsum_partial));
+    pending[b] = false;
+    return true;
+  };
+  for (int i = 0; st == EXSUM_OK; ++i) {
+    const int b = i % kSlots;
+    if (i >= kInFlight && cudaEventSynchronize(c->copied[(i - kInFlight) % kSlots]) != cudaSuccess) {
+      st = EXSUM_ECUDA;
+      break;
+    }
+    if (!drain_slot(b)) {
+      st = EXSUM_ECUDA;
+      break;
+    }
+    // claim [s0, s1): as many segments as fit one staging chunk (CAS: host
+    // workers move the same cursor with fetch_add)
+    size_t s0 = cursor.load(std::memory_order_relaxed), s1 = 0;
+    uint64_t glo = 0, ghi = 0;
+    bool got = false, longseg = false;
+    while (s0 < nseg) {
+      glo = ghi = h_offsets[s0];
+      s1 = s0;
+      while (s1 < nseg && s1 - s0 < kGroupSegs) {
+        const uint64_t nlo = h_offsets[s1 + 1] < glo ? h_offsets[s1 + 1] : glo;
+        const uint64_t nhi = h_offsets[s1 + 1] > ghi ? h_offsets[s1 + 1] : ghi;
+        if (nhi - nlo > c->stage_elems) break;
+        glo = nlo;
+        ghi = nhi;
+        ++s1;
+      }
+      longseg = s1 == s0;  // one segment larger than a chunk: streamed on its own
+      if (longseg) s1 = s0 + 1;
+      if (cursor.compare_exchange_weak(s0, s1, std::memory_order_relaxed)) {
+        got = true;
+        break;
+      }
+    }
+    if (!got) break;
+    if (longseg) {
+      // the ring's pending groups first, then the segment through the incremental
+      // path (chunked copies + exsum_cuda_accumulate, local indices) and a finalize
+      for (int k = 0; k < kSlots && st == EXSUM_OK; ++k)
+        if (!drain_slot(k)) st = EXSUM_ECUDA;
+      if (st != EXSUM_OK) break;
+      const uint64_t b0 = h_offsets[s0], e0 = h_offsets[s0 + 1];
+      std::atomic<size_t> sub{0};
+      dev_terms += feed_device(c, h_x + b0, e0 - b0, 0, &sub, is_pinned(h_x + b0), false, &st);
+      if (st == EXSUM_OK)
+        st = exsum_cuda_finalize(c->d_result, c->d_partial, c->ws, c->ws_bytes, c->compute);
+      if (st == EXSUM_OK &&
+          (cudaMemcpyAsync(c->h_partial, c->d_partial, sizeof(exsum_partial),
+                           cudaMemcpyDeviceToHost, c->compute) != cudaSuccess ||
+           cudaStreamSynchronize(c->compute) != cudaSuccess))
+        st = EXSUM_ECUDA;
+      if (st != EXSUM_OK) break;
+      if (h_partials) h_partials[s0] = *c->h_partial;
+      exsum_partial_round(c->h_partial, h_out + s0);
+      i = -1;  // the ring restarts empty
+      continue;
+    }
+    const size_t len = ghi - glo, ns = s1 - s0;
+    const double *src = h_x + glo;
+    if (!pinned && len) {
+      memcpy(c->host[b], src, len * sizeof(double));
+      src = c->host[b];
+    }
+    memcpy(c->h_offs[b], h_offsets + s0, (ns + 1) * 8);
+    if ((i >= kSlots && cudaStreamWaitEvent(c->copy, c->consumed[b], 0) != cudaSuccess) ||
+        (len && cudaMemcpyAsync(c->stage[b], src, len * sizeof(double), cudaMemcpyHostToDevice,
+                                c->copy) != cudaSuccess) ||
+        cudaMemcpyAsync(c->d_offs[b], c->h_offs[b], (ns + 1) * 8, cudaMemcpyHostToDevice,
+                        c->copy) != cudaSuccess ||
+        cudaEventRecord(c->copied[b], c->copy) != cudaSuccess ||
+        cudaStreamWaitEvent(c->compute, c->copied[b], 0) != cudaSuccess) {
+      st = EXSUM_ECUDA;
+      break;
+    }
+    // the kernel addresses x + offs[s]: hand it the staged span shifted back by glo
+    st = exsum_cuda_sum_segmented(c->stage[b] - glo, c->d_offs[b], ns, c->d_out[b],
+                                  h_partials ? c->d_parts[b] : nullptr, c->seg_ws,
+                                  c->seg_ws_bytes, c->compute);
+    if (st != EXSUM_OK) break;
+    if (cudaMemcpyAsync(c->h_out[b], c->d_out[b], ns * 8, cudaMemcpyDeviceToHost, c->compute) !=
+            cudaSuccess ||
+        (h_partials &&
+         cudaMemcpyAsync(c->h_parts[b], c->d_parts[b], ns * sizeof(exsum_partial),
+                         cudaMemcpyDeviceToHost, c->compute) != cudaSuccess) ||
+        cudaEventRecord(c->consumed[b], c->compute) != cudaSuccess) {
+      st = EXSUM_ECUDA;
+      break;
+    }
+    pend0[b] = s0;
+    pend1[b] = s1;
+    pending[b] = true;
+    for (size_t s = s0; s < s1; ++s)
+      dev_terms += h_offsets[s + 1] > h_offsets[s] ? h_offsets[s + 1] - h_offsets[s] : 0;
+  }
+  for (int b = 0; b < kSlots; ++b)
+    if (st == EXSUM_OK && !drain_slot(b)) st = EXSUM_ECUDA;
+  if (cudaStreamSynchronize(c->compute) != cudaSuccess && st == EXSUM_OK) st = EXSUM_ECUDA;
+  if (hybrid) c->pool->join_helpers();
+  if (st != EXSUM_OK) {
+    reset_after_error(c);
+  } else {
+    uint64_t total = 0;
+    for (size_t s = 0; s < nseg; ++s)
+      total += h_offsets[s + 1] > h_offsets[s] ? h_offsets[s + 1] - h_offsets[s] : 0;
+    c->last_device_terms = dev_terms;
+    c->last_host_terms = total - dev_terms;
   }
   cudaSetDevice(prev);
   return st;

@@ -231,11 +231,16 @@ void Acc::add(const double *x, size_t n, uint64_t gbase) {
 
 void Acc::finish(exsum_partial *out) {
   for (int c = 0; c < kCopies; ++c)
-    for (uint32_t ix = 0; ix < 4096; ++ix)
-      if (bin[c][ix]) {
-        transfer(ix, bin[c][ix], 0);
-        bin[c][ix] = 0;
-      }
+    for (uint32_t g = 0; g < 4096; g += 8) {
+      uint64_t any = 0;
+      for (int k = 0; k < 8; ++k) any |= bin[c][g + k];
+      if (!any) continue;  // most groups are empty for narrow data
+      for (uint32_t ix = g; ix < g + 8; ++ix)
+        if (bin[c][ix]) {
+          transfer(ix, bin[c][ix], 0);
+          bin[c][ix] = 0;
+        }
+    }
   std::memset(out, 0, sizeof *out);
   std::memcpy(out->acc.chunk, chunk, sizeof chunk);
   exsum_canonicalize(out->acc.chunk);
@@ -245,6 +250,18 @@ void Acc::finish(exsum_partial *out) {
   out->first_neg_inf = M;
   out->first_nan = N;
   out->nan_payload = payload;
+}
+
+void Acc::segment(const double *x, uint64_t b, uint64_t e, double *out, exsum_partial *part) {
+  std::memset(chunk, 0, sizeof chunk);
+  transfers = 0;
+  P = M = N = kNoIndex;
+  payload = 0;
+  if (e > b) add(x + b, e - b, 0);
+  exsum_partial rec;
+  finish(&rec);
+  if (part) *part = rec;
+  exsum_partial_round(&rec, out);
 }
 
 int default_threads() {
@@ -278,7 +295,26 @@ bool Pool::ok() const {
   return true;
 }
 
+void Pool::run_segments(int t) {
+  EXSUM_NVTX("exsum_host: worker segments");
+  Acc *a = accs_[static_cast<size_t>(t)];
+  a->reset();
+  for (;;) {
+    const size_t s0 = job_.cursor->fetch_add(job_.grain, std::memory_order_relaxed);
+    if (s0 >= job_.n) break;
+    const size_t s1 = job_.n - s0 < job_.grain ? job_.n : s0 + job_.grain;
+    for (size_t s = s0; s < s1; ++s) {
+      const uint64_t b = job_.offs[s], e = job_.offs[s + 1];
+      a->segment(job_.x, b, e < b ? b : e, job_.out + s, job_.partials ? job_.partials + s : nullptr);
+    }
+  }
+}
+
 void Pool::run_share(int t) {
+  if (job_.offs) {
+    run_segments(t);
+    return;
+  }
   EXSUM_NVTX("exsum_host: worker share");
   Acc *a = accs_[static_cast<size_t>(t)];
   a->reset();
@@ -315,6 +351,26 @@ void Pool::start(const double *x, size_t n, uint64_t base, std::atomic<size_t> *
   empty.first_pos_inf = empty.first_neg_inf = empty.first_nan = kNoIndex;
   parts_.assign(accs_.size(), empty);
   job_ = Job{x, n, base, cursor, grain ? grain : (size_t{1} << 18)};
+  pending_.store(static_cast<int>(threads_.size()), std::memory_order_relaxed);
+  {
+    std::lock_guard<std::mutex> lk(m_);
+    ++gen_;
+  }
+  cv_.notify_all();
+}
+
+void Pool::start_segments(const double *x, const uint64_t *offs, size_t nseg,
+                          std::atomic<size_t> *cursor, size_t grain, double *out,
+                          exsum_partial *partials) {
+  Job j;
+  j.x = x;
+  j.n = nseg;
+  j.cursor = cursor;
+  j.grain = grain ? grain : 4;
+  j.offs = offs;
+  j.out = out;
+  j.partials = partials;
+  job_ = j;
   pending_.store(static_cast<int>(threads_.size()), std::memory_order_relaxed);
   {
     std::lock_guard<std::mutex> lk(m_);

@@ -32,8 +32,12 @@ struct alignas(64) Acc {
   void reset();
   // x[0..n) with global indices gbase .. gbase + n - 1
   void add(const double *x, size_t n, uint64_t gbase);
-  // drain the bins; the canonical record with index-resolved Inf/NaN
+  // drain the bins; the canonical record with index-resolved Inf/NaN (leaves
+  // every bin zero again)
   void finish(exsum_partial *out);
+  // One exact_sum of x[b, e) (indices local to the segment) into *out (and
+  // *part); the bins must be zero on entry (reset(), or a previous finish()).
+  void segment(const double *x, uint64_t b, uint64_t e, double *out, exsum_partial *part);
 
  private:
   void transfer(uint32_t ix, uint64_t v, uint64_t carry);
@@ -63,6 +67,11 @@ class Pool {
   // may call run_share(0) itself, then join_helpers().
   void start(const double *x, size_t n, uint64_t base, std::atomic<size_t> *cursor,
              size_t grain);
+  // Hybrid segmented sum: helpers claim `grain` segments at a time from the
+  // shared segment cursor and write out[s] (and partials[s]) themselves.
+  void start_segments(const double *x, const uint64_t *offs, size_t nseg,
+                      std::atomic<size_t> *cursor, size_t grain, double *out,
+                      exsum_partial *partials);
   void run_share(int t);
   void join_helpers();
   std::vector<exsum_partial> &parts() { return parts_; }
@@ -71,11 +80,15 @@ class Pool {
  private:
   struct Job {
     const double *x = nullptr;
-    size_t n = 0;
+    size_t n = 0;  // terms, or segments for a segmented job
     uint64_t base = 0;
     std::atomic<size_t> *cursor = nullptr;
     size_t grain = 0;
+    const uint64_t *offs = nullptr;  // segmented job: nseg + 1 offsets
+    double *out = nullptr;
+    exsum_partial *partials = nullptr;
   };
+  void run_segments(int t);
   void worker(int t);
 
   std::vector<Acc *> accs_;

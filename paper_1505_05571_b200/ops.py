@@ -280,6 +280,23 @@ class HostContext:
                       C.byref(part) if want_partial else None)
         return (out.value, part) if want_partial else out.value
 
+    def sum_segmented(self, values, offsets, want_partials: bool = False):
+        """One exact sum per segment of a host array (exsum_context_sum_segmented):
+        values[offsets[i]:offsets[i+1]] for every i.  Returns a float64 numpy array
+        (and the raw [nseg, 592] uint8 records when want_partials)."""
+        x = values.numpy() if isinstance(values, torch.Tensor) else values
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+        o = offsets.numpy() if isinstance(offsets, torch.Tensor) else offsets
+        o = np.ascontiguousarray(o).astype(np.uint64, copy=False).reshape(-1)
+        nseg = max(o.size - 1, 0)
+        out = np.empty(nseg, dtype=np.float64)
+        parts = np.empty((nseg, PARTIAL_BYTES), dtype=np.uint8) if want_partials else None
+        if nseg:
+            with self._lock:
+                _lib.call("exsum_context_sum_segmented", self._h, x.ctypes.data, o.ctypes.data,
+                          nseg, out.ctypes.data, parts.ctypes.data if want_partials else None)
+        return (out, parts) if want_partials else out
+
     def sum_file(self, path, fmt: str = "bin", want_partial: bool = False):
         """exact_sum(read_values(path, fmt)) — a bin file streams from disk through
         pinned buffers into the device accumulate.  Returns (result, n[, partial])."""

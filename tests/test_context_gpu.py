@@ -184,3 +184,63 @@ def test_exact_mean_specials_and_small(cuda, checker):
         assert bits_of(ops.exact_mean(torch.from_numpy(x).cuda())) == bits_of(checker.exact_mean(x))
     with pytest.raises(ValueError):
         ops.exact_mean(torch.empty(0, dtype=torch.float64, device="cuda"))
+
+
+# ----------------------------------------------- segmented sums of host arrays
+
+def _seg_ref(x, offs, partials=False):
+    """The device path on the same data (itself checked against the reference in
+    test_gpu.py) — bits and records must not depend on the host/device split."""
+    d = torch.from_numpy(x).cuda()
+    o = torch.from_numpy(offs.astype(np.int64)).cuda()
+    if partials:
+        r, p = ops.exact_sum_segmented(d, o, partials=True)
+        return r.cpu().numpy(), p.cpu().numpy()
+    return ops.exact_sum_segmented(d, o).cpu().numpy()
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_context_segmented_config5(cuda, checker, pinned):
+    nseg = 8192
+    offs = port.gen_offsets(3, nseg)
+    n = int(offs[-1])
+    x = port.gen(5, 3, 0, 0, n)
+    if pinned:
+        t = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        t.numpy()[:] = x
+        x = t.numpy()
+    want, wparts = _seg_ref(x, offs, partials=True)
+    ctx = ops.HostContext(0, staging_bytes=48 << 20)
+    got, parts = ctx.sum_segmented(x, offs, want_partials=True)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(parts, wparts)
+    d, h = ctx.last_split()
+    assert d + h == n and d > 0 and h > 0, (d, h)
+    # first 300 segments against the reference itself
+    m = 300
+    ref = checker.segmented_sum(x[: int(offs[m])], offs[: m + 1])
+    assert np.array_equal(got[:m].view(np.uint64), ref.view(np.uint64))
+    for threads in (0, 3):
+        ctx.set_host_threads(threads)
+        assert np.array_equal(ctx.sum_segmented(x, offs).view(np.uint64), want.view(np.uint64))
+
+
+def test_context_segmented_edges(cuda, checker):
+    """Empty and decreasing pairs, a segment longer than one staging chunk
+    (streamed alone through the incremental path), specials, tiny input."""
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal(3_000_000) * 10.0 ** rng.integers(-30, 30, 3_000_000)
+    x[17] = np.inf
+    x[2_500_000] = np.nan
+    offs = np.array([0, 0, 10, 5, 1_000, 2_600_000, 2_600_000, 2_999_999, 3_000_000],
+                    dtype=np.uint64)
+    want, wparts = _seg_ref(x, offs, partials=True)
+    ctx = ops.HostContext(0, staging_bytes=6 << 20)  # 2 MB chunks: 2.6e6-term segment is long
+    for threads in (-1, 0, 2):
+        ctx.set_host_threads(threads)
+        got, parts = ctx.sum_segmented(x, offs, want_partials=True)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), threads
+        assert np.array_equal(parts, wparts), threads
+    small = ctx.sum_segmented(np.array([1.0, 2.0, 3.0]), np.array([0, 1, 3], dtype=np.uint64))
+    assert list(small) == [1.0, 5.0]
+    assert ctx.sum_segmented(np.zeros(0), np.zeros(1, dtype=np.uint64)).size == 0
