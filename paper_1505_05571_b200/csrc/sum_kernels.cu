@@ -1433,12 +1433,24 @@ __global__ void exsum_finalize_kernel(Workspace *ws, double *result, exsum_parti
 //            per CTA to reserve its range, order[base + rank] = segment.
 // Order within a bucket is arbitrary, which cannot change any result (each
 // segment is summed by one warp either way).
+// Windows (round 2): longest-first over the whole list scatters the warps'
+// concurrent segments across the array, and the step time then varied run to
+// run (2.11-2.77 ms on config 5) while index order was steady but kept a long
+// tail.  The list is cut into kSegWindows windows of consecutive segments,
+// claimed window after window, longest first within each: the working set
+// stays inside one window and the finish is still set by short segments.
+#ifndef EXSUM_SEG_WINDOWS
+#define EXSUM_SEG_WINDOWS 4
+#endif
 constexpr int kOrderThreads = 1024;
 constexpr int kOrderBuckets = 512;
+constexpr int kSegWindows = EXSUM_SEG_WINDOWS;
+constexpr int kOrderKeys = kOrderBuckets * kSegWindows;
+static_assert(kOrderKeys % 32 == 0, "one warp scans the keys");
 constexpr unsigned long long kOrderMaxSegs = 1ull << 24;  // beyond: index order
 struct OrderState {                    // zeroed by exsum_cuda_workspace_init
-  unsigned int hist[kOrderBuckets];    // counts (zero between calls)
-  unsigned int base[kOrderBuckets];    // bucket cursors of the current call
+  unsigned int hist[kOrderKeys];       // counts (zero between calls)
+  unsigned int base[kOrderKeys];       // bucket cursors of the current call
   unsigned int done;                   // hist CTAs finished (zero between calls)
   unsigned int pad_[63];
 };
@@ -1455,18 +1467,24 @@ __device__ __forceinline__ int length_bucket(unsigned long long len) {
   return msb * 8 + static_cast<int>((len >> (msb - 3)) & 7u);
 }
 
+// key of segment s: its window, then its length bucket
+__device__ __forceinline__ int order_key(const unsigned long long *offs, unsigned long long s,
+                                         unsigned long long wsegs) {
+  return static_cast<int>(s / wsegs) * kOrderBuckets + length_bucket(offs[s + 1] - offs[s]);
+}
+
 __global__ void __launch_bounds__(kOrderThreads)
 exsum_segment_hist_kernel(const unsigned long long *__restrict__ offs, unsigned long long nseg,
-                          OrderState *st) {
-  __shared__ unsigned int h[kOrderBuckets];
+                          unsigned long long wsegs, OrderState *st) {
+  __shared__ unsigned int h[kOrderKeys];
   __shared__ bool last;
   const unsigned t = threadIdx.x;
-  for (unsigned k = t; k < kOrderBuckets; k += kOrderThreads) h[k] = 0u;
+  for (unsigned k = t; k < kOrderKeys; k += kOrderThreads) h[k] = 0u;
   __syncthreads();
   const unsigned long long s = static_cast<unsigned long long>(blockIdx.x) * kOrderThreads + t;
-  if (s < nseg) atomicAdd(&h[length_bucket(offs[s + 1] - offs[s])], 1u);
+  if (s < nseg) atomicAdd(&h[order_key(offs, s, wsegs)], 1u);
   __syncthreads();
-  for (unsigned k = t; k < kOrderBuckets; k += kOrderThreads)
+  for (unsigned k = t; k < kOrderKeys; k += kOrderThreads)
     if (h[k]) atomicAdd(&st->hist[k], h[k]);
   __threadfence();
   __syncthreads();
@@ -1474,27 +1492,28 @@ exsum_segment_hist_kernel(const unsigned long long *__restrict__ offs, unsigned 
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // base[k] := number of segments in buckets above k (descending lengths).
-  // 512 counts, one warp: each lane owns 16 consecutive buckets.
+  // Claim position o runs over windows ascending and, within a window, buckets
+  // descending: key(o) = (o / 512) * 512 + 511 - o % 512.  base[key(o)] = the
+  // number of segments at positions before o.  One warp: lane t owns positions
+  // [P t, P t + P).
   if (t < 32) {
-    unsigned v[16], sum = 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      v[i] = __ldcg(&st->hist[16 * t + i]);
-      st->hist[16 * t + i] = 0u;
-      sum += v[i];
-    }
-    unsigned above = sum;  // inclusive suffix sum over lanes >= t
+    constexpr int P = kOrderKeys / 32;
+    auto key_of = [](int o) { return (o / kOrderBuckets) * kOrderBuckets + kOrderBuckets - 1 - o % kOrderBuckets; };
+    unsigned sum = 0;
+    for (int i = 0; i < P; ++i) sum += __ldcg(&st->hist[key_of(P * t + i)]);
+    unsigned before = sum;  // inclusive prefix over lanes <= t
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const unsigned w = __shfl_down_sync(0xffffffffu, above, o);
-      if (t + o < 32) above += w;
+      const unsigned w = __shfl_up_sync(0xffffffffu, before, o);
+      if (t >= o) before += w;
     }
-    above -= sum;  // buckets of higher lanes
-#pragma unroll
-    for (int i = 15; i >= 0; --i) {
-      st->base[16 * t + i] = above;
-      above += v[i];
+    before -= sum;
+    for (int i = 0; i < P; ++i) {
+      const int k = key_of(P * t + i);
+      const unsigned v = __ldcg(&st->hist[k]);
+      st->hist[k] = 0u;
+      st->base[k] = before;
+      before += v;
     }
     if (t == 0) st->done = 0u;
   }
@@ -1502,20 +1521,21 @@ exsum_segment_hist_kernel(const unsigned long long *__restrict__ offs, unsigned 
 
 __global__ void __launch_bounds__(kOrderThreads)
 exsum_segment_scatter_kernel(const unsigned long long *__restrict__ offs, unsigned long long nseg,
-                             OrderState *st, unsigned int *__restrict__ order) {
-  __shared__ unsigned int cnt[kOrderBuckets];
+                             unsigned long long wsegs, OrderState *st,
+                             unsigned int *__restrict__ order) {
+  __shared__ unsigned int cnt[kOrderKeys];
   const unsigned t = threadIdx.x;
-  for (unsigned k = t; k < kOrderBuckets; k += kOrderThreads) cnt[k] = 0u;
+  for (unsigned k = t; k < kOrderKeys; k += kOrderThreads) cnt[k] = 0u;
   __syncthreads();
   const unsigned long long s = static_cast<unsigned long long>(blockIdx.x) * kOrderThreads + t;
   int key = 0;
   unsigned r = 0;
   if (s < nseg) {
-    key = length_bucket(offs[s + 1] - offs[s]);
+    key = order_key(offs, s, wsegs);
     r = atomicAdd(&cnt[key], 1u);
   }
   __syncthreads();
-  for (unsigned k = t; k < kOrderBuckets; k += kOrderThreads)
+  for (unsigned k = t; k < kOrderKeys; k += kOrderThreads)
     if (cnt[k]) cnt[k] = atomicAdd(&st->base[k], cnt[k]);  // this CTA's range in bucket k
   __syncthreads();
   if (s < nseg) order[cnt[key] + r] = static_cast<unsigned>(s);
@@ -2014,10 +2034,11 @@ int exsum_cuda_sum_segmented(const double *d_x, const uint64_t *d_offsets, size_
     auto *st = reinterpret_cast<OrderState *>(base + kOrderStateOffset);
     order = reinterpret_cast<unsigned int *>(base + kOrderOffset);
     const unsigned og = static_cast<unsigned>((nseg + kOrderThreads - 1) / kOrderThreads);
+    const unsigned long long wsegs = (nseg + kSegWindows - 1) / kSegWindows;
     exsum_segment_hist_kernel<<<og, kOrderThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-        offs, nseg, st);
+        offs, nseg, wsegs, st);
     exsum_segment_scatter_kernel<<<og, kOrderThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-        offs, nseg, st, order);
+        offs, nseg, wsegs, st, order);
   }
   // Deferred rounding: raw records go to d_partials when the caller wants them,
   // else to the workspace after the claim order (when it has room).
