@@ -79,6 +79,10 @@
 #ifndef EXSUM_UNIFORM_FAST
 #define EXSUM_UNIFORM_FAST 1  // single-sum kernel: register fast path for one-slot batches
 #endif
+#ifndef EXSUM_FP64_DECODE
+#define EXSUM_FP64_DECODE 0  // general path: slot value by FP64 scaling + conversions (idle FP64
+                             // and conversion pipes) instead of the integer decode
+#endif
 #ifndef EXSUM_XOR_LOP
 #define EXSUM_XOR_LOP 1  // sign complement with two LOP3 (ALU) instead of LEA + 2 IMAD (FMA)
 #endif
@@ -292,6 +296,73 @@ __device__ __forceinline__ void slot_add96(const Lane &a, uint32_t k, uint32_t v
 
 // Add one term (exponent field e != 2047, or 2047 for the blind add of an
 // Inf/NaN that the batch fix-up cancels) to the lane's slots.
+#if EXSUM_FP64_DECODE
+// The slot value of x as a signed 96-bit integer h * 2^32 + u0 computed on the
+// FP64 and conversion pipes: slot k = e >> 5 (e = 0 and 1 share slot 0), value
+// y = x * 2^(1075 - 32k) = s m 2^(e' & 31) — the integer decode's value.
+// t = y / 2^32 = (x * 2^(1011 - 32k)) * 2^32: both products exact (x * A_k lies
+// in [2^-63, 2^20) for every finite x of slot k, denormals included), then
+// h = floor(t) and u0 = (t - h) * 2^32, both exact integers.  An Inf/NaN decodes
+// to garbage (saturated / zero conversions) that cancel_term removes exactly.
+__device__ __forceinline__ void decode_fp64(uint32_t lo, uint32_t hi, uint32_t e, uint32_t &k,
+                                            uint32_t &u0, long long &h) {
+  k = e >> 5;
+  uint32_t ahi;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ahi) : "r"(k), "r"(0xFE000000u), "r"(2034u << 20));
+  const double A = __hiloint2double(static_cast<int>(ahi), 0);
+  const double x = __hiloint2double(static_cast<int>(hi), static_cast<int>(lo));
+  const double t = __dmul_rn(__dmul_rn(x, A), 4294967296.0);
+#if EXSUM_FP64_DECODE == 2
+  // low word on the integer pipes: (m << (e' & 31)) mod 2^32, negated for x < 0
+  // (the two's complement's low word; h = floor(t) is the matching high part)
+  uint32_t ep, w, sg;
+  asm("max.u32 %0, %1, 1;" : "=r"(ep) : "r"(e));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(w) : "r"(0u), "r"(lo), "r"(ep));
+  asm("shr.s32 %0, %1, 31;" : "=r"(sg) : "r"(hi));
+  u0 = (w ^ sg) - sg;
+  h = __double2ll_rd(t);
+#else
+  const double th = floor(t);
+  u0 = __double2uint_rz(__dmul_rn(__dsub_rn(t, th), 4294967296.0));
+  h = __double2ll_rz(th);
+#endif
+}
+
+__device__ __forceinline__ void slot_add_h(const Lane &a, uint32_t k, uint32_t u0, long long h) {
+  uint32_t la, ha;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(k), "r"(a.c128), "r"(a.sl));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));
+  asm volatile(
+      "{\n\t.reg .u32 l, h0, h1;\n\t"
+      "ld.shared.u32 l, [%0];\n\t"
+      "ld.shared.v2.u32 {h0, h1}, [%1];\n\t"
+      "add.cc.u32 l, l, %2;\n\t"
+      "addc.cc.u32 h0, h0, %3;\n\t"
+      "addc.u32 h1, h1, %4;\n\t"
+      "st.shared.u32 [%0], l;\n\t"
+      "st.shared.v2.u32 [%1], {h0, h1};\n\t}"
+      :
+      : "r"(la), "r"(ha), "r"(u0), "r"(static_cast<uint32_t>(h)),
+        "r"(static_cast<uint32_t>(static_cast<unsigned long long>(h) >> 32))
+      : "memory");
+}
+
+__device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
+  uint32_t k, u0;
+  long long h;
+  decode_fp64(lo, hi, e, k, u0, h);
+  slot_add_h(a, k, u0, h);
+}
+
+// Remove exactly what add_term added for the term (lo, hi): its decode negated.
+__device__ __forceinline__ void cancel_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
+  uint32_t k, u0;
+  long long h;
+  decode_fp64(lo, hi, e, k, u0, h);
+  // -(h 2^32 + u0) = (-h - (u0 != 0)) 2^32 + (-u0 mod 2^32)
+  slot_add_h(a, k, 0u - u0, -h - (u0 != 0u ? 1 : 0));
+}
+#else
 __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
   uint32_t s, ep, k, la, ha, u0, u1, u2;
   decode96(lo, hi, e, s, u0, u1, u2, ep);
@@ -312,6 +383,13 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
       : "r"(la), "r"(ha), "r"(s), "r"(u0), "r"(u1), "r"(u2)
       : "memory");
 }
+
+// Remove the blind add of an Inf/NaN term: its sign-flipped twin decodes to the
+// exact negation (modular slot arithmetic).
+__device__ __forceinline__ void cancel_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
+  add_term(a, lo, hi ^ 0x80000000u, e);
+}
+#endif
 
 // Carry upward: L_k in [0, 2^32), H_k = 0 below the top slot, which keeps the
 // rest (with 65 slots: slot 64 holds up to 2^95 units of 2^973 > any finite
@@ -656,7 +734,7 @@ __device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, cons
           EXSUM_FIX_L1 ? __ldg(xb + 4 * vec + q) : __ldcg(xb + 4 * vec + q);
       const uint32_t lo = static_cast<uint32_t>(bits), hi = static_cast<uint32_t>(bits >> 32);
       record_special(sp, lo, hi, ib + 4ull * static_cast<unsigned long long>(vec) + q);
-      add_term(a, lo, hi ^ 0x80000000u, 0x7FFu);  // cancel the garbage add
+      cancel_term(a, lo, hi, 0x7FFu);  // cancel the garbage add
     }
   } else {
 #pragma unroll 1
@@ -674,7 +752,7 @@ __device__ __forceinline__ void fixup_specials(const Lane &a, Specials &sp, cons
           const unsigned long long t = kOp == kSum ? xv : x86_product(xv, yv);
           record_special(sp, static_cast<uint32_t>(t), static_cast<uint32_t>(t >> 32),
                          ib + 4ull * static_cast<unsigned long long>(vec) + q);
-          add_term(a, lo, hi ^ 0x80000000u, 0x7FFu);  // cancel the garbage add
+          cancel_term(a, lo, hi, 0x7FFu);  // cancel the garbage add
         }
       }
     }
