@@ -1,0 +1,6 @@
+mkdir -p gpurun_out/final
+timeout 1500 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/final/gpu_tests.log 2>&1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1
+timeout 600 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > gpurun_out/final/ref.json 2>&1
+timeout 600 python bench.py --gpus 1 --steps 20 --warmup 5 > gpurun_out/final/bench.json 2> gpurun_out/final/bench.err
+true

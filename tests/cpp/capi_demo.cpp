@@ -67,6 +67,12 @@ static int host_checks() {
   CHECK(exsum_small_init(&acc) == EXSUM_OK);
   CHECK(exsum_small_add_array(&acc, z, 3) == EXSUM_OK);
   CHECK(exsum_small_round(&acc, &out) == EXSUM_OK && bits(out) == 0x7FF0000000000123ull);
+  // the library's multithreaded host kernel and the paper's generator (zero sum)
+  std::vector<double> g(200'000);
+  CHECK(exsum_generate(g.size(), 5, 1, g.data()) == EXSUM_OK);
+  CHECK(exsum_generate(3, 5, 0, g.data()) == EXSUM_EINVAL);
+  CHECK(exsum_host_sum(g.data(), g.size(), 0, 4, &out, nullptr) == EXSUM_OK && bits(out) == 0);
+  CHECK(exsum_host_sum(w, 3, 0, 1, &out, nullptr) == EXSUM_OK && out == 1.0);
   std::printf("host ok (%s)\n", exsum_version());
   return 0;
 }
@@ -86,6 +92,21 @@ static int device_checks() {
   CHECK(exsum_large_round(L, &host) == EXSUM_OK);
   exsum_large_free(L);
   CHECK(bits(dev) == bits(host));
+  // the same call split between the device and 3 host workers, and device only
+  uint64_t dterms = 0, hterms = 0;
+  CHECK(exsum_context_set_host_threads(ctx, 3) == EXSUM_OK);
+  CHECK(exsum_context_sum(ctx, x.data(), n, &dev, nullptr) == EXSUM_OK && bits(dev) == bits(host));
+  CHECK(exsum_context_last_split(ctx, &dterms, &hterms) == EXSUM_OK && dterms + hterms == n);
+  CHECK(exsum_context_set_host_threads(ctx, 0) == EXSUM_OK);
+  CHECK(exsum_context_sum(ctx, x.data(), n, &dev, nullptr) == EXSUM_OK && bits(dev) == bits(host));
+  CHECK(exsum_context_last_split(ctx, &dterms, &hterms) == EXSUM_OK && dterms == n);
+  // segmented host arrays: three segments, one empty
+  const uint64_t offs[4] = {0, 1000, 1000, n};
+  double sums[3];
+  CHECK(exsum_context_sum_segmented(ctx, x.data(), offs, 3, sums, nullptr) == EXSUM_OK);
+  double s0 = 0;
+  CHECK(exsum_host_sum(x.data(), 1000, 0, 1, &s0, nullptr) == EXSUM_OK && bits(sums[0]) == bits(s0));
+  CHECK(bits(sums[1]) == 0);
   exsum_context_free(ctx);
   std::printf("device ok: %016llx\n", static_cast<unsigned long long>(bits(dev)));
   return 0;
