@@ -224,8 +224,10 @@ typedef struct exsum_context exsum_context;
 exsum_context *exsum_context_create(int device, size_t staging_bytes);
 void exsum_context_free(exsum_context *ctx);
 /* Host workers beside the device: < 0 = every hardware thread (default),
- * 0 = device only (PCIe-bound), k = k threads.  Arrays under 2^20 terms are
- * always summed on the device alone. */
+ * 0 = device only (PCIe-bound, every size), k = k threads.  With workers
+ * enabled, an array (or segment list) under 2^17 terms is summed by the
+ * calling thread alone: the device round trip (~35 us) costs more than the
+ * whole sum on one core. */
 int exsum_context_set_host_threads(exsum_context *ctx, int threads);
 /* Terms the last successful sum gave the device and the host workers. */
 int exsum_context_last_split(const exsum_context *ctx, uint64_t *device_terms,

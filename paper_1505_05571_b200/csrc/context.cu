@@ -41,6 +41,12 @@ constexpr int kSlots = 4;     // device staging buffers
 constexpr int kInFlight = 3;  // chunks claimed by the feeder and not yet copied (DMA queue
                               // depth: covers the feeder's wake-up latency among busy workers)
 constexpr size_t kHostGrain = size_t{1} << 18;  // terms per host-worker claim (2 MB)
+// Below this many terms a host array is summed by the calling thread alone: the
+// device round trip (~35 us: copy, accumulate, finalize, readback) and a worker
+// wake-up cost more than the whole sum on one core (profiles/r02_latency_probe.log:
+// 1e3 / 1e4 / 1e5 terms: device 37 / 49 / 99 us, one core 4 / 8 / 46 us).
+// exsum_context_set_host_threads(ctx, 0) keeps every size on the device.
+constexpr size_t kHostOnlyTerms = size_t{1} << 17;
 }  // namespace
 
 struct exsum_context {
@@ -58,6 +64,7 @@ struct exsum_context {
   double *host[kSlots] = {};           // pinned bounce buffers (pageable input, files)
   int host_threads = -1;               // < 0: all hardware threads; 0: device only
   exsum_host::Pool *pool = nullptr;
+  exsum_host::Acc *small = nullptr;  // the calling thread's accumulator for small arrays
   uint64_t last_device_terms = 0, last_host_terms = 0;
   // segmented sums of host arrays (allocated on first use)
   void *seg_ws = nullptr;
@@ -72,6 +79,7 @@ namespace {
 void destroy(exsum_context *c) {
   if (!c) return;
   delete c->pool;
+  delete c->small;
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(c->device);
@@ -271,15 +279,26 @@ int exsum_context_sum_at(exsum_context *c, const double *h_x, size_t n, uint64_t
   EXSUM_NVTX("exsum_context_sum");
   if (!c || (n && !h_x) || (!h_result && !h_partial)) return EXSUM_EINVAL;
   std::lock_guard<std::mutex> lk(c->busy);
+  if (n < kHostOnlyTerms && c->host_threads != 0) {
+    if (!c->small && !(c->small = new (std::nothrow) exsum_host::Acc)) return EXSUM_ENOMEM;
+    exsum_partial rec;
+    c->small->reset();
+    c->small->add(h_x, n, base_index);
+    c->small->finish(&rec);
+    if (h_partial) *h_partial = rec;
+    if (h_result) exsum_partial_round(&rec, h_result);
+    c->last_device_terms = 0;
+    c->last_host_terms = n;
+    return EXSUM_OK;
+  }
   int prev = 0;
   cudaGetDevice(&prev);
   if (cudaSetDevice(c->device) != cudaSuccess) return EXSUM_ECUDA;
   const bool pinned = n == 0 || is_pinned(h_x);
   int st = pinned ? EXSUM_OK : ensure_bounce(c);
   // host workers: every hardware thread by default (the feeder mostly sleeps in
-  // blocking event waits); none for arrays too small to amortise a wake-up
+  // blocking event waits)
   int workers = c->host_threads < 0 ? exsum_host::default_threads() : c->host_threads;
-  if (n < (size_t{1} << 20)) workers = 0;
   if (st == EXSUM_OK && workers > 0 && (!c->pool || c->pool->size() != workers + 1)) {
     delete c->pool;
     c->pool = new (std::nothrow) exsum_host::Pool(workers + 1);  // slot 0: the feeder
@@ -294,9 +313,11 @@ int exsum_context_sum_at(exsum_context *c, const double *h_x, size_t n, uint64_t
   if (st == EXSUM_OK && hybrid) c->pool->start(h_x, n, base_index, &cursor, kHostGrain);
   uint64_t dev_terms = 0;
   if (st == EXSUM_OK) dev_terms = feed_device(c, h_x, n, base_index, &cursor, pinned, hybrid, &st);
-  if (st == EXSUM_OK)
+  // the device's record (skipped when the host workers left it nothing)
+  const bool dev_part = dev_terms > 0 || !hybrid;
+  if (st == EXSUM_OK && dev_part)
     st = exsum_cuda_finalize(c->d_result, c->d_partial, c->ws, c->ws_bytes, c->compute);
-  if (st == EXSUM_OK &&
+  if (st == EXSUM_OK && dev_part &&
       cudaMemcpyAsync(c->h_partial, c->d_partial, sizeof(exsum_partial), cudaMemcpyDeviceToHost,
                       c->compute) != cudaSuccess)
     st = EXSUM_ECUDA;
@@ -308,7 +329,7 @@ int exsum_context_sum_at(exsum_context *c, const double *h_x, size_t n, uint64_t
     exsum_partial merged;
     if (hybrid) {
       auto &parts = c->pool->parts();
-      parts[0] = *c->h_partial;
+      if (dev_part) parts[0] = *c->h_partial;  // else parts[0] is the empty record
       exsum_partial_merge(parts.data(), parts.size(), &merged, nullptr);
     } else {
       merged = *c->h_partial;
@@ -344,7 +365,23 @@ int exsum_context_sum_segmented(exsum_context *c, const double *h_x, const uint6
   int st = ensure_segmented(c, h_partials != nullptr);
   if (st == EXSUM_OK && !pinned) st = ensure_bounce(c);
   int workers = c->host_threads < 0 ? exsum_host::default_threads() : c->host_threads;
-  if (hi - lo < (uint64_t{1} << 20)) workers = 0;
+  if (st == EXSUM_OK && hi - lo < kHostOnlyTerms && c->host_threads != 0) {
+    // a small segment list: the calling thread alone (see kHostOnlyTerms)
+    if (!c->small && !(c->small = new (std::nothrow) exsum_host::Acc)) st = EXSUM_ENOMEM;
+    if (st == EXSUM_OK) {
+      c->small->reset();
+      uint64_t total = 0;
+      for (size_t s = 0; s < nseg; ++s) {
+        const uint64_t b = h_offsets[s], e = h_offsets[s + 1];
+        c->small->segment(h_x, b, e < b ? b : e, h_out + s, h_partials ? h_partials + s : nullptr);
+        total += e > b ? e - b : 0;
+      }
+      c->last_device_terms = 0;
+      c->last_host_terms = total;
+    }
+    cudaSetDevice(prev);
+    return st;
+  }
   if (st == EXSUM_OK && workers > 0 && (!c->pool || c->pool->size() != workers + 1)) {
     delete c->pool;
     c->pool = new (std::nothrow) exsum_host::Pool(workers + 1);

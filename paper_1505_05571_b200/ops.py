@@ -238,6 +238,7 @@ class HostContext:
     def __init__(self, device: int = 0, staging_bytes: int = 256 << 20, host_threads: int = -1):
         self.device = device
         self._lock = threading.Lock()
+        self._free = lib.exsum_context_free  # kept: module globals may be gone at exit
         self._h = lib.exsum_context_create(device, staging_bytes)
         if not self._h:
             raise _lib.ExsumError("exsum_context_create", _lib.EXSUM_ECUDA)
@@ -246,7 +247,7 @@ class HostContext:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib.exsum_context_free(h)
+            self._free(h)
             self._h = None
 
     def set_host_threads(self, threads: int) -> None:

@@ -54,7 +54,13 @@ def test_golden_device_sum(golden, cuda):
 
 
 def test_golden_host_buffers(golden, cuda):
-    ctx = ops.HostContext(0, staging_bytes=1 << 20)  # tiny ring: many pipelined chunks
+    # device only (host_threads=0): every golden array through the staging ring
+    ctx = ops.HostContext(0, staging_bytes=1 << 20, host_threads=0)  # tiny ring: many chunks
+    for c in golden:
+        assert bits_of(ctx.sum(c["x"])) == c["large"], c["tag"]
+        assert ctx.last_split() == (c["x"].size, 0)
+    # default policy: arrays under 2^17 terms are summed by the calling thread
+    ctx.set_host_threads(-1)
     for c in golden:
         assert bits_of(ctx.sum(c["x"])) == c["large"], c["tag"]
     assert bits_of(ops.exact_sum(golden[5]["x"])) == golden[5]["large"]
