@@ -1590,18 +1590,20 @@ __global__ void exsum_finalize_kernel(Workspace *ws, double *result, exsum_parti
 //            per CTA to reserve its range, order[base + rank] = segment.
 // Order within a bucket is arbitrary, which cannot change any result (each
 // segment is summed by one warp either way).
-// Windows (round 2): longest-first over the whole list scatters the warps'
-// concurrent segments across the array, and the step time then varied run to
-// run (2.11-2.77 ms on config 5) while index order was steady but kept a long
-// tail.  The list is cut into kSegWindows windows of consecutive segments,
-// claimed window after window, longest first within each: the working set
-// stays inside one window and the finish is still set by short segments.
-#ifndef EXSUM_SEG_WINDOWS
-#define EXSUM_SEG_WINDOWS 4
+// Tail-sorted order (round 2): longest-first over the WHOLE list scatters the
+// warps' concurrent segments across the array; its step time varied run to run
+// (2.11-2.8 ms on config 5, with rare 4.5-7.7 ms outliers at low power, i.e.
+// memory-side stalls) while index order was steady (2.18 ms) but ended on a
+// long tail.  So: segments before tail_start keep index order (one key, ranks
+// by CTA: a sliding, contiguous working set), and only the last
+// EXSUM_SEG_TAIL x (warps in the grid) segments are claimed longest first, which
+// bounds the finish by short segments.  (kSegWindows = 2: head, tail.)
+#ifndef EXSUM_SEG_TAIL
+#define EXSUM_SEG_TAIL 4  // tail of the claim order sorted longest first, in segments per warp
 #endif
 constexpr int kOrderThreads = 1024;
 constexpr int kOrderBuckets = 512;
-constexpr int kSegWindows = EXSUM_SEG_WINDOWS;
+constexpr int kSegWindows = 2;  // head (index order), tail (longest first)
 constexpr int kOrderKeys = kOrderBuckets * kSegWindows;
 static_assert(kOrderKeys % 32 == 0, "one warp scans the keys");
 constexpr unsigned long long kOrderMaxSegs = 1ull << 24;  // beyond: index order
@@ -1624,22 +1626,22 @@ __device__ __forceinline__ int length_bucket(unsigned long long len) {
   return msb * 8 + static_cast<int>((len >> (msb - 3)) & 7u);
 }
 
-// key of segment s: its window, then its length bucket
+// key of segment s: head segments share key 0; tail segments their length bucket
 __device__ __forceinline__ int order_key(const unsigned long long *offs, unsigned long long s,
-                                         unsigned long long wsegs) {
-  return static_cast<int>(s / wsegs) * kOrderBuckets + length_bucket(offs[s + 1] - offs[s]);
+                                         unsigned long long tail_start) {
+  return s < tail_start ? 0 : kOrderBuckets + length_bucket(offs[s + 1] - offs[s]);
 }
 
 __global__ void __launch_bounds__(kOrderThreads)
 exsum_segment_hist_kernel(const unsigned long long *__restrict__ offs, unsigned long long nseg,
-                          unsigned long long wsegs, OrderState *st) {
+                          unsigned long long tail_start, OrderState *st) {
   __shared__ unsigned int h[kOrderKeys];
   __shared__ bool last;
   const unsigned t = threadIdx.x;
   for (unsigned k = t; k < kOrderKeys; k += kOrderThreads) h[k] = 0u;
   __syncthreads();
   const unsigned long long s = static_cast<unsigned long long>(blockIdx.x) * kOrderThreads + t;
-  if (s < nseg) atomicAdd(&h[order_key(offs, s, wsegs)], 1u);
+  if (s < nseg) atomicAdd(&h[order_key(offs, s, tail_start)], 1u);
   __syncthreads();
   for (unsigned k = t; k < kOrderKeys; k += kOrderThreads)
     if (h[k]) atomicAdd(&st->hist[k], h[k]);
@@ -1678,7 +1680,7 @@ exsum_segment_hist_kernel(const unsigned long long *__restrict__ offs, unsigned 
 
 __global__ void __launch_bounds__(kOrderThreads)
 exsum_segment_scatter_kernel(const unsigned long long *__restrict__ offs, unsigned long long nseg,
-                             unsigned long long wsegs, OrderState *st,
+                             unsigned long long tail_start, OrderState *st,
                              unsigned int *__restrict__ order) {
   __shared__ unsigned int cnt[kOrderKeys];
   const unsigned t = threadIdx.x;
@@ -1688,7 +1690,7 @@ exsum_segment_scatter_kernel(const unsigned long long *__restrict__ offs, unsign
   int key = 0;
   unsigned r = 0;
   if (s < nseg) {
-    key = order_key(offs, s, wsegs);
+    key = order_key(offs, s, tail_start);
     r = atomicAdd(&cnt[key], 1u);
   }
   __syncthreads();
@@ -2195,11 +2197,12 @@ int exsum_cuda_sum_segmented(const double *d_x, const uint64_t *d_offsets, size_
     auto *st = reinterpret_cast<OrderState *>(base + kOrderStateOffset);
     order = reinterpret_cast<unsigned int *>(base + kOrderOffset);
     const unsigned og = static_cast<unsigned>((nseg + kOrderThreads - 1) / kOrderThreads);
-    const unsigned long long wsegs = (nseg + kSegWindows - 1) / kSegWindows;
+    const unsigned long long tail = static_cast<unsigned long long>(EXSUM_SEG_TAIL) * g * kWarps;
+    const unsigned long long tail_start = nseg > tail ? nseg - tail : 0;
     exsum_segment_hist_kernel<<<og, kOrderThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-        offs, nseg, wsegs, st);
+        offs, nseg, tail_start, st);
     exsum_segment_scatter_kernel<<<og, kOrderThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-        offs, nseg, wsegs, st, order);
+        offs, nseg, tail_start, st, order);
   }
   // Deferred rounding: raw records go to d_partials when the caller wants them,
   // else to the workspace after the claim order (when it has room).
