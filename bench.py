@@ -438,7 +438,8 @@ def run_segmented(args, wl):
     ordered = args.seg_order == "longest"
     ws = ops.Workspace(dev, ops.segmented_workspace_bytes(nseg) if ordered else 0)
     # ordered: exsum_segment_hist_kernel + exsum_segment_scatter_kernel + the segmented kernel
-    launches_per_step = 3 if ordered and ws.nbytes > ops.WORKSPACE_BYTES and nseg > 148 * 8 else 1
+    # + exsum_segment_emit_kernel (deferred rounding; its records live in the ordered workspace)
+    launches_per_step = 4 if ordered and ws.nbytes > ops.WORKSPACE_BYTES and nseg > 148 * 8 else 1
     out = torch.empty(nseg, dtype=torch.float64, device=dev)
     bytes_step = 8 * n_local + 8 * (nseg + 1) + 8 * nseg  # algorithmic: values, offsets, sums
 
