@@ -271,11 +271,19 @@ int default_threads() {
 
 // ------------------------------------------------------------------ Pool
 
+// No exception leaves the pool (it is built behind the C ABI): an allocation or
+// thread-creation failure leaves ok() false; the threads already started are
+// joined by the destructor.
 Pool::Pool(int nthreads) {
   if (nthreads < 1) nthreads = 1;
-  accs_.resize(static_cast<size_t>(nthreads));
-  for (auto &a : accs_) a = new (std::nothrow) Acc;
-  for (int t = 1; t < nthreads; ++t) threads_.emplace_back([this, t] { worker(t); });
+  try {
+    accs_.resize(static_cast<size_t>(nthreads), nullptr);
+    for (auto &a : accs_) a = new (std::nothrow) Acc;
+    parts_.reserve(static_cast<size_t>(nthreads));
+    for (int t = 1; t < nthreads; ++t) threads_.emplace_back([this, t] { worker(t); });
+  } catch (...) {
+    failed_ = true;
+  }
 }
 
 Pool::~Pool() {
@@ -290,6 +298,7 @@ Pool::~Pool() {
 }
 
 bool Pool::ok() const {
+  if (failed_ || accs_.empty()) return false;
   for (auto *a : accs_)
     if (!a) return false;
   return true;

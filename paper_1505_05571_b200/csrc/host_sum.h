@@ -98,6 +98,7 @@ class Pool {
   std::condition_variable cv_, done_cv_;
   uint64_t gen_ = 0;
   bool quit_ = false;
+  bool failed_ = false;
   std::atomic<int> pending_{0};
   Job job_;
 };
