@@ -129,3 +129,21 @@ def test_cpp_caller_host(tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert "host ok" in r.stdout
+
+
+def test_host_array_path_needs_a_device():
+    """The host-array entry points have no CPU-only mode: without a CUDA device
+    the context cannot be created, and the Python API raises instead of summing
+    on the host (the host workers only ever run beside a device)."""
+    import pytest
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    assert not lib.exsum_context_create(0, 1 << 20)
+    from paper_1505_05571_b200 import ops
+    with pytest.raises(_lib.ExsumError):
+        ops.HostContext(0)
+    with pytest.raises(RuntimeError):
+        ops.exact_sum([1.0, 2.0])
+    assert lib.exsum_context_set_host_threads(None, 1) == _lib.EXSUM_EINVAL
+    assert lib.exsum_context_sum_segmented(None, None, None, 0, None, None) == _lib.EXSUM_EINVAL
