@@ -287,21 +287,26 @@ def run_small(args, wl, impl: str):
         r = R.get()
         acc = (C.c_char * 560)()
 
+        rinit, radd, rrnd, xp = r.lib.ref_small_init, r.lib.ref_small_add_array, r.lib.ref_small_round, \
+            x.ctypes.data
+
         def one():
-            r.lib.ref_small_init(acc)
-            r.lib.ref_small_add_array(acc, x.ctypes.data, n)
-            return r.lib.ref_small_round(acc)
+            rinit(acc)
+            radd(acc, xp, n)
+            return rrnd(acc)
     else:
         from paper_1505_05571_b200 import _lib
         from paper_1505_05571_b200._lib import ExsumSmall
         acc = ExsumSmall()
         out = C.c_double()
         lib = _lib.lib
+        accp, outp, xp = C.pointer(acc), C.pointer(out), x.ctypes.data  # built once, like the
+        init, add, rnd = lib.exsum_small_init, lib.exsum_small_add_array, lib.exsum_small_round
 
-        def one():
-            lib.exsum_small_init(C.byref(acc))
-            lib.exsum_small_add_array(C.byref(acc), x.ctypes.data, n)
-            lib.exsum_small_round(C.byref(acc), C.byref(out))
+        def one():  # reference arm's pre-bound arguments: equal ctypes overhead per call
+            init(accp)
+            add(accp, xp, n)
+            rnd(accp, outp)
             return out.value
     for _ in range(max(args.warmup, 3)):
         res = one()
