@@ -270,10 +270,11 @@ def run_reference_arm(args, wl, n_total):
 
 def run_small(args, wl, impl: str):
     """Config 1: the small-superaccumulator case, N = 1e3.  One
-    step = one exact sum: SmallAccumulator() + add(span) + round()
-    (small_accumulator.cpp:174-189, 330-348) through the host C ABI (ours:
-    exsum_small_*; reference arm: the compiled reference, oracle/_ref).  Reported
-    per sum; the device path's latency for the same 1000 terms is listed too."""
+    step = one exact_sum(values, ExactMethod::small) (vector_ops.cpp:121-130:
+    SmallAccumulator() + add(span) + round(), small_accumulator.cpp:174-189,
+    330-348) as one C call (ours: exsum_exact_sum(x, n, 0); reference arm: the
+    compiled reference's exact_sum, oracle/_ref).  Reported per sum; the device
+    path's latency for the same 1000 terms is listed too."""
     import ctypes as C
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -282,31 +283,22 @@ def run_small(args, wl, impl: str):
     n = int(args.n) if args.n else wl["n"]
     x = port.gen(1, args.seed, n)
     steps = args.steps or 100_000
+    # one step = exact_sum(values, ExactMethod::small) (vector_ops.cpp:121-130): one
+    # C call per step in both arms (equal Python overhead)
+    xp = x.ctypes.data
     if impl == "reference":
         from oracle import ref as R
-        r = R.get()
-        acc = (C.c_char * 560)()
-
-        rinit, radd, rrnd, xp = r.lib.ref_small_init, r.lib.ref_small_add_array, r.lib.ref_small_round, \
-            x.ctypes.data
+        rsum = R.get().lib.ref_exact_sum
 
         def one():
-            rinit(acc)
-            radd(acc, xp, n)
-            return rrnd(acc)
+            return rsum(xp, n, 0)
     else:
         from paper_1505_05571_b200 import _lib
-        from paper_1505_05571_b200._lib import ExsumSmall
-        acc = ExsumSmall()
         out = C.c_double()
-        lib = _lib.lib
-        accp, outp, xp = C.pointer(acc), C.pointer(out), x.ctypes.data  # built once, like the
-        init, add, rnd = lib.exsum_small_init, lib.exsum_small_add_array, lib.exsum_small_round
+        outp, osum = C.pointer(out), _lib.lib.exsum_exact_sum
 
-        def one():  # reference arm's pre-bound arguments: equal ctypes overhead per call
-            init(accp)
-            add(accp, xp, n)
-            rnd(accp, outp)
+        def one():
+            osum(xp, n, 0, outp)
             return out.value
     for _ in range(max(args.warmup, 3)):
         res = one()

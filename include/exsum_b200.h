@@ -140,6 +140,12 @@ int exsum_partial_merge(const exsum_partial *parts, size_t k, exsum_partial *out
  * exact_sum(x) (vector_ops.cpp:121-130).  Outputs: result and/or partial. */
 int exsum_host_sum(const double *x, size_t n, uint64_t base_index, int threads, double *result,
                    exsum_partial *partial);
+/* exact_sum(values, method) on the host, one call (vector_ops.cpp:121-130):
+ * method 0 = ExactMethod::small (SmallAccumulator), 1 = ExactMethod::large (the
+ * host kernel of exsum_host_sum on the calling thread; LargeAccumulator bits).
+ * EXSUM_EINVAL for another method (the reference throws std::invalid_argument,
+ * vector_ops.cpp:107). */
+int exsum_exact_sum(const double *x, size_t n, int method, double *out);
 /* Rounded value of a partial record (SmallAccumulator::round on its acc). */
 int exsum_partial_round(const exsum_partial *p, double *out);
 

@@ -430,3 +430,28 @@ extern "C" int exsum_host_sum(const double *x, size_t n, uint64_t base_index, in
   if (result) exsum_partial_round(&rec, result);
   return EXSUM_OK;
 }
+
+// exact_sum(values, ExactMethod) on the host (vector_ops.cpp:121-130), one call:
+// method 0 = small (SmallAccumulator add(span) + round, exsum_small_*),
+// method 1 = large (this file's host kernel on the calling thread; the same bits
+// as LargeAccumulator + round).
+extern "C" int exsum_exact_sum(const double *x, size_t n, int method, double *out) {
+  if (!out || (n && !x) || (method != 0 && method != 1)) return EXSUM_EINVAL;
+  if (method == 0) {
+    exsum_small acc;
+    exsum_small_init(&acc);
+    exsum_small_add_array(&acc, x, n);
+    return exsum_small_round(&acc, out);
+  }
+  try {
+    thread_local exsum_host::Acc *acc = nullptr;  // 32 KB of bins, reused per thread
+    if (!acc && !(acc = new (std::nothrow) exsum_host::Acc)) return EXSUM_ENOMEM;
+    exsum_partial rec;
+    acc->reset();
+    acc->add(x, n, 0);
+    acc->finish(&rec);
+    return exsum_partial_round(&rec, out);
+  } catch (...) {
+    return EXSUM_ENOMEM;
+  }
+}

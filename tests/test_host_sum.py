@@ -94,3 +94,15 @@ def test_empty_and_errors():
     r, p = host_sum(np.zeros(0))
     assert bits_of(r) == 0 and p.first_nan == _lib.NO_INDEX
     assert _lib.lib.exsum_host_sum(None, 5, 0, 1, None, None) == _lib.EXSUM_EINVAL
+
+
+def test_exact_sum_one_call(golden):
+    """exsum_exact_sum (exact_sum(values, method), vector_ops.cpp:121-130)."""
+    out = C.c_double()
+    for c in golden:
+        x = np.ascontiguousarray(c["x"])
+        _lib.call("exsum_exact_sum", x.ctypes.data, x.size, 0, C.byref(out))
+        assert bits_of(out.value) == c["small"], c["tag"]
+        _lib.call("exsum_exact_sum", x.ctypes.data, x.size, 1, C.byref(out))
+        assert bits_of(out.value) == c["large"], c["tag"]
+    assert _lib.lib.exsum_exact_sum(None, 0, 2, C.byref(out)) == _lib.EXSUM_EINVAL
