@@ -176,6 +176,19 @@ int exsum_cuda_sum_ex(const double *d_x, size_t n, uint64_t base_index, double *
                       exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
                       unsigned flags);
 
+/* Launch configuration (a small POD instead of global state).
+ * max_ctas: cap on the persistent grid (0 = one CTA per SM, fewer for short
+ * sums) — leaves SMs to concurrent work; any value gives the same bits.
+ * flags: EXSUM_SUM_OVERLAP or 0. */
+typedef struct exsum_launch_config {
+  uint32_t max_ctas;
+  uint32_t flags;
+  uint32_t reserved_[6]; /* keep 0 */
+} exsum_launch_config;
+int exsum_cuda_sum_cfg(const double *d_x, size_t n, uint64_t base_index, double *d_result,
+                       exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
+                       const exsum_launch_config *cfg);
+
 /* sqnorm / dot on the device (vector_ops.cpp:143-155): the exact sum of the
  * products rounded as the reference's x86 multiply rounds them (IEEE nearest
  * even; a NaN operand propagates quieted, x first; 0 * Inf is the x86 default

@@ -39,6 +39,12 @@ class ExsumPartial(C.Structure):
                 ("nan_payload", C.c_uint64)]
 
 
+class ExsumLaunchConfig(C.Structure):
+    """``exsum_launch_config``: grid cap + launch flags for exsum_cuda_sum_cfg."""
+
+    _fields_ = [("max_ctas", C.c_uint32), ("flags", C.c_uint32), ("reserved_", C.c_uint32 * 6)]
+
+
 assert C.sizeof(ExsumSmall) == 560
 assert C.sizeof(ExsumPartial) == 592
 
@@ -95,6 +101,7 @@ _SIGNATURES = {
     "exsum_host_sum": (_i32, [_vp, _sz, _u64, _i32, _dp, _pp]),
     "exsum_generate": (_i32, [_u64, _u64, _i32, _vp]),
     "exsum_exact_sum": (_i32, [_vp, _sz, _i32, _dp]),
+    "exsum_cuda_sum_cfg": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _sz, _vp, _vp]),
     "exsum_partial_merge": (_i32, [_pp, _sz, _pp, _dp]),
     "exsum_partial_round": (_i32, [_pp, _dp]),
     "exsum_cuda_workspace_bytes": (_sz, []),

@@ -1938,7 +1938,7 @@ int sum_launch(const double *d_x, size_t n, uint64_t base_index, void *d_ws, siz
                void *stream, int finalize, double *d_result, exsum_partial *d_partial,
                unsigned flags = 0, int op = kSum, const double *d_y = nullptr,
                const P2PArgs *p2p = nullptr, const GroupArgs *grp = nullptr,
-               bool cooperative = false) {
+               bool cooperative = false, unsigned max_ctas = 0) {
   if (!d_ws || ws_bytes < sizeof(Workspace) || (n && !d_x) || (op >= kDot && n && !d_y))
     return EXSUM_EINVAL;
   int sms = 0;
@@ -1950,6 +1950,7 @@ int sum_launch(const double *d_x, size_t n, uint64_t base_index, void *d_ws, siz
   const P2PArgs X = p2p ? *p2p : P2PArgs{};
   cudaLaunchConfig_t cfg = {};
   // emulated ranks: the whole SM set split into equal co-resident groups
+  if (max_ctas && static_cast<unsigned>(sms) > max_ctas) sms = static_cast<int>(max_ctas);
   cfg.gridDim = dim3(G.groups > 1 ? (sms / G.groups) * G.groups
                                    : grid_for(n, sms, (flags & EXSUM_SUM_OVERLAP) != 0));
   cfg.blockDim = dim3(kThreads);
@@ -2025,6 +2026,16 @@ int exsum_cuda_sum_ex(const double *d_x, size_t n, uint64_t base_index, double *
                       unsigned flags) {
   EXSUM_NVTX("exsum_cuda_sum");
   return sum_launch(d_x, n, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial, flags);
+}
+
+int exsum_cuda_sum_cfg(const double *d_x, size_t n, uint64_t base_index, double *d_result,
+                       exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
+                       const exsum_launch_config *cfg) {
+  EXSUM_NVTX("exsum_cuda_sum");
+  if (cfg && (cfg->flags & ~EXSUM_SUM_OVERLAP)) return EXSUM_EINVAL;
+  return sum_launch(d_x, n, base_index, d_ws, ws_bytes, stream, 1, d_result, d_partial,
+                    cfg ? cfg->flags : 0u, kSum, nullptr, nullptr, nullptr, false,
+                    cfg ? cfg->max_ctas : 0u);
 }
 
 int exsum_cuda_sqnorm(const double *d_x, size_t n, uint64_t base_index, double *d_result,

@@ -444,3 +444,19 @@ def test_context_sum_at_global_indices(cuda, checker):
     arr = torch.frombuffer(bytearray(b"".join(bytes(r) for r in recs)), dtype=torch.uint8)
     got, _ = merge_records(arr)
     assert bits_of(got) == want == 0x7FF0000000000AAA
+
+
+def test_launch_config_grid_cap(cuda, checker):
+    """exsum_cuda_sum_cfg: any grid cap gives the same bits (SURVEY.md §5 launch POD)."""
+    x = gen(4, 3_000_000, seed=8)
+    want = bits_of(checker.exact_sum(x.cpu().numpy()))
+    ws = ops.Workspace()
+    res = torch.empty(1, dtype=torch.float64, device="cuda")
+    for cap, flags in ((1, 0), (7, 1), (148, 0), (0, 1), (1000, 0)):
+        cfg = _lib.ExsumLaunchConfig(max_ctas=cap, flags=flags)
+        _lib.call("exsum_cuda_sum_cfg", x.data_ptr(), x.numel(), 0, res.data_ptr(), None, ws.ptr,
+                  ops.WORKSPACE_BYTES, stream(), C.byref(cfg))
+        assert bits_of(res.item()) == want, cap
+    bad = _lib.ExsumLaunchConfig(max_ctas=0, flags=8)
+    assert _lib.lib.exsum_cuda_sum_cfg(x.data_ptr(), x.numel(), 0, res.data_ptr(), None, ws.ptr,
+                                       ops.WORKSPACE_BYTES, stream(), C.byref(bad)) == _lib.EXSUM_EINVAL
