@@ -62,6 +62,9 @@ def parse():
     p.add_argument("--seg-order", default="longest", choices=["longest", "index"],
                    help="config 5: claim segments longest first (default) or in index order")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--hold", type=float, default=0.0,
+                   help="seconds of back-to-back steps after the warm-up, before the timed steps: "
+                        "the power-capped steady state instead of a burst (default 0)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--nccl", action="store_true",
                    help="exchange records with exsum_nccl_sum (NCCL all-gather + merge kernel); "
@@ -446,6 +449,7 @@ def run_segmented(args, wl):
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
+    hold(args, step, world, dev)
     t = time.perf_counter()
     step()
     torch.cuda.synchronize()
@@ -570,6 +574,27 @@ def run_segmented(args, wl):
 
 # ---------------------------------------------------------------- GPU arm
 
+def hold(args, step, world: int, dev) -> None:
+    """--hold S: S seconds of back-to-back steps (the same on every rank) before
+    the timed region, so it measures the power-capped steady state."""
+    if args.hold <= 0:
+        return
+    import torch
+    import torch.distributed as dist
+    t0, k = time.perf_counter(), 0
+    while time.perf_counter() - t0 < args.hold:
+        for _ in range(10):
+            step()
+        torch.cuda.synchronize()
+        k += 10
+    if world > 1:
+        t = torch.tensor([k], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        for _ in range(int(t.item()) - k):
+            step()
+        torch.cuda.synchronize()
+
+
 def agreed_steps(steps: int, world: int, dev) -> int:
     """Every rank must time the same number of steps (the P2P exchange pairs
     step e on every rank): the maximum of the ranks' choices."""
@@ -677,6 +702,7 @@ def main():
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
+    hold(args, step, world, dev)
     # steps: default ~0.5 s of timed region (clock sampling needs a few hundred ms)
     t0 = time.perf_counter()
     for _ in range(5):
@@ -826,6 +852,7 @@ def main():
             "clocks": dict(clocks.report(), remeasured=remeasured),
             "result_bits": hex(result_bits),
             "bit_exact_vs_oracle": parity,
+            "hold_s": args.hold,
         }
         print(json.dumps(line), flush=True)
     if comm is not None:
