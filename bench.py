@@ -282,9 +282,14 @@ def run_small(args, wl, impl: str):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle import port
     n = int(args.n) if args.n else wl["n"]
-    x = port.gen(1, args.seed, n)
+    x = np.empty(n, dtype=np.float64)
+    if impl == "reference":  # the reference arm never loads the product library
+        from oracle import port
+        port.gen(1, args.seed, n, out=x)
+    else:  # the product's own generator (bit-identical, tests/test_synth.py)
+        from paper_1505_05571_b200 import _lib as _gen_lib
+        _gen_lib.call("exsum_host_gen", 1, args.seed, n, 0, n, x.ctypes.data)
     steps = args.steps or 100_000
     # one step = exact_sum(values, ExactMethod::small) (vector_ops.cpp:121-130): one
     # C call per step in both arms (equal Python overhead)
