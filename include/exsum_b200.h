@@ -121,6 +121,10 @@ int exsum_sqnorm(const double *x, size_t n, double *out);
  * rounded products a[i]*b[i]; EXSUM_EINVAL on length mismatch (the reference
  * throws std::invalid_argument, :150-152). */
 int exsum_dot(const double *a, size_t na, const double *b, size_t nb, double *out);
+/* The same sum of rounded products a[i] * b[i] (b == a: sqnorm) on `threads`
+ * host threads (<= 0: all; at most one per 2^20 products) with the host kernel
+ * of exsum_host_sum; exsum_sqnorm / exsum_dot call it with threads = 0. */
+int exsum_host_products(const double *a, const double *b, size_t n, int threads, double *out);
 
 /* ---------------------------------------------------- partial records (host) */
 /* Exact sum of x[0..n) into a partial record (host code; the record format the

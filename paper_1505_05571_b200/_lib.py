@@ -101,6 +101,7 @@ _SIGNATURES = {
     "exsum_host_sum": (_i32, [_vp, _sz, _u64, _i32, _dp, _pp]),
     "exsum_generate": (_i32, [_u64, _u64, _i32, _vp]),
     "exsum_exact_sum": (_i32, [_vp, _sz, _i32, _dp]),
+    "exsum_host_products": (_i32, [_vp, _vp, _sz, _i32, _dp]),
     "exsum_cuda_sum_cfg": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _sz, _vp, _vp]),
     "exsum_partial_merge": (_i32, [_pp, _sz, _pp, _dp]),
     "exsum_partial_round": (_i32, [_pp, _dp]),

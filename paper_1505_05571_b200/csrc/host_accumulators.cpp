@@ -414,32 +414,17 @@ int exsum_large_chunks_in_use(const exsum_large *acc) {
 
 // sum_products (vector_ops.cpp:72-97) with SumMethod::large: every product is
 // rounded by the host multiply (the reference's a[i] * b[i], same x86 rules for
-// NaN operands and 0 * Inf), then summed exactly.  Built without FMA
-// contraction (baseline x86-64), like the reference's products.
+// NaN operands and 0 * Inf), then summed exactly — by the host kernel of
+// host_sum.cpp, on every hardware thread for long vectors (exsum_host_products).
+// Built without FMA contraction (baseline x86-64), like the reference's products.
 int exsum_sqnorm(const double *x, size_t n, double *out) {
   if (!out || (n && !x)) return EXSUM_EINVAL;
-  exsum_large *L = exsum_large_new();
-  if (!L) return EXSUM_ENOMEM;
-  for (size_t i = 0; i < n; ++i) {
-    const double p = x[i] * x[i];
-    large_add_bits(L, bits_of(p));
-  }
-  const int st = exsum_large_round(L, out);
-  exsum_large_free(L);
-  return st;
+  return exsum_host_products(x, x, n, 0, out);
 }
 
 int exsum_dot(const double *a, size_t na, const double *b, size_t nb, double *out) {
   if (!out || na != nb || (na && (!a || !b))) return EXSUM_EINVAL;  // vector_ops.cpp:150-152
-  exsum_large *L = exsum_large_new();
-  if (!L) return EXSUM_ENOMEM;
-  for (size_t i = 0; i < na; ++i) {
-    const double p = a[i] * b[i];
-    large_add_bits(L, bits_of(p));
-  }
-  const int st = exsum_large_round(L, out);
-  exsum_large_free(L);
-  return st;
+  return exsum_host_products(a, b, na, 0, out);
 }
 
 // ------------------------------------------------------------ partial records

@@ -229,6 +229,30 @@ void Acc::add(const double *x, size_t n, uint64_t gbase) {
   terms += n;
 }
 
+// Products in blocks of 512 (rounded by the host multiply, baseline x86-64 SSE2,
+// no FMA contraction: the reference's a[i] * b[i] bit for bit, NaN and 0 * Inf
+// rules included), then the blind-add pass over the block.
+// The operand order matters for NaN payloads (x86 returns the FIRST operand's
+// NaN, quieted, when both are NaN), and a compiler may commute a plain a * b:
+// the multiply is pinned as mulsd with a as the destination operand.
+static inline double x86_mul(double a, double b) {
+#if defined(__x86_64__) || defined(__i386__)
+  __asm__("mulsd %1, %0" : "+x"(a) : "x"(b));
+  return a;
+#else
+  return a * b;
+#endif
+}
+
+void Acc::add_products(const double *a, const double *b, size_t n, uint64_t gbase) {
+  double prod[kBlock];
+  for (size_t i = 0; i < n; i += kBlock) {
+    const size_t len = n - i < kBlock ? n - i : kBlock;
+    for (size_t k = 0; k < len; ++k) prod[k] = x86_mul(a[i + k], b[i + k]);
+    add(prod, len, gbase + i);
+  }
+}
+
 void Acc::finish(exsum_partial *out) {
   for (int c = 0; c < kCopies; ++c)
     for (uint32_t g = 0; g < 4096; g += 8) {
@@ -331,7 +355,10 @@ void Pool::run_share(int t) {
     const size_t begin = job_.cursor->fetch_add(job_.grain, std::memory_order_relaxed);
     if (begin >= job_.n) break;
     const size_t len = job_.n - begin < job_.grain ? job_.n - begin : job_.grain;
-    a->add(job_.x + begin, len, job_.base + begin);
+    if (job_.y)
+      a->add_products(job_.x + begin, job_.y + begin, len, job_.base + begin);
+    else
+      a->add(job_.x + begin, len, job_.base + begin);
   }
   a->finish(&parts_[static_cast<size_t>(t)]);
 }
@@ -354,12 +381,19 @@ void Pool::worker(int t) {
 }
 
 void Pool::start(const double *x, size_t n, uint64_t base, std::atomic<size_t> *cursor,
-                 size_t grain) {
+                 size_t grain, const double *y) {
   exsum_partial empty{};
   empty.acc.adds_until_propagate = kCarryTerms;
   empty.first_pos_inf = empty.first_neg_inf = empty.first_nan = kNoIndex;
   parts_.assign(accs_.size(), empty);
-  job_ = Job{x, n, base, cursor, grain ? grain : (size_t{1} << 18)};
+  Job j;
+  j.x = x;
+  j.y = y;
+  j.n = n;
+  j.base = base;
+  j.cursor = cursor;
+  j.grain = grain ? grain : (size_t{1} << 18);
+  job_ = j;
   pending_.store(static_cast<int>(threads_.size()), std::memory_order_relaxed);
   {
     std::lock_guard<std::mutex> lk(m_);
@@ -393,9 +427,9 @@ void Pool::join_helpers() {
   done_cv_.wait(lk, [&] { return pending_.load(std::memory_order_acquire) == 0; });
 }
 
-void Pool::sum(const double *x, size_t n, uint64_t base, exsum_partial *out) {
+void Pool::sum(const double *x, size_t n, uint64_t base, exsum_partial *out, const double *y) {
   std::atomic<size_t> cursor{0};
-  start(x, n, base, &cursor, 0);
+  start(x, n, base, &cursor, 0, y);
   run_share(0);  // the calling thread is worker 0
   join_helpers();
   exsum_partial_merge(parts_.data(), parts_.size(), out, nullptr);
@@ -450,6 +484,34 @@ extern "C" int exsum_exact_sum(const double *x, size_t n, int method, double *ou
     acc->reset();
     acc->add(x, n, 0);
     acc->finish(&rec);
+    return exsum_partial_round(&rec, out);
+  } catch (...) {
+    return EXSUM_ENOMEM;
+  }
+}
+
+// sum_products on the host: sqnorm (b == a) / dot (vector_ops.cpp:72-97,143-155);
+// threads <= 0: every hardware thread, capped at one per 2^20 products.
+extern "C" int exsum_host_products(const double *a, const double *b, size_t n, int threads,
+                                   double *out) {
+  EXSUM_NVTX("exsum_host_products");
+  if (!out || (n && (!a || !b))) return EXSUM_EINVAL;
+  if (threads <= 0) threads = exsum_host::default_threads();
+  const size_t cap = n >> 20;
+  if (static_cast<size_t>(threads) > cap) threads = cap ? static_cast<int>(cap) : 1;
+  try {
+    exsum_partial rec;
+    if (threads == 1) {
+      thread_local exsum_host::Acc *acc = nullptr;
+      if (!acc && !(acc = new (std::nothrow) exsum_host::Acc)) return EXSUM_ENOMEM;
+      acc->reset();
+      acc->add_products(a, b, n, 0);
+      acc->finish(&rec);
+    } else {
+      exsum_host::Pool pool(threads);
+      if (!pool.ok()) return EXSUM_ENOMEM;
+      pool.sum(a, n, 0, &rec, b);
+    }
     return exsum_partial_round(&rec, out);
   } catch (...) {
     return EXSUM_ENOMEM;

@@ -32,6 +32,9 @@ struct alignas(64) Acc {
   void reset();
   // x[0..n) with global indices gbase .. gbase + n - 1
   void add(const double *x, size_t n, uint64_t gbase);
+  // the rounded products a[i] * b[i] (b == a: squares), as sum_products
+  // (vector_ops.cpp:72-97) forms them, added like add()
+  void add_products(const double *a, const double *b, size_t n, uint64_t gbase);
   // drain the bins; the canonical record with index-resolved Inf/NaN (leaves
   // every bin zero again)
   void finish(exsum_partial *out);
@@ -61,12 +64,14 @@ class Pool {
 
   bool ok() const;
   int size() const { return static_cast<int>(accs_.size()); }
-  // Whole array on the pool, caller included; merged record in *out.
-  void sum(const double *x, size_t n, uint64_t base, exsum_partial *out);
+  // Whole array on the pool, caller included; merged record in *out.  With y:
+  // the sum of the rounded products x[i] * y[i] instead.
+  void sum(const double *x, size_t n, uint64_t base, exsum_partial *out,
+           const double *y = nullptr);
   // Hybrid: helpers start on the shared cursor; the caller does other work,
   // may call run_share(0) itself, then join_helpers().
   void start(const double *x, size_t n, uint64_t base, std::atomic<size_t> *cursor,
-             size_t grain);
+             size_t grain, const double *y = nullptr);
   // Hybrid segmented sum: helpers claim `grain` segments at a time from the
   // shared segment cursor and write out[s] (and partials[s]) themselves.
   void start_segments(const double *x, const uint64_t *offs, size_t nseg,
@@ -80,6 +85,7 @@ class Pool {
  private:
   struct Job {
     const double *x = nullptr;
+    const double *y = nullptr;  // products job: x[i] * y[i]
     size_t n = 0;  // terms, or segments for a segmented job
     uint64_t base = 0;
     std::atomic<size_t> *cursor = nullptr;

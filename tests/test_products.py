@@ -127,3 +127,25 @@ def test_device_products_large(checker, cuda):
         torch.cuda.empty_cache()
     with pytest.raises(_lib.ExsumError):
         ops.exact_dot_tensor(_dev(np.zeros(3)), _dev(np.zeros(4)))
+
+
+def test_host_products_threads_vs_reference(checker):
+    """exsum_sqnorm / exsum_dot on long vectors (multithreaded host kernel) and
+    exsum_host_products at several thread counts, against the reference."""
+    rng = np.random.default_rng(11)
+    n = 3_000_017
+    a = rng.normal(size=n) * 10.0 ** rng.integers(-160, 160, n)
+    b = rng.normal(size=n) * 10.0 ** rng.integers(-160, 160, n)
+    for arr in (a, b):
+        m = rng.random(n) < 1e-6
+        arr[m] = rng.choice([np.inf, -np.inf, np.nan, 0.0], size=int(m.sum()))
+    want_sq = bits_of(checker.sqnorm(a))
+    want_dot = bits_of(checker.dot(a, b))
+    out = C.c_double()
+    _lib.call("exsum_sqnorm", a.ctypes.data, n, C.byref(out))
+    assert bits_of(out.value) == want_sq
+    _lib.call("exsum_dot", a.ctypes.data, n, b.ctypes.data, n, C.byref(out))
+    assert bits_of(out.value) == want_dot
+    for t in (1, 2, 3):
+        _lib.call("exsum_host_products", a.ctypes.data, b.ctypes.data, n, t, C.byref(out))
+        assert bits_of(out.value) == want_dot, t
