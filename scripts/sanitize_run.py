@@ -62,9 +62,32 @@ for bo in (0, 1):
     fails += bits(r.item()) != bits(chk.dot(a[:50_001].cpu().numpy(), b[bo:bo + 50_001].cpu().numpy()))
 r, _ = ops.exact_sqnorm_tensor(a)
 fails += bits(r.item()) != bits(chk.sqnorm(a.cpu().numpy()))
-# host-buffer context (staging ring + accumulate + finalize)
+# host-buffer context (staging ring + accumulate + finalize), device only and hybrid
 h = gen(4, 400_000).cpu().numpy()
 fails += bits(ops.exact_sum(h)) != bits(chk.exact_sum(h))
+ctx = ops.HostContext(0, staging_bytes=3 << 20, host_threads=0)
+fails += bits(ctx.sum(h)) != bits(chk.exact_sum(h))
+ctx.set_host_threads(3)
+fails += bits(ctx.sum(h)) != bits(chk.exact_sum(h))
+# segmented host arrays through the context (device groups + deferred rounding)
+hs = xs.cpu().numpy()
+ctx.set_host_threads(0)
+fails += int(not np.array_equal(ctx.sum_segmented(hs, offs.astype(np.uint64)).view(np.uint64), want))
+# incremental accumulate (carried workspace) + finalize
+ws = ops.Workspace(dev)
+xd = gen(3, 300_000)
+for lo in range(0, 300_000, 70_000):
+    hi = min(lo + 70_000, 300_000)
+    _lib.call("exsum_cuda_accumulate", xd[lo:].data_ptr(), hi - lo, lo, ws.ptr, ops.WORKSPACE_BYTES, stream)
+res = torch.empty(1, dtype=torch.float64, device=dev)
+_lib.call("exsum_cuda_finalize", res.data_ptr(), None, ws.ptr, ops.WORKSPACE_BYTES, stream)
+fails += bits(res.item()) != bits(chk.exact_sum(xd.cpu().numpy()))
+# fused exchange, one rank: publish only, then the collect launch
+from paper_1505_05571_b200.distributed import P2PGroup, p2p_collect, p2p_exact_sum  # noqa: E402
+grp = P2PGroup(dev)
+p2p_exact_sum(xd, grp, base_index=0, publish_only=True)
+fails += bits(p2p_collect(grp).item()) != bits(chk.exact_sum(xd.cpu().numpy()))
+grp.close()
 torch.cuda.synchronize()
 print("sanitize_run: mismatches", fails)
 sys.exit(1 if fails else 0)
