@@ -386,6 +386,17 @@ def test_cpp_caller_device(cuda, tmp_path):
     assert "device ok" in r.stdout
 
 
+def test_cpp_dropin_header_device(cuda, tmp_path):
+    """include/exsum_b200.hpp DeviceContext from C++: host arrays through the
+    device (and the host workers), equal to the host exact_sum."""
+    import subprocess
+    from test_capi import _build_dropin
+    exe = _build_dropin(tmp_path)
+    r = subprocess.run([str(exe), "--device"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    assert "dropin device ok" in r.stdout
+
+
 def test_cuda_graph_capture(cuda):
     """The device entry points inside a captured CUDA graph (replayed several
     times, workspace reused): exact sum with and without programmatic dependent
