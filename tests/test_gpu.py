@@ -208,6 +208,9 @@ def test_configs_full_size(config, n, cuda, checker):
     assert dev_sum(torch.flip(x, (0,)))[0] == got
     neg = dev_sum(-x)[0]
     assert neg == (got ^ (1 << 63) if got & ~(1 << 63) else 0)
+    if config != 3:  # power-of-two scaling is exact term by term and for the rounded sum
+        r = np.array([got], dtype=np.uint64).view(np.float64)[0]
+        assert dev_sum(x * 0.25)[0] == bits_of(r * 0.25)
     del x, h
 
 
