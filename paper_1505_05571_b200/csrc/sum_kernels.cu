@@ -79,6 +79,10 @@
 #ifndef EXSUM_UNIFORM_FAST
 #define EXSUM_UNIFORM_FAST 1  // single-sum kernel: register fast path for one-slot batches
 #endif
+#ifndef EXSUM_INTERLEAVE
+#define EXSUM_INTERLEAVE 1  // single sums: batches round-robin over warps (1) instead of
+                           // contiguous per-warp ranges (0): all warps sweep one window
+#endif
 #ifndef EXSUM_SEG_SPLIT
 #define EXSUM_SEG_SPLIT 0  // segmented kernel: unguarded full batches + a one-vector tail loop
 #endif
@@ -909,7 +913,12 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
                                                 const double *__restrict__ y,
                                                 unsigned long long begin, unsigned long long end,
                                                 unsigned long long index_base, const Lane &a,
-                                                Specials &sp, int &norm_count, int lane) {
+                                                Specials &sp, int &norm_count, int lane,
+                                                long long vfirst = 0, long long vstride = 0,
+                                                bool scalar_terms = true) {
+  // vfirst / vstride (in 32-byte vectors): the warp's batches start at vfirst and
+  // follow every vstride vectors (0: V * 32, one contiguous range); scalar_terms:
+  // this warp adds the range's unaligned head and tail terms.
   constexpr int kNormEvery = 2016 / (4 * V);  // batches between renormalisations
   static_assert(kNormEvery >= 1, "batch too large for the carry budget");
   if (begin >= end) return;
@@ -925,6 +934,7 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
   const double *Y4 = kOp >= kDot ? y + vbeg_t : X4;
   const unsigned long long tail_t = vbeg_t + 4ull * static_cast<unsigned long long>(nvec);
   auto scalars = [&]() {
+    if (!scalar_terms) return;
     if (lane < static_cast<int>(head))
       add_elem_checked<kOp>(a, sp, x, y, begin + lane, index_base + begin + lane);
     if (lane < static_cast<int>(end - tail_t))
@@ -935,20 +945,22 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
     return;
   }
   constexpr long long kStep = V * 32;
+  const long long vs = vstride ? vstride : kStep;  // vectors between this warp's batches
   const unsigned long long ib = index_base + vbeg_t;
   if (lane == 0) {
-    for (int d = 0; d <= kPrefetchBatches; ++d) prefetch_batch<V, kOp>(X4, Y4, d * kStep, nvec);
+    for (int d = 0; d <= kPrefetchBatches; ++d)
+      prefetch_batch<V, kOp>(X4, Y4, vfirst + d * vs, nvec);
   }
   Batch<V, kOp> b;
-  load_batch<V, kOp>(b, X4, Y4, 0, nvec, lane);
+  load_batch<V, kOp>(b, X4, Y4, vfirst, nvec, lane);
   scalars();
   int backoff = 0;
-  for (long long v = 0; v < nvec; v += kStep) {
-    const long long nv = v + kStep;
+  for (long long v = vfirst; v < nvec; v += vs) {
+    const long long nv = v + vs;
     if constexpr (EXSUM_PF_PRED && kOp == kSum) {
-      prefetch_l2_lane0<V>(X4, v + (kPrefetchBatches + 1) * kStep, nvec, lane);
+      prefetch_l2_lane0<V>(X4, v + (kPrefetchBatches + 1) * vs, nvec, lane);
     } else {
-      if (lane == 0) prefetch_batch<V, kOp>(X4, Y4, v + (kPrefetchBatches + 1) * kStep, nvec);
+      if (lane == 0) prefetch_batch<V, kOp>(X4, Y4, v + (kPrefetchBatches + 1) * vs, nvec);
     }
     products_in_place<V, kOp>(b);
     uint32_t emax = 0;
@@ -1454,8 +1466,17 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
   const Lane a = lane_view(wsm, lane);
   Specials sp{~0ull, ~0ull, ~0ull};
   int norm_count = 0;
+#if EXSUM_INTERLEAVE
+  // batches dealt round-robin over the grid's warps: all warps sweep one window
+  (void)tb;
+  (void)te;
+  warp_accumulate<V, EXSUM_UNIFORM_FAST != 0, true, EXSUM_SUM_SCAN != 0 && kOp == kSum, kOp>(
+      x, y, 0, n, base_index, a, sp, norm_count, lane,
+      static_cast<long long>(gw) * V * 32, static_cast<long long>(nw) * V * 32, gw == 0);
+#else
   warp_accumulate<V, EXSUM_UNIFORM_FAST != 0, true, EXSUM_SUM_SCAN != 0 && kOp == kSum, kOp>(
       x, y, tb, te, base_index, a, sp, norm_count, lane);
+#endif
 
   // K2: the warp's 67 chunk sums.
   EXSUM_STAMP(1);
