@@ -79,3 +79,27 @@ def test_device_arm_line(config):
     if config in (2, 4):  # the CPU leg also checks the device result against the reference
         assert line["bit_exact_vs_oracle"] is True
         assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] > 0
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    """The driver launches both arms with torchrun for N > 1: in the reference
+    arm rank 0 alone runs the CPU reference and prints one line; rank 1 exits 0."""
+    from oracle import ref as R
+    if not R.available():
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1",
+                          "--master-port", str(port), str(ROOT / "bench.py"), "--impl",
+                          "reference", "--gpus", "2", "--steps", "2", "--warmup", "3",
+                          "--terms", "1e5"],
+                         capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["config"]["n_gpus"] == 2 and line["config"]["n_total"] == 100_000
