@@ -83,6 +83,10 @@
 #define EXSUM_INTERLEAVE 1  // single sums: batches round-robin over warps (1) instead of
                            // contiguous per-warp ranges (0): all warps sweep one window
 #endif
+#ifndef EXSUM_SEG_AHEAD
+#define EXSUM_SEG_AHEAD 0  // segmented: claim the next segment at the start of the current one and
+                           // prefetch its head into L2 before the current epilogue
+#endif
 #ifndef EXSUM_SEG_SPLIT
 #define EXSUM_SEG_SPLIT 0  // segmented kernel: unguarded full batches + a one-vector tail loop
 #endif
@@ -1769,6 +1773,12 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
     if (s >= nseg) break;
     const unsigned long long b = __shfl_sync(0xffffffffu, ca.b, 0),
                              e = __shfl_sync(0xffffffffu, ca.e, 0);
+#if EXSUM_SEG_AHEAD
+    // claim the next segment now: its result is ready when this one ends, so
+    // its head can be pulled into L2 while this segment's epilogue runs
+    SegmentClaim cn{0u, 0ull, 0ull};
+    if (lane == 0) cn.claim(&ws->seg_next, order, offs, nseg);
+#endif
     zero_warp(wsm, lane);
     __syncwarp();
     int norm_count = 0;
@@ -1786,8 +1796,26 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
                                                                       sp, norm_count, lane);
 #endif
     EXSUM_SEG_PHASE(2);
+#if EXSUM_SEG_AHEAD
+    if (lane == 0) {
+      ca = cn;
+      if (ca.s < nseg && ca.e > ca.b) {  // the next head (<= 2 batches) into L2
+        const unsigned long long hb = ca.b;
+        const unsigned long long he = ca.e - hb > 2ull * 4 * 32 * EXSUM_SEG_VEC
+                                          ? hb + 2ull * 4 * 32 * EXSUM_SEG_VEC
+                                          : ca.e;
+        const uintptr_t p0 = reinterpret_cast<uintptr_t>(x + hb) & ~uintptr_t{15};
+        const uintptr_t p1 = reinterpret_cast<uintptr_t>(x + he);
+        const uint32_t bytes = static_cast<uint32_t>((p1 - p0) & ~uintptr_t{15});
+        if (bytes)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"(bytes)
+                       : "memory");
+      }
+    }
+#else
     if (lane == 0)
       ca.claim(&ws->seg_next, order, offs, nseg);
+#endif
     EXSUM_SEG_PHASE(0);
     warp_chunks(wsm, lane, row);
     const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
