@@ -51,7 +51,7 @@ constexpr size_t kHostOnlyTerms = size_t{1} << 17;
 
 struct exsum_context {
   int device = 0;
-  std::mutex busy;  // one sum at a time per context (staging, workspace, pool)
+  mutable std::mutex busy;  // one sum at a time per context (staging, workspace, pool)
   void *ws = nullptr;
   size_t ws_bytes = 0;
   double *stage[kSlots] = {};
@@ -264,6 +264,7 @@ int exsum_context_set_host_threads(exsum_context *c, int threads) {
 int exsum_context_last_split(const exsum_context *c, uint64_t *device_terms,
                              uint64_t *host_terms) {
   if (!c) return EXSUM_EINVAL;
+  std::lock_guard<std::mutex> lk(c->busy);
   if (device_terms) *device_terms = c->last_device_terms;
   if (host_terms) *host_terms = c->last_host_terms;
   return EXSUM_OK;
