@@ -22,6 +22,10 @@
 
 using namespace exsum_b200;
 
+#ifndef EXSUM_SMALL_COPIES
+#define EXSUM_SMALL_COPIES 2  // local chunk arrays taken in turn by add(span) (store-forwarding chains)
+#endif
+
 namespace {
 
 inline uint64_t bits_of(double v) {
@@ -245,9 +249,9 @@ int exsum_small_add(exsum_small *acc, double v) {
 
 // add(span) (small_accumulator.cpp:174-189): the same runs between
 // propagations, but each run is summed branch-free (sign applied as
-// (v ^ s) - s, no mispredicted sign branch on mixed-sign data) into two local
-// chunk arrays taken alternately (no store-to-load chain through the same
-// chunk on consecutive terms), then added to the accumulator.  Integer adds
+// (v ^ s) - s, no mispredicted sign branch on mixed-sign data) into
+// EXSUM_SMALL_COPIES local chunk arrays taken in turn (no store-to-load chain
+// through the same chunk on consecutive terms), then added to the accumulator.  Integer adds
 // are associative and a run stays within the 2047-add budget, so the chunk
 // values after every call equal the reference's sequential adds exactly.
 int exsum_small_add_array(exsum_small *acc, const double *x, size_t n) {
@@ -257,7 +261,7 @@ int exsum_small_add_array(exsum_small *acc, const double *x, size_t n) {
     if (acc->adds_until_propagate <= 0) small_propagate(acc);
     size_t run = static_cast<size_t>(acc->adds_until_propagate);
     if (run > n - i) run = n - i;
-    int64_t c[2][kChunks + 1] = {};
+    int64_t c[EXSUM_SMALL_COPIES][kChunks + 1] = {};
     for (size_t j = 0; j < run; ++j) {
       const uint64_t bits = bits_of(x[i + j]);
       const uint32_t e = static_cast<uint32_t>(bits >> kMantBits) & 0x7FFu;
@@ -277,11 +281,15 @@ int exsum_small_add_array(exsum_small *acc, const double *x, size_t n) {
       const int64_t s = static_cast<int64_t>(bits) >> 63;  // 0 or -1
       const int64_t low = static_cast<int64_t>((m << sh) & 0xFFFFFFFFull);
       const int64_t high = static_cast<int64_t>(m >> (32u - sh));
-      int64_t *cj = c[j & 1];
+      int64_t *cj = c[j % EXSUM_SMALL_COPIES];
       cj[ix] += (low ^ s) - s;
       cj[ix + 1] += (high ^ s) - s;
     }
-    for (int k = 0; k < kChunks; ++k) acc->chunk[k] += c[0][k] + c[1][k];
+    for (int k = 0; k < kChunks; ++k) {
+      int64_t t = 0;
+      for (int r = 0; r < EXSUM_SMALL_COPIES; ++r) t += c[r][k];
+      acc->chunk[k] += t;
+    }
     acc->adds_until_propagate -= static_cast<int32_t>(run);  // budget per element
     i += run;
   }
