@@ -55,9 +55,10 @@ def draw(rng, n):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=240)
+    ap.add_argument("--seed", type=int, default=2026)
     a = ap.parse_args()
     chk = make_checker()
-    rng = np.random.default_rng(2026)
+    rng = np.random.default_rng(a.seed)
     ctx = ops.HostContext(0, staging_bytes=12 << 20)
     stats = dict(cases=0, terms=0, mismatches=0)
     t0 = time.time()
