@@ -125,6 +125,11 @@
 #define EXSUM_SEG_DEFER 1  // segmented sums: round every segment in a second launch
                            // (exsum_segment_emit_kernel) instead of on the streaming warp
 #endif
+#ifndef EXSUM_SEG_FIX_GROUP
+#define EXSUM_SEG_FIX_GROUP 1  // segmented sums: pipelined Inf/NaN fix-up, flags per group of this
+                               // many vectors (0: the synchronous scanning fix-up); config 5:
+                               // 2.087 / 2.095 / 2.108 ms for 1 / 2 / 0 (r02_segfix.log)
+#endif
 #ifndef EXSUM_DEBUG_CHECKS
 #define EXSUM_DEBUG_CHECKS 0  // debug build: every streaming load checks its vector index against
                               // the range end (printf + trap on a violation)
@@ -792,14 +797,19 @@ __device__ __forceinline__ void products_in_place(Batch<V, kOp> &b) {
 // Add one batch (registers b) with rolling refill from vector nv onward.  kGuard:
 // bounds-checked refills (only the last batches need it).  Returns the batch's
 // maximum exponent field (2047 iff it contained an Inf/NaN term).
-template <int V, bool kGuard, int kOp>
+// kGroup > 0 (pipelined fix-up): returns instead a bitmask of the batch's groups
+// of kGroup vectors that hold an Inf/NaN term (bit g: vectors g kGroup ..).
+template <int V, bool kGuard, int kOp, int kGroup = 0>
 __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &b,
                                                   const double *X4, const double *Y4,
                                                   long long nv, long long nvec, int lane) {
-  uint32_t emax = 0;
+  static_assert(kGroup == 0 || V % kGroup == 0, "groups tile the batch");
+  constexpr int G = kGroup ? kGroup : 1;
+  uint32_t emax = 0, flags = 0;
 #pragma unroll
   for (int u = 0; u < V; ++u) {
     uint32_t lo[4], hi[4], e[4];
+    if (kGroup && u % G == 0) emax = 0;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // terms: products already in place (products_in_place)
       lo[q] = b.w[u][2 * q];
@@ -807,6 +817,7 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
       e[q] = exponent_field(hi[q]);
       emax = max(emax, e[q]);
     }
+    if (kGroup && u % G == G - 1) flags |= static_cast<uint32_t>(emax == 0x7FFu) << (u / G);
 #pragma unroll
     for (int q = 0; q < 4; ++q) add_term(a, lo[q], hi[q], e[q]);
     const long long vec = nv + u * 32 + lane;
@@ -817,7 +828,56 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
       zero_vec<V, kOp>(b, u);
     }
   }
-  return emax;
+  return kGroup ? flags : emax;
+}
+
+// Pipelined Inf/NaN fix-up (plain sums): a batch whose lane saw an Inf/NaN in
+// exactly one group of kGroup vectors does not stall on a re-read.  The group's
+// vectors are re-loaded into registers at the batch's end and consumed one batch
+// later — record by index, cancel the blind add (modular slot arithmetic, so
+// the cancel may trail a renormalisation; it counts against the carry budget
+// like any add: <= 4 kGroup extra adds per window).  Two or more flagged groups
+// (rare) take the synchronous scanning fix-up.
+template <int kGroup>
+struct PendingFix {
+  uint32_t w[kGroup][8];
+  long long vec;  // first vector of the group (the lane's), < 0: none
+};
+
+template <int kGroup>
+__device__ __forceinline__ void pending_issue(PendingFix<kGroup> &p, const double *X4,
+                                              long long vec, long long nvec) {
+  p.vec = vec;
+#pragma unroll
+  for (int j = 0; j < kGroup; ++j) {
+    const long long t = vec + 32 * j;
+    if (t < nvec) {
+      asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(p.w[j][0]), "=r"(p.w[j][1]), "=r"(p.w[j][2]), "=r"(p.w[j][3]),
+                     "=r"(p.w[j][4]), "=r"(p.w[j][5]), "=r"(p.w[j][6]), "=r"(p.w[j][7])
+                   : "l"(X4 + 4 * t));
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) p.w[j][q] = 0u;
+    }
+  }
+}
+
+template <int kGroup>
+__device__ __forceinline__ void pending_apply(PendingFix<kGroup> &p, const Lane &a, Specials &sp,
+                                              unsigned long long ib) {
+#pragma unroll
+  for (int j = 0; j < kGroup; ++j)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t lo = p.w[j][2 * q], hi = p.w[j][2 * q + 1];
+      if (exponent_field(hi) == 0x7FFu) {
+        record_special(sp, lo, hi,
+                       ib + 4ull * static_cast<unsigned long long>(p.vec + 32 * j) + q);
+        cancel_term(a, lo, hi, 0x7FFu);
+      }
+    }
+  p.vec = -1;
 }
 
 // Register fast path: every lane's batch lies in slot k (|sum| < 2^89 per lane):
@@ -912,7 +972,8 @@ __device__ __forceinline__ uint32_t uniform_slot(const Batch<V, kOp> &b, uint32_
 //   kSplit:   separate unguarded steady-state body (larger code, fewer instrs)
 //   kScan:    scanning Inf/NaN fix-up (for data with frequent specials)
 //   kOp:      term source (kSum, kSqnorm, kDot, kDotScalarB); y used by dots
-template <int V, bool kUniform, bool kSplit, bool kScan, int kOp = kSum>
+//   kGroup:   > 0: pipelined Inf/NaN fix-up at this group size (PendingFix)
+template <int V, bool kUniform, bool kSplit, bool kScan, int kOp = kSum, int kGroup = 0>
 __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
                                                 const double *__restrict__ y,
                                                 unsigned long long begin, unsigned long long end,
@@ -959,6 +1020,10 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
   load_batch<V, kOp>(b, X4, Y4, vfirst, nvec, lane);
   scalars();
   int backoff = 0;
+  static_assert(kGroup == 0 || kOp == kSum, "pipelined fix-up: plain sums only");
+  constexpr int kG1 = kGroup ? kGroup : 1;
+  PendingFix<kG1> pf;
+  pf.vec = -1;
   for (long long v = vfirst; v < nvec; v += vs) {
     const long long nv = v + vs;
     if constexpr (EXSUM_PF_PRED && kOp == kSum) {
@@ -992,17 +1057,32 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
     }
     if (k == ~0u) {
       if (kSplit && steady) {
-        emax = batch_rolling<V, false, kOp>(a, b, X4, Y4, nv, nvec, lane);
+        emax = batch_rolling<V, false, kOp, kGroup>(a, b, X4, Y4, nv, nvec, lane);
       } else {
-        emax = batch_rolling<V, true, kOp>(a, b, X4, Y4, nv, nvec, lane);
+        emax = batch_rolling<V, true, kOp, kGroup>(a, b, X4, Y4, nv, nvec, lane);
       }
     }
-    if (__builtin_expect(emax == 0x7FFu, 0))
-      fixup_specials<V, kScan, kOp>(a, sp, X4, Y4, v, nvec, lane, ib);
+    if constexpr (kGroup > 0) {
+      // emax holds the flagged groups
+      if (__builtin_expect(pf.vec >= 0, 0)) pending_apply<kG1>(pf, a, sp, ib);
+      if (__builtin_expect(emax != 0u, 0)) {
+        if ((emax & (emax - 1u)) || nv >= nvec) {
+          fixup_specials<V, kScan, kOp>(a, sp, X4, Y4, v, nvec, lane, ib);
+        } else {
+          pending_issue<kG1>(pf, X4, v + (__ffs(emax) - 1) * kGroup * 32 + lane, nvec);
+        }
+      }
+    } else {
+      if (__builtin_expect(emax == 0x7FFu, 0))
+        fixup_specials<V, kScan, kOp>(a, sp, X4, Y4, v, nvec, lane, ib);
+    }
     if (++norm_count >= kNormEvery) {
       normalize(a);
       norm_count = 0;
     }
+  }
+  if constexpr (kGroup > 0) {
+    if (pf.vec >= 0) pending_apply<kG1>(pf, a, sp, ib);
   }
 }
 
@@ -1792,8 +1872,8 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
 #if EXSUM_SEG_SPLIT
     warp_accumulate_seg<EXSUM_SEG_VEC>(x, b, e, 0ull - b, a, sp, norm_count, lane);
 #else
-    warp_accumulate<EXSUM_SEG_VEC, false, false, true>(x, x, b, e, 0ull - b, a,
-                                                                      sp, norm_count, lane);
+    warp_accumulate<EXSUM_SEG_VEC, false, false, true, kSum, EXSUM_SEG_FIX_GROUP>(
+        x, x, b, e, 0ull - b, a, sp, norm_count, lane);
 #endif
     EXSUM_SEG_PHASE(2);
 #if EXSUM_SEG_AHEAD

@@ -39,6 +39,8 @@ VARIANTS = {
     "nomag": ("EXSUM_UNIFORM_SIGNED=0",),
     "debug": ("EXSUM_DEBUG_CHECKS=1",),
     "pfbranch": ("EXSUM_PF_PRED=0",),
+    "segfix0": ("EXSUM_SEG_FIX_GROUP=0",),
+    "segfix2": ("EXSUM_SEG_FIX_GROUP=2",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 verbose = "-v" in names

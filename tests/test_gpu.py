@@ -474,3 +474,60 @@ def test_launch_config_grid_cap(cuda, checker):
     bad = _lib.ExsumLaunchConfig(max_ctas=0, flags=8)
     assert _lib.lib.exsum_cuda_sum_cfg(x.data_ptr(), x.numel(), 0, res.data_ptr(), None, ws.ptr,
                                        ops.WORKSPACE_BYTES, stream(), C.byref(bad)) == _lib.EXSUM_EINVAL
+
+
+def _seg_check(checker, x: torch.Tensor, offs: np.ndarray, tag):
+    """Ordered claims + deferred rounding (full workspace) vs index-order claims
+    with inline rounding (small workspace) vs the checker: rounded bits and the
+    partial records (chunks, local Inf/NaN indices)."""
+    od = torch.from_numpy(offs.astype(np.int64)).cuda()
+    a, pa = ops.exact_sum_segmented(x, od, partials=True)
+    a2 = ops.exact_sum_segmented(x, od)  # no partials: records in the workspace
+    b, pb = ops.exact_sum_segmented(x, od, partials=True, longest_first=False)
+    h = x.cpu().numpy()
+    want = checker.segmented_sum(h, offs.astype(np.uint64)).view(np.uint64)
+    for got in (a, a2, b):
+        g = got.cpu().numpy().view(np.uint64)
+        assert np.array_equal(g, want), (tag, int((g != want).sum()))
+    assert torch.equal(pa, pb), tag
+
+
+def test_segmented_edges(cuda, checker):
+    """Segmented sums at batch edges: segment lengths at, just below and just
+    above multiples of the 1024-term warp batch; Inf/NaN at segment starts and
+    ends and NaN payloads (the pipelined fix-up, EXSUM_SEG_FIX_GROUP); offsets
+    not starting at 0 over a misaligned array; one 30 M-term segment among
+    tiny ones; empty segments at both ends and in between; fewer terms than
+    warps; decreasing offsets at full size."""
+    rng = np.random.default_rng(2024)
+    cases = []
+    lens = np.array([1024, 1023, 1025, 2048, 1, 0, 3, 4095, 4097, 1000, 0, 0, 5000, 1024 * 7 + 5])
+    cases.append(("batch-edges", np.tile(lens, 300), 0, 0))
+    cases.append(("tiny", rng.integers(0, 9, 40_000), 0, 0))
+    cases.append(("config5-like", np.exp(rng.uniform(np.log(1e3), np.log(1e5), 3000)).astype(np.int64), 3, 1))
+    cases.append(("one-huge", np.array([0, 2, 30_000_000, 1, 0]), 5, 3))
+    cases.append(("few-terms", np.array([0, 1, 2, 0, 3]), 1, 1))
+    cases.append(("halves", np.array([5_000_000, 5_000_001]), 2, 2))
+    for tag, ln, lead, misalign in cases:
+        offs = np.concatenate([[0], np.cumsum(ln)]).astype(np.int64) + lead
+        total = int(offs[-1]) + 7
+        h = np.empty(total, dtype=np.float64)
+        h[:] = rng.standard_normal(total) * np.exp2(rng.integers(-900, 900, total).astype(np.float64))
+        # specials just before/after segment starts and at random places
+        starts = offs[(offs > 0) & (offs < total - 1)]
+        pick = rng.choice(starts, size=min(200, starts.size), replace=False) if starts.size else starts
+        for k, p in enumerate(pick):
+            h[p - 1 + (k % 3)] = (np.inf, -np.inf, np.nan)[k % 3]
+        h[rng.integers(0, total, 50)] = np.nan
+        nanp = np.array([0x7FF0000000000001 + k for k in range(10)], dtype=np.uint64).view(np.float64)
+        h[rng.integers(0, total, 10)] = nanp  # NaN payloads: the first one must win
+        _seg_check(checker, to_dev(h, misalign), offs, tag)
+    # decreasing offsets at full size: empty segments, no wrapped lengths
+    h = rng.standard_normal(3_000_000)
+    offs = np.array([0, 1_000_000, 500_000, 3_000_000, 2_999_999, 3_000_000], dtype=np.int64)
+    od = torch.from_numpy(offs).cuda()
+    got = ops.exact_sum_segmented(to_dev(h), od).cpu().numpy().view(np.uint64)
+    for i in range(offs.size - 1):
+        b, e = int(offs[i]), int(offs[i + 1])
+        want = bits_of(checker.exact_sum(h[b:e])) if e > b else 0
+        assert int(got[i]) == want, i
