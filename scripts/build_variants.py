@@ -41,6 +41,7 @@ VARIANTS = {
     "pfbranch": ("EXSUM_PF_PRED=0",),
     "segfix0": ("EXSUM_SEG_FIX_GROUP=0",),
     "segfix2": ("EXSUM_SEG_FIX_GROUP=2",),
+    "segahead1": ("EXSUM_SEG_AHEAD=1",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 verbose = "-v" in names
