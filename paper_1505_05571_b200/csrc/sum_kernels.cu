@@ -1745,8 +1745,11 @@ exsum_segment_hist_kernel(const unsigned long long *__restrict__ offs, unsigned 
   const unsigned t = threadIdx.x;
   for (unsigned k = t; k < kOrderKeys; k += kOrderThreads) h[k] = 0u;
   __syncthreads();
-  const unsigned long long s = static_cast<unsigned long long>(blockIdx.x) * kOrderThreads + t;
+  // the grid covers the tail only; the head (key 0, index order) is one count
+  const unsigned long long s =
+      tail_start + static_cast<unsigned long long>(blockIdx.x) * kOrderThreads + t;
   if (s < nseg) atomicAdd(&h[order_key(offs, s, tail_start)], 1u);
+  if (blockIdx.x == 0 && t == 0) h[0] += static_cast<unsigned int>(tail_start);
   __syncthreads();
   for (unsigned k = t; k < kOrderKeys; k += kOrderThreads)
     if (h[k]) atomicAdd(&st->hist[k], h[k]);
@@ -1756,6 +1759,14 @@ exsum_segment_hist_kernel(const unsigned long long *__restrict__ offs, unsigned 
   __syncthreads();
   if (!last) return;
   __threadfence();
+  // The totals into shared memory with one load per thread (a serial loop of
+  // L2 round trips here cost ~10 us), cleared for the next call.
+  static_assert(kOrderKeys <= kOrderThreads, "one key per thread");
+  if (t < kOrderKeys) {
+    h[t] = __ldcg(&st->hist[t]);
+    st->hist[t] = 0u;
+  }
+  __syncthreads();
   // Claim position o runs over windows ascending and, within a window, buckets
   // descending: key(o) = (o / 512) * 512 + 511 - o % 512.  base[key(o)] = the
   // number of segments at positions before o.  One warp: lane t owns positions
@@ -1764,7 +1775,7 @@ exsum_segment_hist_kernel(const unsigned long long *__restrict__ offs, unsigned 
     constexpr int P = kOrderKeys / 32;
     auto key_of = [](int o) { return (o / kOrderBuckets) * kOrderBuckets + kOrderBuckets - 1 - o % kOrderBuckets; };
     unsigned sum = 0;
-    for (int i = 0; i < P; ++i) sum += __ldcg(&st->hist[key_of(P * t + i)]);
+    for (int i = 0; i < P; ++i) sum += h[key_of(P * t + i)];
     unsigned before = sum;  // inclusive prefix over lanes <= t
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -1774,10 +1785,8 @@ exsum_segment_hist_kernel(const unsigned long long *__restrict__ offs, unsigned 
     before -= sum;
     for (int i = 0; i < P; ++i) {
       const int k = key_of(P * t + i);
-      const unsigned v = __ldcg(&st->hist[k]);
-      st->hist[k] = 0u;
       st->base[k] = before;
-      before += v;
+      before += h[k];
     }
     if (t == 0) st->done = 0u;
   }
@@ -1792,9 +1801,11 @@ exsum_segment_scatter_kernel(const unsigned long long *__restrict__ offs, unsign
   for (unsigned k = t; k < kOrderKeys; k += kOrderThreads) cnt[k] = 0u;
   __syncthreads();
   const unsigned long long s = static_cast<unsigned long long>(blockIdx.x) * kOrderThreads + t;
+  const bool head = s < tail_start;  // the head keeps index order: claim position s
+  if (head) order[s] = static_cast<unsigned>(s);
   int key = 0;
   unsigned r = 0;
-  if (s < nseg) {
+  if (!head && s < nseg) {
     key = order_key(offs, s, tail_start);
     r = atomicAdd(&cnt[key], 1u);
   }
@@ -1802,7 +1813,7 @@ exsum_segment_scatter_kernel(const unsigned long long *__restrict__ offs, unsign
   for (unsigned k = t; k < kOrderKeys; k += kOrderThreads)
     if (cnt[k]) cnt[k] = atomicAdd(&st->base[k], cnt[k]);  // this CTA's range in bucket k
   __syncthreads();
-  if (s < nseg) order[cnt[key] + r] = static_cast<unsigned>(s);
+  if (!head && s < nseg) order[cnt[key] + r] = static_cast<unsigned>(s);
 }
 
 // Lane 0's claim of the next segment: the claim atomic, the segment's entry in
@@ -2339,7 +2350,9 @@ int exsum_cuda_sum_segmented(const double *d_x, const uint64_t *d_offsets, size_
     const unsigned og = static_cast<unsigned>((nseg + kOrderThreads - 1) / kOrderThreads);
     const unsigned long long tail = static_cast<unsigned long long>(EXSUM_SEG_TAIL) * g * kWarps;
     const unsigned long long tail_start = nseg > tail ? nseg - tail : 0;
-    exsum_segment_hist_kernel<<<og, kOrderThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+    const unsigned hg =
+        static_cast<unsigned>((nseg - tail_start + kOrderThreads - 1) / kOrderThreads);
+    exsum_segment_hist_kernel<<<hg, kOrderThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         offs, nseg, tail_start, st);
     exsum_segment_scatter_kernel<<<og, kOrderThreads, 0, static_cast<cudaStream_t>(stream)>>>(
         offs, nseg, tail_start, st, order);
