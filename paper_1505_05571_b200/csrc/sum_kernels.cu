@@ -71,7 +71,8 @@
 #define EXSUM_DOT_VEC 4  // dot kernel: vectors per lane per batch (x and y each)
 #endif
 #ifndef EXSUM_SEG_VEC
-#define EXSUM_SEG_VEC 8  // segmented kernel: vectors per lane per batch
+#define EXSUM_SEG_VEC 7  // segmented kernel: vectors per lane per batch (7: config 5 2.083 -> 2.068 ms
+                         // vs 8, a smaller loop body; 6: 2.105; r02_knob_resweep_seg.log)
 #endif
 #ifndef EXSUM_PREFETCH_BATCHES
 #define EXSUM_PREFETCH_BATCHES 1  // L2 bulk-prefetch distance, in batches

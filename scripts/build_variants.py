@@ -42,6 +42,11 @@ VARIANTS = {
     "segfix0": ("EXSUM_SEG_FIX_GROUP=0",),
     "segfix2": ("EXSUM_SEG_FIX_GROUP=2",),
     "segahead1": ("EXSUM_SEG_AHEAD=1",),
+    "il0": ("EXSUM_INTERLEAVE=0",),
+    "v7": ("EXSUM_VEC_PER_LANE=7",),
+    "seg8": ("EXSUM_SEG_VEC=8",),
+    "segtail2": ("EXSUM_SEG_TAIL=2",),
+    "segtail8": ("EXSUM_SEG_TAIL=8",),
 }
 names = sys.argv[1:] or list(VARIANTS)
 verbose = "-v" in names
