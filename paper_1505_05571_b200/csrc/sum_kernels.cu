@@ -59,6 +59,7 @@
 
 #include <atomic>
 #include <mutex>
+#include <type_traits>
 
 #include "exsum_b200.h"
 #include "exsum_core.h"
@@ -156,6 +157,11 @@
 #ifndef EXSUM_SUM_SCAN
 #define EXSUM_SUM_SCAN 1  // single-sum kernel: scanning Inf/NaN fix-up (0: per-term loop; 1.43x
                           // faster on 1e-4 Inf/NaN data, neutral otherwise: r01_variants_sumscan.log)
+#endif
+#ifndef EXSUM_UNIFORM_DISPATCH
+#define EXSUM_UNIFORM_DISPATCH 1  // one-slot fast path: a warp whose first batch is not one-slot runs a
+                                  // loop without the fast path's code (kept only for warps that start
+                                  // one-slot; it still backs off per batch there)
 #endif
 #ifndef EXSUM_UNIFORM_BACKOFF
 #define EXSUM_UNIFORM_BACKOFF 7  // batches to skip the one-slot test after a miss
@@ -1025,62 +1031,77 @@ __device__ __forceinline__ void warp_accumulate(const double *__restrict__ x,
   constexpr int kG1 = kGroup ? kGroup : 1;
   PendingFix<kG1> pf;
   pf.vec = -1;
-  for (long long v = vfirst; v < nvec; v += vs) {
-    const long long nv = v + vs;
-    if constexpr (EXSUM_PF_PRED && kOp == kSum) {
-      prefetch_l2_lane0<V>(X4, v + (kPrefetchBatches + 1) * vs, nvec, lane);
-    } else {
-      if (lane == 0) prefetch_batch<V, kOp>(X4, Y4, v + (kPrefetchBatches + 1) * vs, nvec);
-    }
-    products_in_place<V, kOp>(b);
-    uint32_t emax = 0;
-    const bool steady = nv + kStep <= nvec;  // next batch complete: unguarded refills
-    uint32_t k = ~0u, sgn = 1u;
-    if constexpr (kUniform) {
-      if (steady) {
-        if (backoff > 0) {
-          --backoff;
-        } else {
-          k = uniform_slot<V, kOp>(b, &sgn);
-          if (!__all_sync(0xffffffffu, k != ~0u)) {
-            k = ~0u;
-            backoff = kUniformBackoff;  // wide data rarely turns uniform
+  auto run = [&](auto uniform_tag) {
+    constexpr bool U = decltype(uniform_tag)::value;
+    for (long long v = vfirst; v < nvec; v += vs) {
+      const long long nv = v + vs;
+      if constexpr (EXSUM_PF_PRED && kOp == kSum) {
+        prefetch_l2_lane0<V>(X4, v + (kPrefetchBatches + 1) * vs, nvec, lane);
+      } else {
+        if (lane == 0) prefetch_batch<V, kOp>(X4, Y4, v + (kPrefetchBatches + 1) * vs, nvec);
+      }
+      products_in_place<V, kOp>(b);
+      uint32_t emax = 0;
+      const bool steady = nv + kStep <= nvec;  // next batch complete: unguarded refills
+      uint32_t k = ~0u, sgn = 1u;
+      if constexpr (U) {
+        if (steady) {
+          if (backoff > 0) {
+            --backoff;
+          } else {
+            k = uniform_slot<V, kOp>(b, &sgn);
+            if (!__all_sync(0xffffffffu, k != ~0u)) {
+              k = ~0u;
+              backoff = kUniformBackoff;  // wide data rarely turns uniform
+            }
+          }
+        }
+        if (k != ~0u) {
+          if (EXSUM_UNIFORM_SIGNED && __all_sync(0xffffffffu, sgn != 1u && k >= 1u)) {
+            batch_uniform_mag<V, kOp>(a, b, X4, Y4, nv, lane, k, sgn, nvec);
+          } else {
+            batch_uniform<V, kOp>(a, b, X4, Y4, nv, lane, k, nvec);
           }
         }
       }
-      if (k != ~0u) {
-        if (EXSUM_UNIFORM_SIGNED && __all_sync(0xffffffffu, sgn != 1u && k >= 1u)) {
-          batch_uniform_mag<V, kOp>(a, b, X4, Y4, nv, lane, k, sgn, nvec);
+      if (k == ~0u) {
+        if (kSplit && steady) {
+          emax = batch_rolling<V, false, kOp, kGroup>(a, b, X4, Y4, nv, nvec, lane);
         } else {
-          batch_uniform<V, kOp>(a, b, X4, Y4, nv, lane, k, nvec);
+          emax = batch_rolling<V, true, kOp, kGroup>(a, b, X4, Y4, nv, nvec, lane);
         }
       }
-    }
-    if (k == ~0u) {
-      if (kSplit && steady) {
-        emax = batch_rolling<V, false, kOp, kGroup>(a, b, X4, Y4, nv, nvec, lane);
+      if constexpr (kGroup > 0) {
+        // emax holds the flagged groups
+        if (__builtin_expect(pf.vec >= 0, 0)) pending_apply<kG1>(pf, a, sp, ib);
+        if (__builtin_expect(emax != 0u, 0)) {
+          if ((emax & (emax - 1u)) || nv >= nvec) {
+            fixup_specials<V, kScan, kOp>(a, sp, X4, Y4, v, nvec, lane, ib);
+          } else {
+            pending_issue<kG1>(pf, X4, v + (__ffs(emax) - 1) * kGroup * 32 + lane, nvec);
+          }
+        }
       } else {
-        emax = batch_rolling<V, true, kOp, kGroup>(a, b, X4, Y4, nv, nvec, lane);
-      }
-    }
-    if constexpr (kGroup > 0) {
-      // emax holds the flagged groups
-      if (__builtin_expect(pf.vec >= 0, 0)) pending_apply<kG1>(pf, a, sp, ib);
-      if (__builtin_expect(emax != 0u, 0)) {
-        if ((emax & (emax - 1u)) || nv >= nvec) {
+        if (__builtin_expect(emax == 0x7FFu, 0))
           fixup_specials<V, kScan, kOp>(a, sp, X4, Y4, v, nvec, lane, ib);
-        } else {
-          pending_issue<kG1>(pf, X4, v + (__ffs(emax) - 1) * kGroup * 32 + lane, nvec);
-        }
       }
+      if (++norm_count >= kNormEvery) {
+        normalize(a);
+        norm_count = 0;
+      }
+    }
+  };
+  if constexpr (kUniform && EXSUM_UNIFORM_DISPATCH) {
+    // the first batch decides which loop this warp runs
+    uint32_t sg0;
+    const uint32_t k0 = uniform_slot<V, kOp>(b, &sg0);
+    if (__all_sync(0xffffffffu, k0 != ~0u)) {
+      run(std::true_type{});
     } else {
-      if (__builtin_expect(emax == 0x7FFu, 0))
-        fixup_specials<V, kScan, kOp>(a, sp, X4, Y4, v, nvec, lane, ib);
+      run(std::false_type{});
     }
-    if (++norm_count >= kNormEvery) {
-      normalize(a);
-      norm_count = 0;
-    }
+  } else {
+    run(std::integral_constant<bool, kUniform>{});
   }
   if constexpr (kGroup > 0) {
     if (pf.vec >= 0) pending_apply<kG1>(pf, a, sp, ib);

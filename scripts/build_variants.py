@@ -43,6 +43,7 @@ VARIANTS = {
     "segfix2": ("EXSUM_SEG_FIX_GROUP=2",),
     "segahead1": ("EXSUM_SEG_AHEAD=1",),
     "il0": ("EXSUM_INTERLEAVE=0",),
+    "nodisp": ("EXSUM_UNIFORM_DISPATCH=0",),
     "v7": ("EXSUM_VEC_PER_LANE=7",),
     "seg8": ("EXSUM_SEG_VEC=8",),
     "segtail2": ("EXSUM_SEG_TAIL=2",),
