@@ -217,10 +217,13 @@ int exsum_cuda_finalize(double *d_result, exsum_partial *d_partial, void *d_ws,
  * empty segment, sum +0.0, never as a wrapped length).  No reference batch API exists;
  * semantics = exact_sum(segment_i) for every i.
  * d_partials may be NULL; otherwise nseg records, indices local to the segment.
- * With ws_bytes >= exsum_cuda_segmented_workspace_bytes(nseg) the segments are
- * scheduled longest first (a second, one-CTA launch orders them; the order
- * cannot change any result), otherwise in index order.  exsum_cuda_workspace_init
- * with the full ws_bytes prepares both (it zeroes the order state as well). */
+ * With ws_bytes >= exsum_cuda_segmented_workspace_bytes(nseg) (and more segments
+ * than warps) two small launches build the claim order (index order, the last
+ * 4 x warps segments longest first) and a last launch rounds every segment from
+ * its raw record; otherwise segments are claimed in index order and rounded in
+ * the streaming launch.  The order cannot change any result.
+ * exsum_cuda_workspace_init with the full ws_bytes prepares both (it zeroes the
+ * order state as well). */
 int exsum_cuda_sum_segmented(const double *d_x, const uint64_t *d_offsets, size_t nseg,
                              double *d_out, exsum_partial *d_partials, void *d_ws,
                              size_t ws_bytes, void *stream);

@@ -28,7 +28,10 @@
 // exponent ranges) the batch is summed in registers and the slot gets one
 // read-modify-write; when each lane's batch also has one sign (U[0,1)), the
 // magnitudes are summed without the sign complement (8.5 instructions/term).
-// Inf/NaN are added blindly and cancelled by a per-batch fix-up.  Sustained
+// A warp whose first batch is not one-slot runs a loop compiled without that
+// fast path (EXSUM_UNIFORM_DISPATCH).  Inf/NaN are added blindly and cancelled
+// by a per-batch fix-up (pipelined one batch behind in the segmented kernel,
+// EXSUM_SEG_FIX_GROUP).  Sustained
 // rates sit at the 1 kW power cap, so energy per term (not DRAM) bounds the
 // general path.
 //
