@@ -531,3 +531,22 @@ def test_segmented_edges(cuda, checker):
         b, e = int(offs[i]), int(offs[i + 1])
         want = bits_of(checker.exact_sum(h[b:e])) if e > b else 0
         assert int(got[i]) == want, i
+
+
+def test_uniform_dispatch_mixed_halves(cuda, checker):
+    """Each warp picks its loop from its first batch (EXSUM_UNIFORM_DISPATCH):
+    arrays whose character changes part-way (one-slot U[0,1) data then every
+    exponent, and the reverse; one-slot runs of one sign then mixed signs) go
+    through both loops and the general path inside the fast-path loop; bits
+    and chunks equal the reference either way."""
+    rng = np.random.default_rng(5)
+    n = 6_000_000
+    uni = rng.random(n)                                     # one slot, one sign
+    wide = gen(3, n, seed=8).cpu().numpy()                  # every exponent + denormals
+    pm = np.where(rng.random(n) < 0.5, -1.0, 1.0) * (1.0 + rng.random(n))  # one slot, mixed signs
+    for parts in ((uni, wide), (wide, uni), (uni, pm, wide), (pm, uni)):
+        h = np.concatenate(parts)
+        for off in (0, 1):
+            got, part = dev_sum(to_dev(h, off))
+            assert got == bits_of(checker.exact_sum(h)), (len(parts), off)
+            assert list(part.acc.chunk) == [int(c) for c in checker.canonical(h)[0]]
