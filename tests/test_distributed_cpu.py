@@ -1,4 +1,4 @@
-"""Host-side logic of the multi-GPU path on CPU: world_size 2 over gloo.
+"""Host-side logic of the multi-GPU path on CPU: world_size 2 and 4 over gloo.
 
 Each rank builds its shard's 592-byte partial record with the host API
 (exsum_partial_from_array, global indices), the records are all-gathered, and
@@ -58,7 +58,9 @@ def test_shard_bounds_matches_reference_split():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
 
 
-def test_gloo_world2_exchange_and_merge(golden):
+@pytest.mark.parametrize("world", [2, 4])
+def test_gloo_world2_exchange_and_merge(golden, world):
+    """world 2 and 4 (4: short arrays leave some ranks empty)."""
     cases = [c for c in golden if c["group"] in ("spec", "random")]
     xs = [c["x"] for c in cases]
     nan123 = np.array([0x7FF0000000000123], dtype=np.uint64).view(np.float64)[0]
@@ -71,7 +73,7 @@ def test_gloo_world2_exchange_and_merge(golden):
     ]
     want = [c["large"] for c in cases] + [0x7FF8000000000000, 0x7FF0000000000123,
                                           0x7FF0000000000000]
-    world, port = 2, _free_port()
+    port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker, args=(r, world, port, xs + extra, q)) for r in range(world)]
