@@ -17,6 +17,13 @@
 #include <cstring>
 #include <new>
 
+#if defined(__x86_64__) && !defined(EXSUM_NO_AVX512)
+#include <immintrin.h>
+#define EXSUM_HAVE_AVX512 1
+#else
+#define EXSUM_HAVE_AVX512 0
+#endif
+
 #include "exsum_b200.h"
 #include "exsum_core.h"
 
@@ -254,6 +261,89 @@ int exsum_small_add(exsum_small *acc, double v) {
 // through the same chunk on consecutive terms), then added to the accumulator.  Integer adds
 // are associative and a run stays within the 2047-add budget, so the chunk
 // values after every call equal the reference's sequential adds exactly.
+// One term of a run (small_add_term's arithmetic) into the local chunk array cj:
+// branch-free sign ((v ^ s) - s); zeros skipped, denormals at exponent 1, Inf/NaN
+// to the accumulator's special state.
+static inline void small_term_local(exsum_small *acc, int64_t *cj, uint64_t bits) {
+  const uint32_t e = static_cast<uint32_t>(bits >> kMantBits) & 0x7FFu;
+  uint64_t m = bits & kMantMask;
+  uint32_t ee = e;
+  if (__builtin_expect(e - 1u >= 0x7FEu, 0)) {  // e == 0 or e == 0x7FF
+    if (e == 0x7FFu) {
+      small_special(acc, bits);
+      return;
+    }
+    if (m == 0) return;
+    ee = 1;
+  } else {
+    m |= uint64_t{1} << kMantBits;
+  }
+  const uint32_t sh = ee & 31u, ix = ee >> 5;
+  const int64_t s = static_cast<int64_t>(bits) >> 63;  // 0 or -1
+  const int64_t low = static_cast<int64_t>((m << sh) & 0xFFFFFFFFull);
+  const int64_t high = static_cast<int64_t>(m >> (32u - sh));
+  cj[ix] += (low ^ s) - s;
+  cj[ix + 1] += (high ^ s) - s;
+}
+
+// AVX-512 form of a run's adds for the common case: 8 terms at a time whose
+// exponent fields are all in [1, 2046] (no zero, denormal, Inf or NaN) and
+// share one chunk index e >> 5 (every U[-1,1) term but those below 2^-31, for
+// example).  Such groups are split exactly as small_add_term does and summed in
+// two vector accumulators (chunk ix and ix + 1; per-lane sums stay below 2^43
+// and 2^63 within a run); a group that does not qualify returns to the scalar
+// loop at its first term.  Returns how many terms of [0, run) it consumed.
+#if EXSUM_HAVE_AVX512
+__attribute__((target("avx512f"))) static size_t small_run_avx512(const uint64_t *b, size_t run,
+                                                           int64_t *c) {
+  const __m512i kMask11 = _mm512_set1_epi64(0x7FF), kMant = _mm512_set1_epi64(kMantMask),
+                kOne = _mm512_set1_epi64(int64_t{1} << kMantBits),
+                kLow = _mm512_set1_epi64(0xFFFFFFFFll), k32 = _mm512_set1_epi64(32),
+                k31 = _mm512_set1_epi64(31), k1 = _mm512_set1_epi64(1),
+                kSpan = _mm512_set1_epi64(0x7FE);
+  __m512i accl = _mm512_setzero_si512(), acch = _mm512_setzero_si512();
+  int64_t hot = -1;
+  size_t j = 0;
+  for (; j + 8 <= run; j += 8) {
+    const __m512i v = _mm512_loadu_si512(b + j);
+    const __m512i e = _mm512_and_si512(_mm512_srli_epi64(v, kMantBits), kMask11);
+    const __m512i ix = _mm512_srli_epi64(e, 5);
+    const __m512i ix0 = _mm512_permutexvar_epi64(_mm512_setzero_si512(), ix);
+    // all normal (e - 1 < 2046 unsigned) and one chunk index
+    const __mmask8 ok = _mm512_cmplt_epu64_mask(_mm512_sub_epi64(e, k1), kSpan) &
+                        _mm512_cmpeq_epi64_mask(ix, ix0);
+    if (ok != 0xFF) break;
+    const int64_t gix = _mm512_cvtsi512_si32(ix0);
+    if (gix != hot) {
+      if (hot >= 0) {
+        c[hot] += _mm512_reduce_add_epi64(accl);
+        c[hot + 1] += _mm512_reduce_add_epi64(acch);
+        accl = _mm512_setzero_si512();
+        acch = _mm512_setzero_si512();
+      }
+      hot = gix;
+    }
+    const __m512i m = _mm512_or_si512(_mm512_and_si512(v, kMant), kOne);
+    const __m512i sh = _mm512_and_si512(e, k31);
+    const __m512i low = _mm512_and_si512(_mm512_sllv_epi64(m, sh), kLow);
+    const __m512i high = _mm512_srlv_epi64(m, _mm512_sub_epi64(k32, sh));
+    const __m512i sg = _mm512_srai_epi64(v, 63);  // 0 or -1
+    accl = _mm512_add_epi64(accl, _mm512_sub_epi64(_mm512_xor_si512(low, sg), sg));
+    acch = _mm512_add_epi64(acch, _mm512_sub_epi64(_mm512_xor_si512(high, sg), sg));
+  }
+  if (hot >= 0) {
+    c[hot] += _mm512_reduce_add_epi64(accl);
+    c[hot + 1] += _mm512_reduce_add_epi64(acch);
+  }
+  return j;
+}
+
+static bool have_avx512() {
+  static const bool yes = __builtin_cpu_supports("avx512f");
+  return yes;
+}
+#endif
+
 int exsum_small_add_array(exsum_small *acc, const double *x, size_t n) {
   if (!acc || (n && !x)) return EXSUM_EINVAL;
   size_t i = 0;
@@ -262,29 +352,18 @@ int exsum_small_add_array(exsum_small *acc, const double *x, size_t n) {
     size_t run = static_cast<size_t>(acc->adds_until_propagate);
     if (run > n - i) run = n - i;
     int64_t c[EXSUM_SMALL_COPIES][kChunks + 1] = {};
-    for (size_t j = 0; j < run; ++j) {
-      const uint64_t bits = bits_of(x[i + j]);
-      const uint32_t e = static_cast<uint32_t>(bits >> kMantBits) & 0x7FFu;
-      uint64_t m = bits & kMantMask;
-      uint32_t ee = e;
-      if (__builtin_expect(e - 1u >= 0x7FEu, 0)) {  // e == 0 or e == 0x7FF
-        if (e == 0x7FFu) {
-          small_special(acc, bits);
-          continue;
-        }
-        if (m == 0) continue;
-        ee = 1;
-      } else {
-        m |= uint64_t{1} << kMantBits;
-      }
-      const uint32_t sh = ee & 31u, ix = ee >> 5;
-      const int64_t s = static_cast<int64_t>(bits) >> 63;  // 0 or -1
-      const int64_t low = static_cast<int64_t>((m << sh) & 0xFFFFFFFFull);
-      const int64_t high = static_cast<int64_t>(m >> (32u - sh));
-      int64_t *cj = c[j % EXSUM_SMALL_COPIES];
-      cj[ix] += (low ^ s) - s;
-      cj[ix + 1] += (high ^ s) - s;
+    size_t j = 0;
+#if EXSUM_HAVE_AVX512
+    // vector groups first, then the scalar loop from the first group that did
+    // not qualify; the vector path re-enters after every scalar stretch of 8
+    while (j < run && have_avx512()) {
+      j += small_run_avx512(reinterpret_cast<const uint64_t *>(x + i) + j, run - j, c[0]);
+      if (j + 8 > run) break;
+      const size_t stop = j + 8;  // one group's worth through the scalar loop
+      for (; j < stop; ++j) small_term_local(acc, c[j % EXSUM_SMALL_COPIES], bits_of(x[i + j]));
     }
+#endif
+    for (; j < run; ++j) small_term_local(acc, c[j % EXSUM_SMALL_COPIES], bits_of(x[i + j]));
     for (int k = 0; k < kChunks; ++k) {
       int64_t t = 0;
       for (int r = 0; r < EXSUM_SMALL_COPIES; ++r) t += c[r][k];

@@ -121,3 +121,42 @@ def test_device_matches_reference(ref, cuda, x, off, off2):
     assert bits_of(r.item()) == bits_of(ref.dot(x, y))
     r, _ = ops.exact_sqnorm_tensor(dev(x, off))
     assert bits_of(r.item()) == bits_of(ref.sqnorm(x))
+
+
+def test_small_add_array_vector_groups(ref):
+    """exsum_small_add_array takes groups of 8 one-chunk normal terms through its
+    AVX-512 path and everything else through the scalar loop; the raw 560-byte
+    state after add(span) must equal the reference's sequential adds whatever
+    the mix: long U[-1,1) runs (one chunk), runs that switch chunk, zeros,
+    denormals, Inf/NaN and wide values dropped in at every offset mod 8, and
+    lengths across the 2047-add propagation budget."""
+    rng = np.random.default_rng(11)
+    odd = np.array([0.0, -0.0, 5e-324, -2.2e-308, np.inf, -np.inf, np.nan, 1e300, -3e-200,
+                    np.array([0x7FF0000000000123], dtype=np.uint64).view(np.float64)[0]])
+    for n in (0, 7, 8, 9, 64, 1000, 2047, 2048, 2049, 4096 + 5, 10_000):
+        for variant in range(6):
+            if variant == 0:
+                x = rng.uniform(-1, 1, n)
+            elif variant == 1:  # chunk switches every few groups (binades 2^-40 .. 2^40)
+                x = rng.uniform(1, 2, n) * np.exp2(np.repeat(rng.integers(-40, 40, n // 24 + 1), 24)[:n])
+                x *= np.where(rng.random(n) < 0.5, -1.0, 1.0)
+            else:  # disruptive terms at random positions
+                x = rng.uniform(-1, 1, n)
+                if n:
+                    k = max(1, n // (50 * variant))
+                    x[rng.integers(0, n, k)] = odd[rng.integers(0, odd.size, k)]
+            x = np.ascontiguousarray(x)
+            acc = _small_of(x)
+            rbuf = ref.small_new()
+            ref.lib.ref_small_add_array(rbuf, x.ctypes.data, x.size)
+            assert bytes(acc) == bytes(rbuf), (n, variant)
+            # the same array in two calls split at an offset that is not a multiple of 8
+            if n > 11:
+                acc2 = ExsumSmall()
+                _lib.call("exsum_small_init", C.byref(acc2))
+                _lib.call("exsum_small_add_array", C.byref(acc2), x.ctypes.data, 11)
+                _lib.call("exsum_small_add_array", C.byref(acc2), x[11:].ctypes.data, n - 11)
+                rb2 = ref.small_new()
+                ref.lib.ref_small_add_array(rb2, x.ctypes.data, 11)
+                ref.lib.ref_small_add_array(rb2, x[11:].ctypes.data, n - 11)
+                assert bytes(acc2) == bytes(rb2), (n, variant, "split")
