@@ -652,6 +652,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
     begin, end = shard_bounds(n_total, world, rank)
     n_local = end - begin
+    two_phase_min = int(_lib.lib.exsum_cuda_two_phase_min())
     x = torch.empty(n_local, dtype=torch.float64, device=dev)
     _lib.call("exsum_cuda_gen", args.config, args.seed, n_total, begin, n_local, x.data_ptr(),
               stream.cuda_stream)
@@ -845,14 +846,19 @@ def main():
             "terms_per_s": round(value * 1e9 / 8, 1),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                         "kernel": "exsum_sum_kernel", "kernel_ms": round(k_ms, 4),
+                         "kernel": "exsum_wsum_kernel + exsum_sum_kernel (two-phase)"
+                         if p2p is None and 0 < two_phase_min <= n_local else "exsum_sum_kernel",
+                         "kernel_ms": round(k_ms, 4),
                          "timing": "CUDA events over back-to-back launches (PDL overlap), per-launch average",
                          "frac_of": peak_of,
                          "frac_of_spec_8000": round(achieved / 8000.0, 4),  # north_star's ~8 TB/s
                          "peak_source": peak_src},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": steps * (2 if comm is not None else 1),  # p2p: 1 per step
+            # p2p: 1 per step; NCCL: + the merge kernel; a two-phase sum (>= 2^28 terms per
+            # GPU, not fused with the exchange): the windowed pass + the full kernel
+            "gpu_launches": steps * ((2 if comm is not None else 1) + (
+                1 if p2p is None and 0 < two_phase_min <= n_local else 0)),
             "exchange": exchange_note,
             "clocks": dict(clocks.report(), remeasured=remeasured),
             "result_bits": hex(result_bits),

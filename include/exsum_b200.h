@@ -193,6 +193,12 @@ int exsum_cuda_sum_cfg(const double *d_x, size_t n, uint64_t base_index, double 
                        exsum_partial *d_partial, void *d_ws, size_t ws_bytes, void *stream,
                        const exsum_launch_config *cfg);
 
+/* Two-phase plain sums: exsum_cuda_sum(_ex) of at least this many terms, with a
+ * workspace of exsum_cuda_workspace_bytes(), runs a windowed pass (16 warps per
+ * SM, narrow exponent ranges) and then the full kernel over what it left — two
+ * launches instead of one; the bits do not depend on it.  0: disabled. */
+uint64_t exsum_cuda_two_phase_min(void);
+
 /* sqnorm / dot on the device (vector_ops.cpp:143-155): the exact sum of the
  * products rounded as the reference's x86 multiply rounds them (IEEE nearest
  * even; a NaN operand propagates quieted, x first; 0 * Inf is the x86 default

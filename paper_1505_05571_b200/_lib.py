@@ -106,6 +106,7 @@ _SIGNATURES = {
     "exsum_partial_merge": (_i32, [_pp, _sz, _pp, _dp]),
     "exsum_partial_round": (_i32, [_pp, _dp]),
     "exsum_cuda_workspace_bytes": (_sz, []),
+    "exsum_cuda_two_phase_min": (_u64, []),
     "exsum_cuda_workspace_init": (_i32, [_vp, _sz, _vp]),
     "exsum_cuda_sum": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _sz, _vp]),
     "exsum_cuda_sum_ex": (_i32, [_vp, _sz, _u64, _vp, _vp, _vp, _sz, _vp, C.c_uint]),

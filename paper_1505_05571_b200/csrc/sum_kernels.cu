@@ -50,6 +50,10 @@
 //                           other ranks over peer memory and merges
 //                           (exsum_p2p_sum); with a group split, one cooperative
 //                           launch emulates several ranks (tests).
+//   exsum_wsum_kernel       K1w: the windowed first phase of plain sums of
+//                           >= 2^28 terms (16 warps per SM, a 16-slot window per
+//                           warp); exsum_sum_kernel then sums what it left
+//                           ("jobs") or returns at once if it left nothing.
 //   exsum_segmented_kernel  K4: one warp per segment (dynamic claim), compact
 //                           loop body (instruction-cache bound otherwise).
 //   exsum_merge_kernel      K5: merge of k gathered partial records + round.
@@ -185,7 +189,7 @@ struct Workspace {
   unsigned int done;      // CTAs finished in the current launch
   unsigned int seg_next;  // segmented: next segment to claim
   unsigned int seg_done;  // segmented: warps finished
-  unsigned int pad_;
+  unsigned int wdone;     // two-phase: windowed CTAs finished (zero between calls)
 };
 
 struct Specials {                // first occurrences seen by one lane
@@ -1520,12 +1524,340 @@ __device__ bool p2p_collect(const P2PArgs &p2p, int me, long long *row, unsigned
   return true;
 }
 
+// --------------------------------------------------------- K1w (round 2, late)
+//
+// Two-phase plain sum for large arrays (EXSUM_TWO_PHASE): a windowed pass, then
+// the full kernel over what it left.  Lane-private slots cost 25 KB of shared
+// memory per warp, so the full kernel runs 8 warps per SM; an array whose
+// terms sit in a narrow exponent range (config 4: slots 29-35) needs only a
+// window of 16 slots — 6.5 KB per warp, 16 warps per SM, twice the latency
+// hiding (profiles/r02_window_occupancy.log).  The windowed kernel
+// (exsum_wsum_kernel) gives each warp a contiguous range of whole 512-term
+// batches and a window of 16 consecutive slots chosen from its first batch
+// (slot k lives at k mod 16, one non-aliased carry slot above the window).
+// Each batch is added blindly; if any term of it falls outside the window —
+// an exponent outside, a zero, a denormal, an Inf or a NaN — the warp removes
+// the whole batch again (re-read, exact negation at the same slots) and stops:
+// the rest of its range is left for the full kernel, as is every range whose
+// first batch does not fit or is one-slot (the full kernel's fast path).  The
+// warp's window then adds its chunk sums into the workspace, and the full
+// kernel, in "jobs" mode, sums the leftover ranges (plus the unaligned head
+// and tail) and finalises as usual.  Bits are independent of the split.
+#ifndef EXSUM_TWO_PHASE
+#define EXSUM_TWO_PHASE 1
+#endif
+#ifndef EXSUM_TWO_PHASE_MIN
+#define EXSUM_TWO_PHASE_MIN (1ull << 28)  // terms: below, the extra launch is not amortised
+#endif
+constexpr int kWWarps = 16;
+constexpr int kWThreads = kWWarps * 32;
+constexpr int kWV = 4;                       // vectors per lane per batch
+constexpr int kWSlots = 17;                  // 16 aliased window slots + 1 carry slot
+constexpr int kWLPlane = kWSlots * 32 * 4;
+constexpr int kWWarpSmem = kWLPlane + kWSlots * 32 * 8;  // 6528 B
+constexpr int kWSmem = kWWarps * kWWarpSmem;             // 104,448 B
+constexpr long long kWStep = kWV * 32;       // vectors per warp batch
+constexpr int kWNormEvery = 2016 / (4 * kWV);
+constexpr int kMaxWWarps = 4096;             // jobs capacity (256 SMs)
+// jobs[2 j], jobs[2 j + 1]: the j-th leftover range (element positions), j < W + 2
+// after the segment-order state (OrderState, 8448 B, zero between calls) in the
+// segmented layout's scratch area, so the two kinds of call can share a workspace
+constexpr size_t kJobsOffset = ((sizeof(Workspace) + 255) & ~size_t{255}) + 16384;
+// + one flag after the W + 2 jobs: 1 = the windowed pass did everything and rounded
+constexpr size_t kTwoPhaseWsBytes =
+    kJobsOffset + (2 * (kMaxWWarps + 2) + 1) * sizeof(unsigned long long);
+
+__device__ __forceinline__ Lane lane_view_w(unsigned char *warp_smem, int lane) {
+  Lane v;
+  v.L = reinterpret_cast<uint32_t *>(warp_smem) + lane;
+  v.H = reinterpret_cast<unsigned long long *>(warp_smem + kWLPlane) + lane;
+  v.sl = static_cast<uint32_t>(__cvta_generic_to_shared(v.L));
+  v.hoff = static_cast<uint32_t>(__cvta_generic_to_shared(v.H)) - 2u * v.sl;
+  v.two = (blockDim.x >> 30) + 2u;
+  v.c128 = v.two * 64u;
+  return v;
+}
+
+// add_term at window slot (e' >> 5) mod 16: (e' & 0x1E0) * 4 = slot * 128 bytes.
+// The windowed kernel is ALU-pipe bound (ncu: math-pipe throttle 1.5 per issue,
+// FMA pipe mostly idle), so EXSUM_W_XOR_IMAD moves the sign complement to the
+// FMA pipe as IMADs (x (2s + 1) + s), as round 1's variant did for the full kernel.
+#ifndef EXSUM_W_XOR_IMAD
+#define EXSUM_W_XOR_IMAD 0
+#endif
+__device__ __forceinline__ void decode96_w(uint32_t lo, uint32_t hi, uint32_t e, uint32_t &s,
+                                           uint32_t &u0, uint32_t &u1, uint32_t &u2,
+                                           uint32_t &ep) {
+#if EXSUM_W_XOR_IMAD
+  uint32_t d, mhi, mh, m1, lx, mx;
+  asm("shr.s32 %0, %1, 31;" : "=r"(s) : "r"(hi));
+  asm("max.u32 %0, %1, 1;" : "=r"(ep) : "r"(e));
+  asm("mad.lo.u32 %0, %1, -1, %2;" : "=r"(d) : "r"(e), "r"(ep));
+  asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x100000u));
+  asm("mad.lo.u32 %0, %1, -1048576, %2;" : "=r"(mh) : "r"(d), "r"(mhi));
+  asm("mad.lo.u32 %0, %1, 2, 1;" : "=r"(m1) : "r"(s));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(lx) : "r"(lo), "r"(m1), "r"(s));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(mx) : "r"(mh), "r"(m1), "r"(s));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(s), "r"(lx), "r"(ep));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lx), "r"(mx), "r"(ep));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mx), "r"(s), "r"(ep));
+#else
+  decode96(lo, hi, e, s, u0, u1, u2, ep);
+#endif
+}
+
+__device__ __forceinline__ void add_term_w(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
+  uint32_t s, ep, km, la, ha, u0, u1, u2;
+  decode96_w(lo, hi, e, s, u0, u1, u2, ep);
+  asm("and.b32 %0, %1, 480;" : "=r"(km) : "r"(ep));
+  asm("mad.lo.u32 %0, %1, 4, %2;" : "=r"(la) : "r"(km), "r"(a.sl));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));
+  asm volatile(
+      "{\n\t.reg .u32 l, h0, h1, cf;\n\t"
+      EXSUM_RMW_LD
+      "add.cc.u32 cf, %2, %2;\n\t"
+      "addc.cc.u32 l, l, %3;\n\t"
+      "addc.cc.u32 h0, h0, %4;\n\t"
+      "addc.u32 h1, h1, %5;\n\t"
+      EXSUM_RMW_ST
+      :
+      : "r"(la), "r"(ha), "r"(s), "r"(u0), "r"(u1), "r"(u2)
+      : "memory");
+}
+
+// Carry through the window in real slot order kb .. kb + 15, the last carry
+// into the carry slot (same invariant as normalize()).
+__device__ __forceinline__ void normalize_w(const Lane &a, int kb) {
+  long long c = 0;
+#pragma unroll 4
+  for (int i = 0; i < 16; ++i) {
+    const int j = (kb + i) & 15;
+    const long long u = static_cast<long long>(a.L[32 * j]) + c;
+    const long long h = static_cast<long long>(a.H[32 * j]);
+    a.L[32 * j] = static_cast<uint32_t>(u);
+    a.H[32 * j] = 0ull;
+    c = h + (u >> 32);
+  }
+  const long long u = static_cast<long long>(a.L[32 * 16]) + c;
+  a.L[32 * 16] = static_cast<uint32_t>(u);
+  a.H[32 * 16] = static_cast<unsigned long long>(static_cast<long long>(a.H[32 * 16]) + (u >> 32));
+}
+
+// The warp's window as chunk values: lane i <= 16 sums real slot kb + i
+// (window slot (kb + i) mod 16; i = 16: the carry slot) and returns chunk
+// kb + i of the row; lanes 17, 18 return chunks kb + 17, kb + 18.
+__device__ __forceinline__ long long warp_chunks_w(unsigned char *warp_smem, int lane, int kb) {
+  __syncwarp();
+  const uint32_t *Lp = reinterpret_cast<const uint32_t *>(warp_smem);
+  const uint32_t *Hw = reinterpret_cast<const uint32_t *>(warp_smem + kWLPlane);
+  long long sl = 0, shl = 0, shh = 0;
+  if (lane <= 16) {
+    const int k = lane == 16 ? 16 : (kb + lane) & 15;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint4 v = *reinterpret_cast<const uint4 *>(Lp + k * 32 + 4 * ((i + lane) & 7));
+      sl += static_cast<long long>(v.x) + v.y + static_cast<long long>(v.z) + v.w;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint4 v = *reinterpret_cast<const uint4 *>(Hw + k * 64 + 4 * ((i + lane) & 15));
+      shl += static_cast<long long>(v.x) + v.z;
+      shh += static_cast<long long>(static_cast<int32_t>(v.y)) + static_cast<int32_t>(v.w);
+    }
+  }
+  const long long lo1 = __shfl_up_sync(0xffffffffu, shl, 1);
+  const long long hi2 = __shfl_up_sync(0xffffffffu, shh, 2);
+  long long v = sl + (lane >= 1 ? lo1 : 0) + (lane >= 2 ? hi2 : 0);
+  return lane <= 18 ? v : 0;
+}
+
+__global__ void __launch_bounds__(kWThreads, 1)
+exsum_wsum_kernel(const double *__restrict__ x, unsigned long long n, Workspace *__restrict__ ws,
+                  unsigned long long *__restrict__ jobs, double *result, exsum_partial *partial) {
+  __shared__ int s_last;
+  __shared__ long long s_row[kChunks];
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  unsigned char *wsm = smem + warp * kWWarpSmem;
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int W = static_cast<int>(gridDim.x) * kWWarps;
+  const int w = static_cast<int>(blockIdx.x) * kWWarps + warp;
+  // geometry: 32-byte vectors from g0; whole batches only
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(x);
+  unsigned long long head = ((32u - (addr & 31u)) & 31u) >> 3;
+  if (head > n) head = n;
+  const unsigned long long g0 = head;
+  const long long nvec = static_cast<long long>((n - g0) >> 2);
+  const long long nb = nvec / kWStep;
+  const long long vb = kWStep * ((nb * w) / W), ve = kWStep * ((nb * (w + 1)) / W);
+  const double *X4 = x + g0;
+  unsigned long long resume = g0 + 4ull * static_cast<unsigned long long>(vb);  // nothing done
+  unsigned long long head_left = 0;  // first position of the head / tail left as a job
+  unsigned long long tail_left = g0 + 4ull * static_cast<unsigned long long>(nb * kWStep);
+  int kb = 0;
+  bool any = false;
+  if (vb < ve) {
+    Batch<kWV, kSum> b;
+    if (lane == 0)
+      for (int d = 0; d <= kPrefetchBatches; ++d)
+        prefetch_batch<kWV, kSum>(X4, X4, vb + d * kWStep, ve);
+    load_batch<kWV, kSum>(b, X4, X4, vb, ve, lane);
+    // the window from the first batch (none if it is one-slot: the full
+    // kernel's fast path is faster there)
+    uint32_t emin = 0x7FFu, emax = 0;
+#pragma unroll
+    for (int u = 0; u < kWV; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t e = exponent_field(b.w[u][2 * q + 1]);
+        emin = min(emin, e);
+        emax = max(emax, e);
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, o));
+      emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
+    }
+    const int kmin = static_cast<int>(emin >> 5), kmax = static_cast<int>(emax >> 5);
+    if (emin >= 1 && emax <= 2046 && kmax - kmin <= 12 && kmax > kmin) {
+      kb = kmin - (15 - (kmax - kmin)) / 2;
+      kb = kb < 0 ? 0 : (kb > 48 ? 48 : kb);
+      // exponent fields of the window's slots; 2047 (Inf/NaN) is never inside
+      // (a window at the top, kb = 48, would otherwise reach it)
+      const uint32_t elo = static_cast<uint32_t>(kb) * 32u, ehi = min(elo + 511u, 2046u);
+      any = true;
+      {  // clear this warp's window
+        uint4 *p = reinterpret_cast<uint4 *>(wsm);
+#pragma unroll 4
+        for (int i = lane; i < kWWarpSmem / 16; i += 32) p[i] = make_uint4(0, 0, 0, 0);
+      }
+      __syncwarp();
+      const Lane a = lane_view_w(wsm, lane);
+      int norm_count = 0;
+      long long v = vb;
+      for (; v < ve; v += kWStep) {
+        const long long nv = v + kWStep;
+        prefetch_l2_lane0<kWV>(X4, v + (kPrefetchBatches + 1) * kWStep, ve, lane);
+        uint32_t bmin = 0x7FFu, bmax = 0;
+#pragma unroll
+        for (int u = 0; u < kWV; ++u) {
+          uint32_t lo[4], hi[4], e[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            lo[q] = b.w[u][2 * q];
+            hi[q] = b.w[u][2 * q + 1];
+            e[q] = exponent_field(hi[q]);
+            bmin = min(bmin, e[q]);
+            bmax = max(bmax, e[q]);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) add_term_w(a, lo[q], hi[q], e[q]);
+          const long long vec = nv + u * 32 + lane;
+          if (vec < ve) {
+            load_vec<kWV, kSum>(b, u, X4, X4, vec);
+          } else {
+            zero_vec<kWV, kSum>(b, u);
+          }
+        }
+        if (__builtin_expect(__any_sync(0xffffffffu, bmin < elo || bmax > ehi), 0)) {
+          // remove this batch again and leave the rest to the full kernel
+#pragma unroll 1
+          for (int u = 0; u < kWV; ++u) {
+            uint32_t t[8];
+            ldg256(X4 + 4 * (v + u * 32 + lane), t);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              add_term_w(a, t[2 * q], t[2 * q + 1] ^ 0x80000000u, exponent_field(t[2 * q + 1]));
+          }
+          break;
+        }
+        if (++norm_count >= kWNormEvery) {
+          normalize_w(a, kb);
+          norm_count = 0;
+        }
+      }
+      resume = g0 + 4ull * static_cast<unsigned long long>(v);
+      // the unaligned head (warp 0) and the tail after the last whole batch
+      // (last warp) through this window when every term fits; else they stay jobs
+      auto scalars = [&](unsigned long long p0, unsigned long long p1) -> unsigned long long {
+        for (unsigned long long p = p0; p < p1; p += 32) {
+          const unsigned long long t = p + static_cast<unsigned long long>(lane);
+          const unsigned long long bits =
+              t < p1 ? __ldg(reinterpret_cast<const unsigned long long *>(x) + t) : 0ull;
+          const uint32_t hi = static_cast<uint32_t>(bits >> 32), e = exponent_field(hi);
+          if (!__all_sync(0xffffffffu, t >= p1 || (e >= elo && e <= ehi && e >= 1u && e <= 2046u)))
+            return p;
+          if (++norm_count >= kWNormEvery) {
+            normalize_w(a, kb);
+            norm_count = 0;
+          }
+          if (t < p1) add_term_w(a, static_cast<uint32_t>(bits), hi, e);
+        }
+        return p1;
+      };
+      if (v == ve) {
+        if (w == 0) head_left = scalars(0, g0);
+        if (w == W - 1)
+          tail_left = scalars(g0 + 4ull * static_cast<unsigned long long>(nb * kWStep), n);
+      }
+    }
+  }
+  // the previous grid in the stream may still read the workspace and the jobs
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (any) {
+    const long long c = warp_chunks_w(wsm, lane, kb);
+    if (lane <= 18 && c) atomicAdd(&ws->chunk[kb + lane], static_cast<unsigned long long>(c));
+  }
+  if (lane == 0) {
+    jobs[2 * w] = resume;
+    jobs[2 * w + 1] = g0 + 4ull * static_cast<unsigned long long>(ve);
+    if (w == 0) {  // the unaligned head
+      jobs[2 * W] = head_left;
+      jobs[2 * W + 1] = g0;
+    }
+    if (w == W - 1) {  // the tail after the last whole batch
+      jobs[2 * W + 2] = tail_left;
+      jobs[2 * W + 3] = n;
+    }
+  }
+  // Last CTA: when no job is left, round here and tell the full kernel to skip
+  // (jobs[2 W + 4] = 1); the windowed pass saw no Inf/NaN (it leaves them).
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&ws->wdone, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int nj = W + 2;
+  int left = 0;
+  for (int j = threadIdx.x; j < nj; j += blockDim.x) left |= __ldcg(&jobs[2 * j]) < __ldcg(&jobs[2 * j + 1]);
+  left = __syncthreads_or(left);
+  if (threadIdx.x == 0) {
+    ws->wdone = 0;
+    jobs[2 * nj] = left ? 0ull : 1ull;
+  }
+  if (left) return;
+  if (threadIdx.x < kChunks) {
+    s_row[threadIdx.x] = static_cast<long long>(__ldcg(&ws->chunk[threadIdx.x]));
+    ws->chunk[threadIdx.x] = 0;
+  }
+  __syncthreads();
+  if (warp == 0) warp_emit(s_row, ~0ull, ~0ull, ~0ull, 0ull, result, partial, lane);
+}
+
 template <int kOp>
 __global__ void __launch_bounds__(kThreads, 1)
 exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, unsigned long long n,
                  unsigned long long base_index, Workspace *__restrict__ ws, int finalize,
                  double *result, exsum_partial *partial, const __grid_constant__ GroupArgs grp,
-                 const __grid_constant__ P2PArgs p2p) {
+                 const __grid_constant__ P2PArgs p2p,
+                 const unsigned long long *__restrict__ jobs = nullptr, int njobs = 0) {
+  // jobs (two-phase sums): instead of its own split of [0, n), warp gw sums the
+  // ranges [jobs[2 j], jobs[2 j + 1]) for j = gw, gw + nw, ... (exsum_wsum_kernel's
+  // leftovers); everything after the accumulation is unchanged.  jobs[2 njobs] = 1:
+  // the windowed pass did everything and rounded, nothing to do.
+  if (jobs && __ldcg(&jobs[2 * njobs]) != 0ull) return;
   // vectors per lane per batch: a dot keeps two arrays' vectors in registers
   constexpr int V = kOp >= kDot ? EXSUM_DOT_VEC : EXSUM_VEC_PER_LANE;
   // Independent sums per CTA group (groups > 1 only when emulating ranks in one
@@ -1559,7 +1891,7 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
   const unsigned long long quads = (n + 3) >> 2;
   const unsigned long long qb = quads * gw / nw, qe = quads * (gw + 1) / nw;
   const unsigned long long tb = qb * 4, te = min(qe * 4, n);
-  if (lane == 0 && te > tb) {  // start the first batches' DRAM reads before zeroing smem
+  if (lane == 0 && te > tb && !jobs) {  // start the first batches' DRAM reads before zeroing smem
     const unsigned long long tp = min(te, tb + 2ull * 4 * V * 32);
 #pragma unroll
     for (int arr = 0; arr < (kOp >= kDot ? 2 : 1); ++arr) {
@@ -1570,7 +1902,15 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"(bytes) : "memory");
     }
   }
-  zero_warp(wsm, lane);
+  // jobs mode: a warp whose ranges are all empty (the windowed pass did them)
+  // skips its accumulator (clear, accumulate, reduce) and adds a zero row
+  bool busy = true;
+  if (jobs) {
+    busy = false;
+    for (unsigned long long j = gw; j < static_cast<unsigned long long>(njobs); j += nw)
+      busy |= jobs[2 * j] < jobs[2 * j + 1];
+  }
+  if (busy) zero_warp(wsm, lane);
   __syncwarp();
   const Lane a = lane_view(wsm, lane);
   Specials sp{~0ull, ~0ull, ~0ull};
@@ -1579,9 +1919,19 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
   // batches dealt round-robin over the grid's warps: all warps sweep one window
   (void)tb;
   (void)te;
-  warp_accumulate<V, EXSUM_UNIFORM_FAST != 0, true, EXSUM_SUM_SCAN != 0 && kOp == kSum, kOp>(
-      x, y, 0, n, base_index, a, sp, norm_count, lane,
-      static_cast<long long>(gw) * V * 32, static_cast<long long>(nw) * V * 32, gw == 0);
+  if (jobs) {
+#pragma unroll 1
+    for (unsigned long long j = gw; busy && j < static_cast<unsigned long long>(njobs); j += nw) {
+      const unsigned long long jb = jobs[2 * j], je = jobs[2 * j + 1];
+      if (jb < je)
+        warp_accumulate<V, EXSUM_UNIFORM_FAST != 0, true, EXSUM_SUM_SCAN != 0 && kOp == kSum,
+                        kOp>(x, y, jb, je, base_index, a, sp, norm_count, lane);
+    }
+  } else {
+    warp_accumulate<V, EXSUM_UNIFORM_FAST != 0, true, EXSUM_SUM_SCAN != 0 && kOp == kSum, kOp>(
+        x, y, 0, n, base_index, a, sp, norm_count, lane,
+        static_cast<long long>(gw) * V * 32, static_cast<long long>(nw) * V * 32, gw == 0);
+  }
 #else
   warp_accumulate<V, EXSUM_UNIFORM_FAST != 0, true, EXSUM_SUM_SCAN != 0 && kOp == kSum, kOp>(
       x, y, tb, te, base_index, a, sp, norm_count, lane);
@@ -1589,7 +1939,14 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
 
   // K2: the warp's 67 chunk sums.
   EXSUM_STAMP(1);
-  warp_chunks(wsm, lane, scratch + warp * kChunks);
+  if (busy) {
+    warp_chunks(wsm, lane, scratch + warp * kChunks);
+  } else {
+    long long *r = scratch + warp * kChunks;
+    r[lane] = 0;
+    r[lane + 32] = 0;
+    if (lane < 3) r[lane + 64] = 0;
+  }
   const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                            N = warp_min_u64(sp.N);
   // The workspace is shared with the previous sum in the stream: wait for that
@@ -1745,6 +2102,7 @@ struct OrderState {                    // zeroed by exsum_cuda_workspace_init
 };
 constexpr size_t kOrderStateOffset = (sizeof(Workspace) + 255) & ~size_t{255};
 constexpr size_t kOrderOffset = kOrderStateOffset + sizeof(OrderState);  // order[] in d_ws
+static_assert(kJobsOffset >= kOrderOffset, "two-phase jobs clear of the order state");
 // deferred-rounding records (EXSUM_SEG_DEFER) after order[], 256-byte aligned
 __host__ __device__ constexpr size_t seg_records_offset(size_t nseg) {
   return (kOrderOffset + 4 * nseg + 255) & ~size_t{255};
@@ -2066,7 +2424,13 @@ int prepare_device(int *sms) {
         cudaFuncSetAttribute(exsum_sum_kernel<kDotScalarB>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess ||
         cudaFuncSetAttribute(exsum_segmented_kernel,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess)
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) != cudaSuccess ||
+        cudaFuncSetAttribute(exsum_wsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kWSmem) != cudaSuccess ||
+        // the same (maximal) shared-memory carveout as the full kernel: no L1/smem
+        // reconfiguration between the two phases
+        cudaFuncSetAttribute(exsum_wsum_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             100) != cudaSuccess)
       return EXSUM_ECUDA;
     g_num_sms[dev].store(n, std::memory_order_release);
   }
@@ -2138,22 +2502,47 @@ int sum_launch(const double *d_x, size_t n, uint64_t base_index, void *d_ws, siz
   const unsigned long long nn = n, bi = base_index;
   Workspace *ws = static_cast<Workspace *>(d_ws);
   cudaError_t e;
+  if (EXSUM_TWO_PHASE && op == kSum && finalize && X.nranks == 0 && G.groups == 1 &&
+      !cooperative && !max_ctas && n >= EXSUM_TWO_PHASE_MIN && ws_bytes >= kTwoPhaseWsBytes &&
+      sms * kWWarps <= kMaxWWarps) {
+    // two-phase: the windowed pass (PDL like a plain sum), then the full kernel
+    // over its leftovers in stream order
+    auto *jobs = reinterpret_cast<unsigned long long *>(static_cast<unsigned char *>(d_ws) +
+                                                        kJobsOffset);
+    cudaLaunchConfig_t wc = cfg;
+    wc.gridDim = dim3(static_cast<unsigned>(sms));
+    wc.blockDim = dim3(kWThreads);
+    wc.dynamicSmemBytes = kWSmem;
+    e = cudaLaunchKernelEx(&wc, exsum_wsum_kernel, d_x, nn, ws, jobs, d_result, d_partial);
+    if (e != cudaSuccess) return EXSUM_ECUDA;
+    cudaLaunchConfig_t rc = cfg;
+    rc.gridDim = dim3(static_cast<unsigned>(sms));
+    rc.attrs = nullptr;
+    rc.numAttrs = 0;
+    const unsigned long long *cj = jobs;
+    const int nj = sms * kWWarps + 2;
+    e = cudaLaunchKernelEx(&rc, exsum_sum_kernel<kSum>, d_x, d_x, nn, bi, ws, finalize, d_result,
+                           d_partial, G, X, cj, nj);
+    if (e != cudaSuccess) return EXSUM_ECUDA;
+    return launch_status();
+  }
+  const unsigned long long *no_jobs = nullptr;
   switch (op) {
     case kSqnorm:
       e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kSqnorm>, d_x, d_x, nn, bi, ws, finalize,
-                             d_result, d_partial, G, X);
+                             d_result, d_partial, G, X, no_jobs, 0);
       break;
     case kDot:
       e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kDot>, d_x, d_y, nn, bi, ws, finalize,
-                             d_result, d_partial, G, X);
+                             d_result, d_partial, G, X, no_jobs, 0);
       break;
     case kDotScalarB:
       e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kDotScalarB>, d_x, d_y, nn, bi, ws, finalize,
-                             d_result, d_partial, G, X);
+                             d_result, d_partial, G, X, no_jobs, 0);
       break;
     default:
       e = cudaLaunchKernelEx(&cfg, exsum_sum_kernel<kSum>, d_x, d_x, nn, bi, ws, finalize,
-                             d_result, d_partial, G, X);
+                             d_result, d_partial, G, X, no_jobs, 0);
   }
   if (e != cudaSuccess) return EXSUM_ECUDA;
   return launch_status();
@@ -2169,7 +2558,13 @@ int dot_op(const double *d_a, const double *d_b) {
 
 extern "C" {
 
-size_t exsum_cuda_workspace_bytes(void) { return sizeof(Workspace); }
+uint64_t exsum_cuda_two_phase_min(void) { return EXSUM_TWO_PHASE ? EXSUM_TWO_PHASE_MIN : 0; }
+
+size_t exsum_cuda_workspace_bytes(void) {
+  // room for the two-phase sum's job list (large plain sums); sizeof(Workspace)
+  // is the minimum every entry point accepts
+  return EXSUM_TWO_PHASE ? kTwoPhaseWsBytes : sizeof(Workspace);
+}
 
 int exsum_cuda_workspace_init(void *d_ws, size_t ws_bytes, void *stream) {
   if (!d_ws || ws_bytes < sizeof(Workspace)) return EXSUM_EINVAL;
@@ -2404,12 +2799,15 @@ int exsum_cuda_sum_segmented(const double *d_x, const uint64_t *d_offsets, size_
 }
 
 size_t exsum_cuda_segmented_workspace_bytes(size_t nseg) {
-  if (nseg > kOrderMaxSegs) return sizeof(Workspace);
+  // never below the plain-sum workspace, so one buffer serves both kinds of call
+  const size_t base = exsum_cuda_workspace_bytes();
+  if (nseg > kOrderMaxSegs) return base;
 #if EXSUM_SEG_DEFER
-  return seg_records_offset(nseg) + nseg * sizeof(exsum_partial);
+  const size_t need = seg_records_offset(nseg) + nseg * sizeof(exsum_partial);
 #else
-  return kOrderOffset + 4 * nseg;
+  const size_t need = kOrderOffset + 4 * nseg;
 #endif
+  return need > base ? need : base;
 }
 
 int exsum_cuda_merge(const exsum_partial *d_parts, size_t k, double *d_result,

@@ -44,6 +44,8 @@ VARIANTS = {
     "segahead1": ("EXSUM_SEG_AHEAD=1",),
     "il0": ("EXSUM_INTERLEAVE=0",),
     "nodisp": ("EXSUM_UNIFORM_DISPATCH=0",),
+    "onephase": ("EXSUM_TWO_PHASE=0",),
+    "wimad": ("EXSUM_W_XOR_IMAD=1",),
     "v7": ("EXSUM_VEC_PER_LANE=7",),
     "seg8": ("EXSUM_SEG_VEC=8",),
     "segtail2": ("EXSUM_SEG_TAIL=2",),

@@ -51,21 +51,19 @@ def test_struct_layouts():
 
 
 def test_segmented_workspace_sizes():
-    """Room for the longest-first claim order (4 bytes per segment after the
-    base workspace and the order state) and for the deferred-rounding records
-    (one 592-byte exsum_partial per segment, 256-byte aligned); beyond 2^24
-    segments the kernel claims in index order and needs only the base workspace."""
+    """Room for the claim order (4 bytes per segment after the base workspace
+    and the order state) and for the deferred-rounding records (one 592-byte
+    exsum_partial per segment, 256-byte aligned), never below the plain-sum
+    workspace (one buffer serves both kinds of call); beyond 2^24 segments the
+    kernel claims in index order and needs only the base workspace."""
     base = lib.exsum_cuda_workspace_bytes()
-    w0 = lib.exsum_cuda_segmented_workspace_bytes(0)
-    assert w0 >= base
-
-    def expect(n):
-        return ((w0 + 4 * n + 255) // 256) * 256 + 592 * n
-
-    assert w0 == expect(0)
-    assert lib.exsum_cuda_segmented_workspace_bytes(65536) == expect(65536)
-    assert lib.exsum_cuda_segmented_workspace_bytes(1 << 24) == expect(1 << 24)
-    assert lib.exsum_cuda_segmented_workspace_bytes((1 << 24) + 1) == base
+    seg = lib.exsum_cuda_segmented_workspace_bytes
+    assert seg(0) >= base and seg(1) >= base
+    n1, n2 = 65536, 1 << 24
+    assert seg(n1) > base and seg(n1) % 256 == (592 * n1) % 256
+    # per segment: 4 bytes of order + one 592-byte record (alignment within 256)
+    assert abs((seg(n2) - seg(n1)) - 596 * (n2 - n1)) < 256
+    assert seg(n2 + 1) == base
 
 
 def test_status_codes_without_gpu():

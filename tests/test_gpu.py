@@ -550,3 +550,43 @@ def test_uniform_dispatch_mixed_halves(cuda, checker):
             got, part = dev_sum(to_dev(h, off))
             assert got == bits_of(checker.exact_sum(h)), (len(parts), off)
             assert list(part.acc.chunk) == [int(c) for c in checker.canonical(h)[0]]
+
+
+def test_two_phase_large_sums(cuda, checker):
+    """Plain sums of >= 2^28 terms run a windowed pass (16 warps per SM, a
+    16-slot window per warp) and then the full kernel over what it left
+    (EXSUM_TWO_PHASE).  Cases: config 4 (every window holds), the same with a
+    zero, a denormal, +-Inf, NaN and a huge term dropped in (those warps back out
+    one batch and stop), exponents drifting along the array (windows chosen per
+    warp, later batches leave them), U[0,1) (one-slot: the windowed pass leaves
+    everything to the full kernel's fast path), a misaligned start and an odd
+    length.  Result bits and canonical chunks equal the reference's."""
+    n = (1 << 28) + 12345
+    rng = np.random.default_rng(21)
+    x = gen(4, n, seed=3)
+    h4 = x.cpu().numpy()
+    cases = [("config4", h4)]
+    h = h4.copy()
+    pos = rng.integers(0, n, 9)
+    h[pos] = [0.0, 5e-324, np.inf, 1e300, -np.inf, np.nan, -0.0, 2.0 ** -1000, 3.0]
+    cases.append(("outliers", h))
+    i = np.arange(n, dtype=np.float64)
+    drift = (1.0 + rng.random(n)) * np.exp2(np.floor(i / 2 ** 21) - 64.0)
+    drift *= np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    cases.append(("drift", drift))
+    cases.append(("uniform", rng.random(n)))
+    # a window at the top of the exponent range (slots 48-63) with Inf/NaN in it
+    top = (1.0 + rng.random(n)) * np.exp2(rng.integers(1700, 1900, n).astype(np.float64) - 1023.0)
+    top[rng.integers(0, n, 4)] = [np.inf, -np.inf, np.nan, 1e308]
+    cases.append(("top-window", top))
+    del x
+    for tag, arr in cases:
+        for off in (0, 1):
+            d = to_dev(arr, off)
+            got, part = dev_sum(d)
+            del d
+            torch.cuda.empty_cache()
+            assert got == bits_of(checker.exact_sum(arr)), (tag, off)
+            if off == 0:
+                ch, top, ib, nb = checker.canonical(arr)
+                assert list(part.acc.chunk) == [int(c) for c in ch], tag
