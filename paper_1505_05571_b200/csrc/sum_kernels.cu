@@ -1555,7 +1555,22 @@ constexpr int kWV = 4;                       // vectors per lane per batch
 constexpr int kWSlots = 17;                  // 16 aliased window slots + 1 carry slot
 constexpr int kWLPlane = kWSlots * 32 * 4;
 constexpr int kWWarpSmem = kWLPlane + kWSlots * 32 * 8;  // 6528 B
-constexpr int kWSmem = kWWarps * kWWarpSmem;             // 104,448 B
+// Two sign planes (EXSUM_W_PLANES = 2, default): the window holds unsigned
+// magnitudes, one plane per sign, so a term needs no sign complement, no
+// carry-in and no exponent extraction (see add_w2).  CTA layout, 204 KB:
+//   L region [0, 64 KB): warp w's positive plane at (w >> 2) 16 KB + (w & 3) 2 KB,
+//     its negative plane 8 KB above (the sign bit lands there: add_w2);
+//     16 window slots x 32 lanes x 4 B each
+//   H region [64 KB, 192 KB): the same with doubled offsets (64-bit high parts)
+//   C region [192 KB, 204 KB): per warp and sign the carry slot, L (128 B) + H (256 B)
+#ifndef EXSUM_W_PLANES
+#define EXSUM_W_PLANES 2
+#endif
+constexpr int kW2LRegion = kWWarps * 2 * 2048;
+constexpr int kW2HRegion = 2 * kW2LRegion;
+constexpr int kW2CSlot = 32 * 4 + 32 * 8;
+constexpr int kW2Smem = kW2LRegion + kW2HRegion + kWWarps * 2 * kW2CSlot;  // 208,896 B
+constexpr int kWSmem = EXSUM_W_PLANES == 2 ? kW2Smem : kWWarps * kWWarpSmem;  // 104,448 B (one plane)
 constexpr long long kWStep = kWV * 32;       // vectors per warp batch
 constexpr int kWNormEvery = 2016 / (4 * kWV);
 constexpr int kMaxWWarps = 4096;             // jobs capacity (256 SMs)
@@ -1671,6 +1686,167 @@ __device__ __forceinline__ long long warp_chunks_w(unsigned char *warp_smem, int
   return lane <= 18 ? v : 0;
 }
 
+// ---- two sign planes (EXSUM_W_PLANES = 2) ----
+// A window slot holds an unsigned 96-bit magnitude sum (L: low 32 bits, H:
+// high 64).  Per term (ALU: shr, and, lop3, 3 funnel shifts, max, 3 adds;
+// FMA: the fit value and the two addresses), against the one-plane decode's
+// sign mask, implicit-bit and denormal handling and sign complement:
+//   sh = hi >> 20 = s << 11 | e: shift amount (e mod 32, the funnel shifts
+//        use sh mod 32) and, masked with 0x9E0, s << 11 | (e >> 5 mod 16) << 5:
+//        times 4 the byte offset of the term's plane and window slot.
+//   fit = 2 hi - (elo << 21): (e - elo) << 21 | mantissa bits for e >= elo, a
+//        wrapped (huge) value below; the batch fits iff max(fit) <= lim.
+// Window slots hold exponent fields e >= 32 only (kb >= 1): normal terms, so
+// the implicit bit is always set.
+struct WLane2 {
+  uint32_t sl;    // shared address of this lane's positive-plane slot 0 (L)
+  uint32_t hoff;  // H address = 2 L address + hoff
+  uint32_t two;   // 2 and 4, opaque to ptxas (IMADs on the FMA pipe)
+  uint32_t four;
+  uint32_t *L;             // generic: positive plane slot 0, slot k at L[32 k], negative at +2048
+  unsigned long long *H;   // the same for H (negative at +2048)
+  uint32_t *CL;            // carry slot of the positive plane, negative at +96 words
+  unsigned long long *CH;  // its H words, negative at +48
+};
+
+__device__ __forceinline__ WLane2 lane_view_w2(unsigned char *smem, int warp, int lane) {
+  WLane2 v;
+  const int loff = (warp >> 2) * 16384 + (warp & 3) * 2048 + lane * 4;
+  v.L = reinterpret_cast<uint32_t *>(smem + loff);
+  v.H = reinterpret_cast<unsigned long long *>(smem + kW2LRegion + 2 * loff);
+  unsigned char *c = smem + kW2LRegion + kW2HRegion + warp * 2 * kW2CSlot;
+  v.CL = reinterpret_cast<uint32_t *>(c) + lane;
+  v.CH = reinterpret_cast<unsigned long long *>(c + 128) + lane;
+  const uint32_t base = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  v.sl = base + static_cast<uint32_t>(loff);
+  v.hoff = base + static_cast<uint32_t>(kW2LRegion) - 2u * base;
+  v.two = (blockDim.x >> 30) + 2u;
+  v.four = v.two + v.two;
+  return v;
+}
+
+// Zero the warp's planes and carry slots.
+__device__ __forceinline__ void zero_w2(unsigned char *smem, int warp, int lane) {
+  const int l0 = (warp >> 2) * 16384 + (warp & 3) * 2048;
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    uint4 *pl = reinterpret_cast<uint4 *>(smem + l0 + s * 8192);
+    uint4 *ph = reinterpret_cast<uint4 *>(smem + kW2LRegion + 2 * (l0 + s * 8192));
+#pragma unroll
+    for (int i = lane; i < 128; i += 32) pl[i] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int i = lane; i < 256; i += 32) ph[i] = make_uint4(0, 0, 0, 0);
+  }
+  uint4 *pc = reinterpret_cast<uint4 *>(smem + kW2LRegion + kW2HRegion + warp * 2 * kW2CSlot);
+  for (int i = lane; i < 2 * kW2CSlot / 16; i += 32) pc[i] = make_uint4(0, 0, 0, 0);
+}
+
+// The term (lo, hi) added to (kSub: subtracted from) its plane's window slot;
+// returns the fit value.
+template <bool kSub>
+__device__ __forceinline__ uint32_t add_w2(const WLane2 &a, uint32_t lo, uint32_t hi,
+                                           uint32_t neg_elo21) {
+  uint32_t fit, sh, t, mhi, u0, u1, u2, la, ha;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(fit) : "r"(hi), "r"(a.two), "r"(neg_elo21));
+  asm("shr.u32 %0, %1, 20;" : "=r"(sh) : "r"(hi));
+  asm("and.b32 %0, %1, 2528;" : "=r"(t) : "r"(sh));  // 0x9E0
+  asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x100000u));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(0u), "r"(lo), "r"(sh));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lo), "r"(mhi), "r"(sh));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mhi), "r"(0u), "r"(sh));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(t), "r"(a.four), "r"(a.sl));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));
+  if constexpr (kSub) {
+    asm volatile(
+        "{\n\t.reg .u32 l, h0, h1;\n\t" EXSUM_RMW_LD
+        "sub.cc.u32 l, l, %2;\n\t"
+        "subc.cc.u32 h0, h0, %3;\n\t"
+        "subc.u32 h1, h1, %4;\n\t" EXSUM_RMW_ST
+        :
+        : "r"(la), "r"(ha), "r"(u0), "r"(u1), "r"(u2)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .u32 l, h0, h1;\n\t" EXSUM_RMW_LD
+        "add.cc.u32 l, l, %2;\n\t"
+        "addc.cc.u32 h0, h0, %3;\n\t"
+        "addc.u32 h1, h1, %4;\n\t" EXSUM_RMW_ST
+        :
+        : "r"(la), "r"(ha), "r"(u0), "r"(u1), "r"(u2)
+        : "memory");
+  }
+  return fit;
+}
+
+// Carry each plane through real slots kb .. kb + 15 into its carry slot
+// (unsigned: every slot sum stays below 2^96, normalize every kWNormEvery batches).
+__device__ __forceinline__ void normalize_w2(const WLane2 &a, int kb) {
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    uint32_t *L = a.L + s * 2048;
+    unsigned long long *H = a.H + s * 2048;
+    unsigned long long c = 0;
+#pragma unroll 4
+    for (int i = 0; i < 16; ++i) {
+      const int j = (kb + i) & 15;
+      const unsigned long long u = static_cast<unsigned long long>(L[32 * j]) + c;
+      const unsigned long long h = H[32 * j];
+      L[32 * j] = static_cast<uint32_t>(u);
+      H[32 * j] = 0ull;
+      c = h + (u >> 32);
+    }
+    uint32_t *CL = a.CL + s * 96;
+    unsigned long long *CH = a.CH + s * 48;
+    const unsigned long long u = static_cast<unsigned long long>(*CL) + c;
+    *CL = static_cast<uint32_t>(u);
+    *CH += u >> 32;
+  }
+}
+
+// The warp's window as chunk values (positive minus negative plane): lane
+// i <= 16 sums real slot kb + i (i = 16: the carry slot) over the 32 lanes
+// and returns chunk kb + i; lanes 17, 18 return chunks kb + 17, kb + 18.
+__device__ __forceinline__ long long warp_chunks_w2(unsigned char *smem, int warp, int lane,
+                                                    int kb) {
+  __syncwarp();
+  long long sl = 0, shl = 0, shh = 0;
+  if (lane <= 16) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      const uint32_t *Lp, *Hp;
+      if (lane == 16) {
+        const unsigned char *c =
+            smem + kW2LRegion + kW2HRegion + (warp * 2 + s) * kW2CSlot;
+        Lp = reinterpret_cast<const uint32_t *>(c);
+        Hp = reinterpret_cast<const uint32_t *>(c + 128);
+      } else {
+        const int l0 = (warp >> 2) * 16384 + (warp & 3) * 2048 + s * 8192 + ((kb + lane) & 15) * 128;
+        Lp = reinterpret_cast<const uint32_t *>(smem + l0);
+        Hp = reinterpret_cast<const uint32_t *>(smem + kW2LRegion + 2 * l0);
+      }
+      long long ql = 0, qhl = 0, qhh = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(Lp + 4 * ((i + lane) & 7));
+        ql += static_cast<long long>(v.x) + v.y + static_cast<long long>(v.z) + v.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(Hp + 4 * ((i + lane) & 15));
+        qhl += static_cast<long long>(v.x) + v.z;
+        qhh += static_cast<long long>(v.y) + v.w;
+      }
+      sl += s ? -ql : ql;
+      shl += s ? -qhl : qhl;
+      shh += s ? -qhh : qhh;
+    }
+  }
+  const long long lo1 = __shfl_up_sync(0xffffffffu, shl, 1);
+  const long long hi2 = __shfl_up_sync(0xffffffffu, shh, 2);
+  long long v = sl + (lane >= 1 ? lo1 : 0) + (lane >= 2 ? hi2 : 0);
+  return lane <= 18 ? v : 0;
+}
+
 __global__ void __launch_bounds__(kWThreads, 1)
 exsum_wsum_kernel(const double *__restrict__ x, unsigned long long n, Workspace *__restrict__ ws,
                   unsigned long long *__restrict__ jobs, double *result, exsum_partial *partial) {
@@ -1679,7 +1855,9 @@ exsum_wsum_kernel(const double *__restrict__ x, unsigned long long n, Workspace 
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+#if EXSUM_W_PLANES != 2
   unsigned char *wsm = smem + warp * kWWarpSmem;
+#endif
   asm volatile("griddepcontrol.launch_dependents;");
   const int W = static_cast<int>(gridDim.x) * kWWarps;
   const int w = static_cast<int>(blockIdx.x) * kWWarps + warp;
@@ -1720,13 +1898,78 @@ exsum_wsum_kernel(const double *__restrict__ x, unsigned long long n, Workspace 
       emax = max(emax, __shfl_xor_sync(0xffffffffu, emax, o));
     }
     const int kmin = static_cast<int>(emin >> 5), kmax = static_cast<int>(emax >> 5);
+#if EXSUM_W_PLANES == 2
+    // two planes: window slots from 1 up (normal terms only)
+    if (kmin >= 1 && emax <= 2046 && kmax - kmin <= 12 && kmax > kmin) {
+      kb = kmin - (15 - (kmax - kmin)) / 2;
+      kb = kb < 1 ? 1 : (kb > 48 ? 48 : kb);
+#else
     if (emin >= 1 && emax <= 2046 && kmax - kmin <= 12 && kmax > kmin) {
       kb = kmin - (15 - (kmax - kmin)) / 2;
       kb = kb < 0 ? 0 : (kb > 48 ? 48 : kb);
+#endif
       // exponent fields of the window's slots; 2047 (Inf/NaN) is never inside
       // (a window at the top, kb = 48, would otherwise reach it)
       const uint32_t elo = static_cast<uint32_t>(kb) * 32u, ehi = min(elo + 511u, 2046u);
       any = true;
+#if EXSUM_W_PLANES == 2
+      zero_w2(smem, warp, lane);
+      __syncwarp();
+      const WLane2 a = lane_view_w2(smem, warp, lane);
+      // fit = 2 hi - (elo << 21) <= lim  <=>  elo <= e <= ehi
+      const uint32_t neg_elo21 = 0u - (elo << 21), lim = ((ehi - elo + 1u) << 21) - 1u;
+      int norm_count = 0;
+      long long v = vb;
+      for (; v < ve; v += kWStep) {
+        const long long nv = v + kWStep;
+        prefetch_l2_lane0<kWV>(X4, v + (kPrefetchBatches + 1) * kWStep, ve, lane);
+        uint32_t fmax = 0;
+#pragma unroll
+        for (int u = 0; u < kWV; ++u) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            fmax = max(fmax, add_w2<false>(a, b.w[u][2 * q], b.w[u][2 * q + 1], neg_elo21));
+          const long long vec = nv + u * 32 + lane;
+          if (vec < ve) {
+            load_vec<kWV, kSum>(b, u, X4, X4, vec);
+          } else {
+            zero_vec<kWV, kSum>(b, u);
+          }
+        }
+        if (__builtin_expect(__any_sync(0xffffffffu, fmax > lim), 0)) {
+          // remove this batch again (same planes and slots) and leave the rest
+          // to the full kernel
+#pragma unroll 1
+          for (int u = 0; u < kWV; ++u) {
+            uint32_t t[8];
+            ldg256(X4 + 4 * (v + u * 32 + lane), t);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) add_w2<true>(a, t[2 * q], t[2 * q + 1], neg_elo21);
+          }
+          break;
+        }
+        if (++norm_count >= kWNormEvery) {
+          normalize_w2(a, kb);
+          norm_count = 0;
+        }
+      }
+      resume = g0 + 4ull * static_cast<unsigned long long>(v);
+      auto scalars = [&](unsigned long long p0, unsigned long long p1) -> unsigned long long {
+        for (unsigned long long p = p0; p < p1; p += 32) {
+          const unsigned long long t = p + static_cast<unsigned long long>(lane);
+          const unsigned long long bits =
+              t < p1 ? __ldg(reinterpret_cast<const unsigned long long *>(x) + t) : 0ull;
+          const uint32_t hi = static_cast<uint32_t>(bits >> 32);
+          if (!__all_sync(0xffffffffu, t >= p1 || 2u * hi + neg_elo21 <= lim)) return p;
+          if (++norm_count >= kWNormEvery) {
+            normalize_w2(a, kb);
+            norm_count = 0;
+          }
+          if (t < p1) add_w2<false>(a, static_cast<uint32_t>(bits), hi, neg_elo21);
+        }
+        return p1;
+      };
+#else
       {  // clear this warp's window
         uint4 *p = reinterpret_cast<uint4 *>(wsm);
 #pragma unroll 4
@@ -1796,6 +2039,7 @@ exsum_wsum_kernel(const double *__restrict__ x, unsigned long long n, Workspace 
         }
         return p1;
       };
+#endif
       if (v == ve) {
         if (w == 0) head_left = scalars(0, g0);
         if (w == W - 1)
@@ -1806,7 +2050,11 @@ exsum_wsum_kernel(const double *__restrict__ x, unsigned long long n, Workspace 
   // the previous grid in the stream may still read the workspace and the jobs
   asm volatile("griddepcontrol.wait;" ::: "memory");
   if (any) {
+#if EXSUM_W_PLANES == 2
+    const long long c = warp_chunks_w2(smem, warp, lane, kb);
+#else
     const long long c = warp_chunks_w(wsm, lane, kb);
+#endif
     if (lane <= 18 && c) atomicAdd(&ws->chunk[kb + lane], static_cast<unsigned long long>(c));
   }
   if (lane == 0) {

@@ -45,7 +45,8 @@ VARIANTS = {
     "il0": ("EXSUM_INTERLEAVE=0",),
     "nodisp": ("EXSUM_UNIFORM_DISPATCH=0",),
     "onephase": ("EXSUM_TWO_PHASE=0",),
-    "wimad": ("EXSUM_W_XOR_IMAD=1",),
+    "wimad": ("EXSUM_W_XOR_IMAD=1", "EXSUM_W_PLANES=1"),
+    "oneplane": ("EXSUM_W_PLANES=1",),
     "v7": ("EXSUM_VEC_PER_LANE=7",),
     "seg8": ("EXSUM_SEG_VEC=8",),
     "segtail2": ("EXSUM_SEG_TAIL=2",),

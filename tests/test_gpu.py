@@ -579,6 +579,12 @@ def test_two_phase_large_sums(cuda, checker):
     top = (1.0 + rng.random(n)) * np.exp2(rng.integers(1700, 1900, n).astype(np.float64) - 1023.0)
     top[rng.integers(0, n, 4)] = [np.inf, -np.inf, np.nan, 1e308]
     cases.append(("top-window", top))
+    # windows at the bottom: exponent fields 40-300 (window from slot 1; the
+    # two-plane window holds normal terms only) and 20-200 (slot 0: no window)
+    for tag, (e0, e1) in (("bottom-window", (40, 300)), ("slot0", (20, 200))):
+        low = (1.0 + rng.random(n)) * np.exp2(rng.integers(e0, e1, n).astype(np.float64) - 1023.0)
+        low *= np.where(rng.random(n) < 0.5, -1.0, 1.0)
+        cases.append((tag, low))
     del x
     for tag, arr in cases:
         for off in (0, 1):
