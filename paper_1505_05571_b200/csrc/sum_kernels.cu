@@ -200,8 +200,13 @@ __device__ __forceinline__ uint32_t exponent_field(uint32_t hi) { return (hi >> 
 
 // ------------------------------------------------------ lane accumulators
 
+#ifndef EXSUM_RIPPLE
+#define EXSUM_RIPPLE 0  // lane accumulators as two unsigned planes of 32-bit words with immediate
+                        // carry ripple (536 B per lane, 12 warps per SM) instead of 66 signed
+                        // 96-bit slots with deferred carries (792 B per lane, 8 warps per SM)
+#endif
 #ifndef EXSUM_WARPS
-#define EXSUM_WARPS 8  // warps per CTA (one CTA per SM)
+#define EXSUM_WARPS (EXSUM_RIPPLE ? 12 : 8)  // warps per CTA (one CTA per SM)
 #endif
 #ifndef EXSUM_SLOTS
 #define EXSUM_SLOTS 66  // 65: one carry-only slot (fits a 9th warp in shared memory)
@@ -212,9 +217,19 @@ constexpr int kSlots = EXSUM_SLOTS;  // slots 0..63 take terms (e' >> 5), the re
 static_assert(kSlots == 65 || kSlots == 66, "slot count");
 constexpr int kLPlane = kSlots * 32 * 4;
 constexpr int kHPlane = kSlots * 32 * 8;
+#if EXSUM_RIPPLE
+// Two warps share a region of kChunks rows of 512 B: row r = word r (weight
+// 2^(32 r - 1075)) of four planes, [warp & 1][sign][lane] x 4 B.
+static_assert(kWarps % 2 == 0, "warps pair up");
+constexpr int kRowBytes = 512;
+constexpr int kPairSmem = kChunks * kRowBytes;          // 34,304 B
+constexpr int kAccSmem = (kWarps / 2) * kPairSmem;      // 205,824 B (12 warps)
+#else
 constexpr int kWarpSmem = kLPlane + kHPlane;            // 25,344 B
+constexpr int kAccSmem = kWarps * kWarpSmem;
+#endif
 constexpr int kScratch = kWarps * kChunks * 8;          // per-warp chunk rows
-constexpr int kSmem = kWarps * kWarpSmem + kScratch;    // 207,040 B (8 warps, 66 slots)
+constexpr int kSmem = kAccSmem + kScratch;              // 207,040 B (8 warps, 66 slots)
 constexpr int kPrefetchBatches = EXSUM_PREFETCH_BATCHES;
 constexpr int kUniformBackoff = EXSUM_UNIFORM_BACKOFF;
 
@@ -251,7 +266,37 @@ struct Lane {
   uint32_t hoff;
   uint32_t two;   // 2 and 128, opaque to ptxas: keeps the address arithmetic
   uint32_t c128;  // IMADs on the FMA pipe instead of LEAs on the ALU pipe
+  uint32_t one;   // EXSUM_RIPPLE: 1, opaque likewise (L: word 0 of the positive plane,
+                  // word r at L[128 r], the negative plane 32 words above; H unused)
 };
+
+#if EXSUM_RIPPLE
+__device__ __forceinline__ unsigned char *warp_base(unsigned char *smem, int warp) {
+  return smem + (warp >> 1) * kPairSmem + (warp & 1) * 256;
+}
+
+__device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
+  Lane v;
+  v.L = reinterpret_cast<uint32_t *>(warp_smem) + lane;
+  v.H = nullptr;
+  v.sl = static_cast<uint32_t>(__cvta_generic_to_shared(v.L));
+  v.hoff = 0u;
+  v.one = (blockDim.x >> 30) + 1u;
+  v.two = v.one + v.one;
+  v.c128 = v.two * 64u;
+  return v;
+}
+
+// Zero one warp's two planes: 256 contiguous bytes in each of the 67 rows.
+__device__ __forceinline__ void zero_warp(unsigned char *warp_smem, int lane) {
+#pragma unroll 8
+  for (int r = 0; r < kChunks; ++r)
+    *reinterpret_cast<uint2 *>(warp_smem + r * kRowBytes + lane * 8) = make_uint2(0u, 0u);
+}
+#else
+__device__ __forceinline__ unsigned char *warp_base(unsigned char *smem, int warp) {
+  return smem + warp * kWarpSmem;
+}
 
 __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
   Lane v;
@@ -272,6 +317,8 @@ __device__ __forceinline__ void zero_warp(unsigned char *warp_smem, int lane) {
   for (int i = lane; i < n16; i += 32) p[i] = make_uint4(0, 0, 0, 0);
 }
 
+
+#endif
 
 // The term as three 32-bit words of its complemented, shifted significand
 // (u2:u1:u0 = s ? ~(m << sh) : m << sh; a negative term's +1 is the carry-in
@@ -304,6 +351,172 @@ __device__ __forceinline__ void decode96(uint32_t lo, uint32_t hi, uint32_t e, u
   asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mx), "r"(s), "r"(ep));
 }
 
+#define EXSUM_RMW_LD "ld.shared.u32 l, [%0];\n\tld.shared.v2.u32 {h0, h1}, [%1];\n\t"
+#define EXSUM_RMW_ST "st.shared.u32 [%0], l;\n\tst.shared.v2.u32 [%1], {h0, h1};\n\t}"
+
+#if EXSUM_RIPPLE
+// ---- two unsigned planes of 32-bit words, carries rippled at once ----
+// A lane's sum is P - N, each plane an unsigned 2144-bit integer in 67 words
+// (word r of weight 2^(32 r - 1075): the reference's chunk weight).  A term adds
+// its magnitude m << (e' & 31) (three words) to words e' >> 5 .. + 2 of its
+// sign's plane; a carry out of the third word (probability ~2^-12 per term) is
+// rippled upward right after the vector's four terms.  Planes only grow, so the
+// ripple is amortised O(1) for any input (a carry through j all-ones words
+// clears them); there is no carry budget and no renormalisation.  The blind
+// add of an Inf/NaN term (slot 63: words 63..65, word 66 takes the ripple) is
+// cancelled by subtracting the same magnitude from the same plane.
+
+// Shared address of word e >> 5 of the term's plane: PRMT puts the high byte
+// (s << 7 | e >> 4) in byte 1 and its replicated sign in byte 0, so one AND
+// leaves (e >> 5) << 9 | s << 7 = row * 512 + sign * 128.
+__device__ __forceinline__ uint32_t word_addr(const Lane &a, uint32_t hi) {
+  uint32_t r, t, la;
+  asm("prmt.b32 %0, %1, %2, 0x443B;" : "=r"(r) : "r"(hi), "r"(0u));
+  asm("and.b32 %0, %1, 0x7E80;" : "=r"(t) : "r"(r));
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(t), "r"(a.one), "r"(a.sl));
+  return la;
+}
+
+// u2:u1:u0 = m << (e' & 31), e' = max(e, 1), m without the implicit bit for e = 0.
+__device__ __forceinline__ void decode_mag(uint32_t lo, uint32_t hi, uint32_t e, uint32_t &u0,
+                                           uint32_t &u1, uint32_t &u2) {
+  uint32_t ep, d, mhi, mh;
+  asm("max.u32 %0, %1, 1;" : "=r"(ep) : "r"(e));                          // ALU
+  asm("mad.lo.u32 %0, %1, -1, %2;" : "=r"(d) : "r"(e), "r"(ep));           // FMA: 1 iff e == 0
+  asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mhi) : "r"(hi), "r"(0x100000u));
+  asm("mad.lo.u32 %0, %1, -1048576, %2;" : "=r"(mh) : "r"(d), "r"(mhi));   // FMA: drop implicit 1
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(0u), "r"(lo), "r"(ep));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lo), "r"(mh), "r"(ep));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mh), "r"(0u), "r"(ep));
+}
+
+// + 1 at the word at shared address addr, rippling while words wrap to zero.
+__device__ __forceinline__ void ripple_up(uint32_t addr) {
+  uint32_t w;
+#pragma unroll 1
+  do {
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(addr) : "memory");
+    w += 1u;
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(w) : "memory");
+    addr += kRowBytes;
+  } while (w == 0u);
+}
+
+// - 1 likewise (the plane holds at least what is being removed).
+__device__ __forceinline__ void ripple_down(uint32_t addr) {
+  uint32_t w;
+#pragma unroll 1
+  do {
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w) : "r"(addr) : "memory");
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(w - 1u) : "memory");
+    addr += kRowBytes;
+  } while (w == 0u);
+}
+
+// words [la], [la + 512], [la + 1024] += u0, u1, u2; cb = 2 cb + carry out
+__device__ __forceinline__ void words_add(uint32_t la, uint32_t u0, uint32_t u1, uint32_t u2,
+                                          uint32_t &cb) {
+  asm volatile(
+      "{\n\t.reg .u32 w0, w1, w2;\n\t"
+      "ld.shared.u32 w0, [%1];\n\t"
+      "ld.shared.u32 w1, [%1+512];\n\t"
+      "ld.shared.u32 w2, [%1+1024];\n\t"
+      "add.cc.u32 w0, w0, %2;\n\t"
+      "addc.cc.u32 w1, w1, %3;\n\t"
+      "addc.cc.u32 w2, w2, %4;\n\t"
+      "addc.u32 %0, %0, %0;\n\t"
+      "st.shared.u32 [%1], w0;\n\t"
+      "st.shared.u32 [%1+512], w1;\n\t"
+      "st.shared.u32 [%1+1024], w2;\n\t}"
+      : "+r"(cb)
+      : "r"(la), "r"(u0), "r"(u1), "r"(u2)
+      : "memory");
+}
+
+// One term of a vector: cb collects the carries (bit 3 - q for term q of 4).
+__device__ __forceinline__ void add_term_cb(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e,
+                                            uint32_t &cb) {
+  uint32_t u0, u1, u2;
+  decode_mag(lo, hi, e, u0, u1, u2);
+  words_add(word_addr(a, hi), u0, u1, u2, cb);
+}
+
+// The carries of a vector's four terms (cold).
+__device__ __forceinline__ void ripple_fix4(const Lane &a, const uint32_t (&hi)[4], uint32_t cb) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (cb & (8u >> q)) ripple_up(word_addr(a, hi[q]) + 3 * kRowBytes);
+}
+
+__device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
+  uint32_t cb = 0u;
+  add_term_cb(a, lo, hi, e, cb);
+  if (__builtin_expect(cb != 0u, 0)) ripple_up(word_addr(a, hi) + 3 * kRowBytes);
+}
+
+// Remove exactly what add_term added for the term (lo, hi).
+__device__ __forceinline__ void cancel_term(const Lane &a, uint32_t lo, uint32_t hi, uint32_t e) {
+  uint32_t u0, u1, u2, bw;
+  decode_mag(lo, hi, e, u0, u1, u2);
+  const uint32_t la = word_addr(a, hi);
+  asm volatile(
+      "{\n\t.reg .u32 w0, w1, w2;\n\t"
+      "ld.shared.u32 w0, [%1];\n\t"
+      "ld.shared.u32 w1, [%1+512];\n\t"
+      "ld.shared.u32 w2, [%1+1024];\n\t"
+      "sub.cc.u32 w0, w0, %2;\n\t"
+      "subc.cc.u32 w1, w1, %3;\n\t"
+      "subc.cc.u32 w2, w2, %4;\n\t"
+      "subc.u32 %0, 0, 0;\n\t"
+      "st.shared.u32 [%1], w0;\n\t"
+      "st.shared.u32 [%1+512], w1;\n\t"
+      "st.shared.u32 [%1+1024], w2;\n\t}"
+      : "=r"(bw)
+      : "r"(la), "r"(u0), "r"(u1), "r"(u2)
+      : "memory");
+  if (bw != 0u) ripple_down(la + 3 * kRowBytes);
+}
+
+// A signed 96-bit value (a one-slot batch summed in registers) into word k ..
+// k + 2 of the plane of its sign.
+__device__ __forceinline__ void slot_add96(const Lane &a, uint32_t k, uint32_t v0, uint32_t v1,
+                                           uint32_t v2) {
+  const uint32_t neg = static_cast<uint32_t>(static_cast<int32_t>(v2) >> 31);
+  uint32_t m0 = v0 ^ neg, m1 = v1 ^ neg, m2 = v2 ^ neg;
+  asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, 0;\n\taddc.u32 %2, %2, 0;"
+      : "+r"(m0), "+r"(m1), "+r"(m2)
+      : "r"(neg & 1u));
+  const uint32_t la = a.sl + k * kRowBytes + (neg & 128u);
+  uint32_t cb = 0u;
+  words_add(la, m0, m1, m2, cb);
+  if (cb != 0u) ripple_up(la + 3 * kRowBytes);
+}
+
+__device__ __forceinline__ void normalize(const Lane &) {}  // nothing is deferred
+
+// The warp's exact sum as 67 chunk values: chunk r = sum over lanes of
+// P[r] - N[r] (|chunk| < 2^37).  Lane j sums rows j, j + 32, j + 64 with
+// bank-skewed 128-bit reads (the 8 lanes of a wavefront hit 8 bank groups).
+__device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, int lane, long long *row) {
+  __syncwarp();
+#pragma unroll
+  for (int rr = 0; rr < 3; ++rr) {
+    const int r = 32 * rr + lane;
+    if (r < kChunks) {
+      const uint4 *p = reinterpret_cast<const uint4 *>(warp_smem + r * kRowBytes);
+      long long acc = 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int idx = (i + lane) & 15;
+        const uint4 v = p[idx];
+        const long long t = static_cast<long long>(v.x) + v.y + static_cast<long long>(v.z) + v.w;
+        acc += (idx & 8) ? -t : t;
+      }
+      row[r] = acc;
+    }
+  }
+}
+#else
 // Read-modify-write of slot k with a 96-bit two's-complement value (no carry-in).
 __device__ __forceinline__ void slot_add96(const Lane &a, uint32_t k, uint32_t v0, uint32_t v1,
                                            uint32_t v2) {
@@ -399,8 +612,6 @@ __device__ __forceinline__ void add_term(const Lane &a, uint32_t lo, uint32_t hi
   asm("shr.u32 %0, %1, 5;" : "=r"(k) : "r"(ep));
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(k), "r"(a.c128), "r"(a.sl));
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(ha) : "r"(la), "r"(a.two), "r"(a.hoff));
-#define EXSUM_RMW_LD "ld.shared.u32 l, [%0];\n\tld.shared.v2.u32 {h0, h1}, [%1];\n\t"
-#define EXSUM_RMW_ST "st.shared.u32 [%0], l;\n\tst.shared.v2.u32 [%1], {h0, h1};\n\t}"
   asm volatile(
       "{\n\t.reg .u32 l, h0, h1, cf;\n\t"
       EXSUM_RMW_LD
@@ -494,6 +705,8 @@ __device__ __forceinline__ void warp_chunks(unsigned char *warp_smem, int lane, 
     if (c < kChunks) row[c] = v;
   }
 }
+
+#endif  // EXSUM_RIPPLE
 
 // ------------------------------------------------------------- term streams
 
@@ -832,8 +1045,15 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
       emax = max(emax, e[q]);
     }
     if (kGroup && u % G == G - 1) flags |= static_cast<uint32_t>(emax == 0x7FFu) << (u / G);
+#if EXSUM_RIPPLE
+    uint32_t cb = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) add_term_cb(a, lo[q], hi[q], e[q], cb);
+    if (__builtin_expect(cb != 0u, 0)) ripple_fix4(a, hi, cb);
+#else
 #pragma unroll
     for (int q = 0; q < 4; ++q) add_term(a, lo[q], hi[q], e[q]);
+#endif
     const long long vec = nv + u * 32 + lane;
     if (!kGuard || vec < nvec) {
       EXSUM_DCHECK(vec >= 0 && vec < nvec);
@@ -2127,8 +2347,8 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
   __shared__ unsigned long long s_spec[4];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  unsigned char *wsm = smem + warp * kWarpSmem;
-  long long *scratch = reinterpret_cast<long long *>(smem + kWarps * kWarpSmem);
+  unsigned char *wsm = warp_base(smem, warp);
+  long long *scratch = reinterpret_cast<long long *>(smem + kAccSmem);
   // Programmatic dependent launch: let the next sum in the stream start its CTAs
   // on SMs this grid releases (no-op unless launched with EXSUM_SUM_OVERLAP).
   asm volatile("griddepcontrol.launch_dependents;");
@@ -2476,9 +2696,9 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
   extern __shared__ __align__(16) unsigned char smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  long long *rows = reinterpret_cast<long long *>(smem + kWarps * kWarpSmem);
+  long long *rows = reinterpret_cast<long long *>(smem + kAccSmem);
   long long *row = rows + warp * kChunks;
-  unsigned char *wsm = smem + warp * kWarpSmem;
+  unsigned char *wsm = warp_base(smem, warp);
   const Lane a = lane_view(wsm, lane);
   SegmentClaim ca{0u, 0ull, 0ull};
   if (lane == 0)

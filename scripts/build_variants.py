@@ -47,6 +47,8 @@ VARIANTS = {
     "onephase": ("EXSUM_TWO_PHASE=0",),
     "wimad": ("EXSUM_W_XOR_IMAD=1", "EXSUM_W_PLANES=1"),
     "oneplane": ("EXSUM_W_PLANES=1",),
+    "ripple": ("EXSUM_RIPPLE=1",),
+    "ripplev6": ("EXSUM_RIPPLE=1", "EXSUM_VEC_PER_LANE=6", "EXSUM_SEG_VEC=6"),
     "v7": ("EXSUM_VEC_PER_LANE=7",),
     "seg8": ("EXSUM_SEG_VEC=8",),
     "segtail2": ("EXSUM_SEG_TAIL=2",),
