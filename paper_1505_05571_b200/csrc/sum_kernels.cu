@@ -6,13 +6,23 @@
 // split-merge of parallel_exact_sum (vector_ops.cpp:172-186).  See DESIGN.md.
 //
 // Device representation (B200-first, not the reference's): every LANE owns a
-// private fixed-point superaccumulator in shared memory — 66 slots, slot k a
-// signed 96-bit integer of weight 2^(32k - 1075) (the reference's chunk weight)
-// stored as a u32 plane L[k][lane] and an s64 plane H[k][lane] (25.3 KB per
-// warp, 8 warps per SM).  A term (-1)^s m 2^(e' - 1075), e' = max(e, 1), adds
-// m << (e' & 31) (< 2^84) to slot e' >> 5: one conflict-free read-modify-write,
-// no atomics, independent of the exponent distribution.  2^11 of headroom per
-// slot = 2047 terms; each lane renormalises at most every 2016 terms.
+// private fixed-point superaccumulator in shared memory, so a term costs one
+// conflict-free read-modify-write, no atomics, independent of the exponent
+// distribution.  Two layouts:
+//   EXSUM_RIPPLE = 1 (default, round 2): two unsigned planes (positive and
+//     negative terms) of 67 32-bit words, word r of weight 2^(32 r - 1075) (the
+//     reference's chunk weight): 536 B per lane, 12 warps per SM.  A term
+//     (-1)^s m 2^(e' - 1075), e' = max(e, 1), adds m << (e' & 31) (three words)
+//     at word e' >> 5 of plane s; the rare carry out of the third word ripples
+//     upward at once, so there is no carry budget and no renormalisation.
+//   EXSUM_RIPPLE = 0 (round 1): 66 slots, slot k a signed 96-bit integer of
+//     weight 2^(32k - 1075) stored as a u32 plane L[k][lane] and an s64 plane
+//     H[k][lane] (25.3 KB per warp, 8 warps per SM); 2^11 of headroom per slot
+//     = 2047 terms, each lane renormalises at most every 2016 terms.
+// The kernels are latency-bound on the shared read-modify-write chain, so warps
+// per SM are the lever: 8 -> 12 warps took config 3 from 5.84 to 6.34 TB/s and
+// config 5 from 5.44 to 6.09 TB/s at the same ~23.5 instructions per term
+// (profiles/r02_ripple_ab.log, r02_ripple_knobs.log: 10 warps 5.76 / 5.63).
 //
 // Why not the reference's 4096 shared bins: 64-bit shared atomics compile to
 // ATOMS.CAST.SPIN.64 CAS loops on sm_100a, random-bin read-modify-writes cost
@@ -20,7 +30,7 @@
 // without counts or transfers that step measures 0.04-2.0 TB/s
 // (scripts/probes/bins.cu, profiles/r01_probe_bins.log).
 //
-// Per-term cost: 23.9 SASS instructions (14 integer ALU, 5 FMA-pipe IMADs, 4.25
+// Per-term cost: ~23.5 SASS instructions (13 integer ALU, 4 FMA-pipe IMADs, 6
 // LSU) and 6 shared wavefronts.  Loads are 256-bit (LDG.E.EF.ENL2.256),
 // "rolling": a vector's registers are refilled with the next batch's vector
 // right after its four terms are added, with one 8 KB cp.async.bulk L2
@@ -72,6 +82,11 @@
 #include "exsum_core.h"
 #include "exsum_nvtx.h"
 
+#ifndef EXSUM_RIPPLE
+#define EXSUM_RIPPLE 1  // lane accumulators as two unsigned planes of 32-bit words with immediate
+                        // carry ripple (536 B per lane, 12 warps per SM) instead of 66 signed
+                        // 96-bit slots with deferred carries (792 B per lane, 8 warps per SM)
+#endif
 #ifndef EXSUM_VEC_PER_LANE
 #define EXSUM_VEC_PER_LANE 8  // single-sum kernel: 256-bit vectors per lane per batch
 #endif
@@ -97,7 +112,9 @@
                            // prefetch its head into L2 before the current epilogue
 #endif
 #ifndef EXSUM_SEG_SPLIT
-#define EXSUM_SEG_SPLIT 0  // segmented kernel: unguarded full batches + a one-vector tail loop
+#define EXSUM_SEG_SPLIT EXSUM_RIPPLE  // segmented kernel: unguarded full batches + a one-vector tail
+                                     // loop (config 5: +1.1% with the ripple accumulators, r02_ripple_knobs.log;
+                                     // no gain with the slot accumulators, r02_variants_segsplit.log)
 #endif
 #ifndef EXSUM_FP64_DECODE
 #define EXSUM_FP64_DECODE 0  // general path: slot value by FP64 scaling + conversions (idle FP64
@@ -200,11 +217,6 @@ __device__ __forceinline__ uint32_t exponent_field(uint32_t hi) { return (hi >> 
 
 // ------------------------------------------------------ lane accumulators
 
-#ifndef EXSUM_RIPPLE
-#define EXSUM_RIPPLE 0  // lane accumulators as two unsigned planes of 32-bit words with immediate
-                        // carry ripple (536 B per lane, 12 warps per SM) instead of 66 signed
-                        // 96-bit slots with deferred carries (792 B per lane, 8 warps per SM)
-#endif
 #ifndef EXSUM_WARPS
 #define EXSUM_WARPS (EXSUM_RIPPLE ? 12 : 8)  // warps per CTA (one CTA per SM)
 #endif

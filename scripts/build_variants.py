@@ -21,10 +21,10 @@ VARIANTS = {
     "xorimad": ("EXSUM_XOR_LOP=0",),
     "cta132": ("EXSUM_MAX_CTAS=132",),
     "fullgrid": ("EXSUM_OVERLAP_SHORT=0",),
-    "w8s65": ("EXSUM_SLOTS=65",),
-    "w9v8": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9"),
-    "w9v7": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9", "EXSUM_VEC_PER_LANE=7"),
-    "w9v6": ("EXSUM_SLOTS=65", "EXSUM_WARPS=9", "EXSUM_VEC_PER_LANE=6"),
+    "w8s65": ("EXSUM_RIPPLE=0", "EXSUM_SLOTS=65",),
+    "w9v8": ("EXSUM_RIPPLE=0", "EXSUM_SLOTS=65", "EXSUM_WARPS=9"),
+    "w9v7": ("EXSUM_RIPPLE=0", "EXSUM_SLOTS=65", "EXSUM_WARPS=9", "EXSUM_VEC_PER_LANE=7"),
+    "w9v6": ("EXSUM_RIPPLE=0", "EXSUM_SLOTS=65", "EXSUM_WARPS=9", "EXSUM_VEC_PER_LANE=6"),
     "sumloop": ("EXSUM_SUM_SCAN=0",),
     "ldg1": ("EXSUM_LDG_KIND=1",),
     "ldg0": ("EXSUM_LDG_KIND=0",),
@@ -48,6 +48,19 @@ VARIANTS = {
     "wimad": ("EXSUM_W_XOR_IMAD=1", "EXSUM_W_PLANES=1"),
     "oneplane": ("EXSUM_W_PLANES=1",),
     "ripple": ("EXSUM_RIPPLE=1",),
+    "noripple": ("EXSUM_RIPPLE=0",),
+    "rsplit": ("EXSUM_RIPPLE=1", "EXSUM_SEG_SPLIT=1"),
+    "rseg8": ("EXSUM_RIPPLE=1", "EXSUM_SEG_VEC=8"),
+    "rseg6": ("EXSUM_RIPPLE=1", "EXSUM_SEG_VEC=6"),
+    "rv7": ("EXSUM_RIPPLE=1", "EXSUM_VEC_PER_LANE=7"),
+    "rpf2": ("EXSUM_RIPPLE=1", "EXSUM_PREFETCH_BATCHES=2"),
+    "rw10": ("EXSUM_RIPPLE=1", "EXSUM_WARPS=10"),
+    "rsegfix0": ("EXSUM_RIPPLE=1", "EXSUM_SEG_FIX_GROUP=0"),
+    "rv4": ("EXSUM_VEC_PER_LANE=4",),
+    "rv5": ("EXSUM_VEC_PER_LANE=5",),
+    "rseg5": ("EXSUM_SEG_VEC=5",),
+    "rsegahead": ("EXSUM_SEG_AHEAD=1",),
+    "rnosplit": ("EXSUM_SEG_SPLIT=0",),
     "ripplev6": ("EXSUM_RIPPLE=1", "EXSUM_VEC_PER_LANE=6", "EXSUM_SEG_VEC=6"),
     "v7": ("EXSUM_VEC_PER_LANE=7",),
     "seg8": ("EXSUM_SEG_VEC=8",),

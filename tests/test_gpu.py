@@ -552,6 +552,47 @@ def test_uniform_dispatch_mixed_halves(cuda, checker):
             assert list(part.acc.chunk) == [int(c) for c in checker.canonical(h)[0]]
 
 
+def test_carry_ripple_chains(cuda, checker):
+    """Lane accumulators as unsigned planes of 32-bit words (EXSUM_RIPPLE): terms
+    whose significands are all ones or a single bit, at every exponent and both
+    signs, fill words with 0xFFFFFFFF so that later small terms carry through
+    runs of them (ripple_up); huge finite terms around blind-added Inf/NaN make
+    the cancelling subtraction borrow past its three words (ripple_down).
+    Single sums (result, canonical chunks, Inf/NaN state) and segmented sums."""
+    rng = np.random.default_rng(77)
+    n = 2_500_000
+    e = rng.integers(0, 2047, n).astype(np.uint64)
+    kind = rng.integers(0, 4, n)
+    man = np.where(kind == 0, np.uint64(0xFFFFFFFFFFFFF),
+                   np.where(kind == 1, np.uint64(0),
+                            np.where(kind == 2, np.uint64(0xFFFFFFFF00000),
+                                     rng.integers(0, 1 << 52, n).astype(np.uint64))))
+    sign = rng.integers(0, 2, n).astype(np.uint64) << np.uint64(63)
+    wide = (sign | (e << np.uint64(52)) | man).view(np.float64)
+    # one sign only: the positive plane alone, long all-ones runs
+    pos = ((e << np.uint64(52)) | man).view(np.float64)
+    # top slots with specials: words 62..66
+    top = (sign | (rng.integers(1980, 2047, n).astype(np.uint64) << np.uint64(52)) | man).view(np.float64).copy()
+    top[rng.integers(0, n, n // 200)] = np.inf
+    top[rng.integers(0, n, n // 200)] = -np.inf
+    top[rng.integers(0, n, n // 200)] = np.nan
+    # narrow: three adjacent exponents, all-ones significands (carries out of the third word often)
+    nar = (sign | (rng.integers(1054, 1057, n).astype(np.uint64) << np.uint64(52)) |
+           np.uint64(0xFFFFFFFFFFFFF)).view(np.float64)
+    for tag, h in (("wide", wide), ("pos", pos), ("top", top), ("narrow", nar)):
+        fin = h[np.isfinite(h)]
+        for arr in (h, fin[: n // 3]):
+            got, part = dev_sum(to_dev(arr, 1))
+            assert got == bits_of(checker.exact_sum(arr)), tag
+            ch, _, ib, nb = checker.canonical(arr)
+            assert list(part.acc.chunk) == [int(c) for c in ch], tag
+            assert (part.acc.inf_bits, part.acc.nan_bits) == (ib, nb), tag
+    lens = rng.integers(0, 30_000, 300)
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    both = np.concatenate([wide, top])[: int(offs[-1])]
+    _seg_check(checker, to_dev(both, 3), offs, "ripple-seg")
+
+
 def test_two_phase_large_sums(cuda, checker):
     """Plain sums of >= 2^28 terms run a windowed pass (16 warps per SM, a
     16-slot window per warp) and then the full kernel over what it left
