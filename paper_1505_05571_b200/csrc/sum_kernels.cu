@@ -111,6 +111,10 @@
 #define EXSUM_SEG_AHEAD 0  // segmented: claim the next segment at the start of the current one and
                            // prefetch its head into L2 before the current epilogue
 #endif
+#ifndef EXSUM_SEG_PF_NEXT
+#define EXSUM_SEG_PF_NEXT 0  // segmented: L2 prefetch of the next (already claimed) segment's head
+                             // right after the current segment's chunk sums
+#endif
 #ifndef EXSUM_SEG_SPLIT
 #define EXSUM_SEG_SPLIT EXSUM_RIPPLE  // segmented kernel: unguarded full batches + a one-vector tail
                                      // loop (config 5: +1.1% with the ripple accumulators, r02_ripple_knobs.log;
@@ -2772,6 +2776,22 @@ exsum_segmented_kernel(const double *__restrict__ x, const unsigned long long *_
 #endif
     EXSUM_SEG_PHASE(0);
     warp_chunks(wsm, lane, row);
+#if EXSUM_SEG_PF_NEXT && !EXSUM_SEG_AHEAD
+    // the claim has returned by now: start the next segment's first batches
+    // towards L2 while this segment's record is written and the planes cleared
+    if (lane == 0 && ca.s < nseg && ca.e > ca.b) {
+      const unsigned long long hb = ca.b;
+      const unsigned long long he = ca.e - hb > 2ull * 4 * 32 * EXSUM_SEG_VEC
+                                        ? hb + 2ull * 4 * 32 * EXSUM_SEG_VEC
+                                        : ca.e;
+      const uintptr_t p0 = (reinterpret_cast<uintptr_t>(x + hb) + 15) & ~uintptr_t{15};
+      const uintptr_t p1 = reinterpret_cast<uintptr_t>(x + he) & ~uintptr_t{15};
+      if (p1 > p0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0),
+                     "r"(static_cast<uint32_t>(p1 - p0))
+                     : "memory");
+    }
+#endif
     const unsigned long long P = warp_min_u64(sp.P), M = warp_min_u64(sp.M),
                              N = warp_min_u64(sp.N);
     __syncwarp();

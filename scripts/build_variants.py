@@ -59,6 +59,7 @@ VARIANTS = {
     "rv4": ("EXSUM_VEC_PER_LANE=4",),
     "rv5": ("EXSUM_VEC_PER_LANE=5",),
     "rseg5": ("EXSUM_SEG_VEC=5",),
+    "rpfnext": ("EXSUM_SEG_PF_NEXT=1",),
     "rsegahead": ("EXSUM_SEG_AHEAD=1",),
     "rnosplit": ("EXSUM_SEG_SPLIT=0",),
     "ripplev6": ("EXSUM_RIPPLE=1", "EXSUM_VEC_PER_LANE=6", "EXSUM_SEG_VEC=6"),
