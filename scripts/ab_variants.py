@@ -48,9 +48,17 @@ for case in %r:
         r = f(); torch.cuda.synchronize()
         h = int(np.bitwise_xor.reduce(r.cpu().numpy().view(np.uint64)))
     else:
-        cfg = int(case[1]); n = 1_000_000_000 if cfg == 4 else 100_000_000
-        x = torch.empty(n, dtype=torch.float64, device=dev)
-        _lib.call("exsum_cuda_gen", cfg, 1, n, 0, n, x.data_ptr(), st)
+        if case == "n01":      # N(0,1), 1e8 terms: a few slots, mixed signs
+            n = 100_000_000
+            x = torch.randn(n, dtype=torch.float64, device=dev, generator=torch.Generator(dev).manual_seed(1))
+        elif case == "c4s":    # one shard of config 4 split over 8 GPUs
+            n = 125_000_000
+            x = torch.empty(n, dtype=torch.float64, device=dev)
+            _lib.call("exsum_cuda_gen", 4, 1, 1_000_000_000, 0, n, x.data_ptr(), st)
+        else:
+            cfg = int(case[1]); n = 1_000_000_000 if cfg == 4 else 100_000_000
+            x = torch.empty(n, dtype=torch.float64, device=dev)
+            _lib.call("exsum_cuda_gen", cfg, 1, n, 0, n, x.data_ptr(), st)
         res = torch.empty(1, dtype=torch.float64, device=dev)
         part = torch.empty(ops.PARTIAL_BYTES, dtype=torch.uint8, device=dev)
         ws = ops.Workspace(dev)

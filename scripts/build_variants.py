@@ -59,6 +59,8 @@ VARIANTS = {
     "rv4": ("EXSUM_VEC_PER_LANE=4",),
     "rv5": ("EXSUM_VEC_PER_LANE=5",),
     "rseg5": ("EXSUM_SEG_VEC=5",),
+    "rpf0": ("EXSUM_PREFETCH_BATCHES=0",),
+    "rtp27": ("EXSUM_TWO_PHASE_MIN=(1ull<<26)",),
     "rpfnext": ("EXSUM_SEG_PF_NEXT=1",),
     "rsegahead": ("EXSUM_SEG_AHEAD=1",),
     "rnosplit": ("EXSUM_SEG_SPLIT=0",),
