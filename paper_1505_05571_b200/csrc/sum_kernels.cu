@@ -111,6 +111,19 @@
 #define EXSUM_SEG_AHEAD 0  // segmented: claim the next segment at the start of the current one and
                            // prefetch its head into L2 before the current epilogue
 #endif
+#ifndef EXSUM_RIPPLE_FAST0
+#define EXSUM_RIPPLE_FAST0 0  // ripple accumulators: a 256-bit vector with no zero, denormal, Inf or NaN
+                              // in the whole warp (one vote per vector) takes a decode without the
+                              // e = 0 handling and the Inf/NaN watch (18.3 instead of 23.5
+                              // instructions per term on that side); the vote serialises each
+                              // vector: config 5 and N(0,1) -10% in bursts, config 5 +5% held
+                              // (profiles/r02_ripple_fast0.log): off
+#endif
+#ifndef EXSUM_RIPPLE_PIPE
+#define EXSUM_RIPPLE_PIPE 0  // ripple accumulators: decode vector u + 1 before the read-modify-writes
+                             // of vector u (same basic block), so the decode is not exposed after
+                             // each vector's carry test; 0.6-3.5% slower (r02_ripple_fast0.log): off
+#endif
 #ifndef EXSUM_SEG_PF_NEXT
 #define EXSUM_SEG_PF_NEXT 0  // segmented: L2 prefetch of the next (already claimed) segment's head
                              // right after the current segment's chunk sums
@@ -455,6 +468,43 @@ __device__ __forceinline__ void add_term_cb(const Lane &a, uint32_t lo, uint32_t
   uint32_t u0, u1, u2;
   decode_mag(lo, hi, e, u0, u1, u2);
   words_add(word_addr(a, hi), u0, u1, u2, cb);
+}
+
+// A normal term (1 <= e <= 2046): the implicit bit is set and hi >> 20 is the
+// shift (the funnel shifts take it mod 32).
+__device__ __forceinline__ void add_normal_cb(const Lane &a, uint32_t lo, uint32_t hi,
+                                              uint32_t &cb) {
+  uint32_t sh, mh, u0, u1, u2;
+  asm("shr.u32 %0, %1, 20;" : "=r"(sh) : "r"(hi));
+  asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mh) : "r"(hi), "r"(0x100000u));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(0u), "r"(lo), "r"(sh));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lo), "r"(mh), "r"(sh));
+  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mh), "r"(0u), "r"(sh));
+  words_add(word_addr(a, hi), u0, u1, u2, cb);
+}
+
+// 2 hi - 2^21 (mod 2^32) >= 0xFFC00000  <=>  the exponent field is 0 or 2047.
+__device__ __forceinline__ uint32_t normal_fit(const Lane &a, uint32_t hi) {
+  uint32_t f;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(f) : "r"(hi), "r"(a.two), "r"(0u - (1u << 21)));
+  return f;
+}
+
+// A vector's four terms decoded: magnitude words and the shared address.
+struct Dec4 {
+  uint32_t u0[4], u1[4], u2[4], la[4];
+};
+
+__device__ __forceinline__ void decode4(const Lane &a, const uint32_t (&w)[8], Dec4 &d,
+                                        uint32_t &emax) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint32_t lo = w[2 * q], hi = w[2 * q + 1];
+    const uint32_t e = exponent_field(hi);
+    emax = max(emax, e);
+    decode_mag(lo, hi, e, d.u0[q], d.u1[q], d.u2[q]);
+    d.la[q] = word_addr(a, hi);
+  }
 }
 
 // The carries of a vector's four terms (cold).
@@ -1049,10 +1099,69 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
   static_assert(kGroup == 0 || V % kGroup == 0, "groups tile the batch");
   constexpr int G = kGroup ? kGroup : 1;
   uint32_t emax = 0, flags = 0;
+#if EXSUM_RIPPLE && EXSUM_RIPPLE_PIPE
+  {
+    // software-pipelined: vector u + 1 is decoded in the basic block of vector
+    // u's read-modify-writes; emax_n is the Inf/NaN watch of the decoded vector
+    Dec4 d;
+    uint32_t emax_d = 0;
+    decode4(a, b.w[0], d, emax_d);
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      Dec4 n;
+      uint32_t emax_n = 0;
+      if (u + 1 < V) decode4(a, b.w[u + 1], n, emax_n);
+      if (kGroup && u % G == 0) emax = 0;
+      emax = max(emax, emax_d);
+      if (kGroup && u % G == G - 1) flags |= static_cast<uint32_t>(emax == 0x7FFu) << (u / G);
+      uint32_t cb = 0u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) words_add(d.la[q], d.u0[q], d.u1[q], d.u2[q], cb);
+      if (__builtin_expect(cb != 0u, 0)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (cb & (8u >> q)) ripple_up(d.la[q] + 3 * kRowBytes);
+      }
+      const long long vec = nv + u * 32 + lane;
+      if (!kGuard || vec < nvec) {
+        EXSUM_DCHECK(vec >= 0 && vec < nvec);
+        load_vec<V, kOp>(b, u, X4, Y4, vec);
+      } else {
+        zero_vec<V, kOp>(b, u);
+      }
+      d = n;
+      emax_d = emax_n;
+    }
+    return kGroup ? flags : emax;
+  }
+#endif
 #pragma unroll
   for (int u = 0; u < V; ++u) {
     uint32_t lo[4], hi[4], e[4];
     if (kGroup && u % G == 0) emax = 0;
+#if EXSUM_RIPPLE && EXSUM_RIPPLE_FAST0
+    uint32_t cb = 0u;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {  // terms: products already in place (products_in_place)
+      lo[q] = b.w[u][2 * q];
+      hi[q] = b.w[u][2 * q + 1];
+    }
+    const uint32_t fit = max(max(normal_fit(a, hi[0]), normal_fit(a, hi[1])),
+                             max(normal_fit(a, hi[2]), normal_fit(a, hi[3])));
+    if (__builtin_expect(__any_sync(0xffffffffu, fit >= 0xFFC00000u), 0)) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        e[q] = exponent_field(hi[q]);
+        emax = max(emax, e[q]);
+        add_term_cb(a, lo[q], hi[q], e[q], cb);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) add_normal_cb(a, lo[q], hi[q], cb);
+    }
+    if (kGroup && u % G == G - 1) flags |= static_cast<uint32_t>(emax == 0x7FFu) << (u / G);
+    if (__builtin_expect(cb != 0u, 0)) ripple_fix4(a, hi, cb);
+#else
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // terms: products already in place (products_in_place)
       lo[q] = b.w[u][2 * q];
@@ -1061,7 +1170,10 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
       emax = max(emax, e[q]);
     }
     if (kGroup && u % G == G - 1) flags |= static_cast<uint32_t>(emax == 0x7FFu) << (u / G);
-#if EXSUM_RIPPLE
+#endif
+#if EXSUM_RIPPLE && EXSUM_RIPPLE_FAST0
+    // (added above)
+#elif EXSUM_RIPPLE
     uint32_t cb = 0u;
 #pragma unroll
     for (int q = 0; q < 4; ++q) add_term_cb(a, lo[q], hi[q], e[q], cb);

@@ -59,6 +59,9 @@ VARIANTS = {
     "rv4": ("EXSUM_VEC_PER_LANE=4",),
     "rv5": ("EXSUM_VEC_PER_LANE=5",),
     "rseg5": ("EXSUM_SEG_VEC=5",),
+    "rfast0": ("EXSUM_RIPPLE_FAST0=1",),
+    "rpipe": ("EXSUM_RIPPLE_PIPE=1",),
+    "rpipev7": ("EXSUM_RIPPLE_PIPE=1", "EXSUM_VEC_PER_LANE=7"),
     "rpf0": ("EXSUM_PREFETCH_BATCHES=0",),
     "rtp27": ("EXSUM_TWO_PHASE_MIN=(1ull<<26)",),
     "rpfnext": ("EXSUM_SEG_PF_NEXT=1",),
