@@ -28,7 +28,7 @@ def bits(v) -> int:
 
 
 def draw(rng, n):
-    kind = rng.integers(0, 6)
+    kind = rng.integers(0, 8)
     u = rng.integers(0, 1 << 63, n, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, n, dtype=np.uint64)
     if kind == 0:    # every exponent
         x = (u & np.uint64(0x800FFFFFFFFFFFFF)) | (rng.integers(1, 2046, n, dtype=np.uint64) << np.uint64(52))
@@ -45,6 +45,14 @@ def draw(rng, n):
         return v, kind
     elif kind == 4:  # huge magnitudes near overflow
         x = (u & np.uint64(0x800FFFFFFFFFFFFF)) | (rng.integers(2030, 2047, n, dtype=np.uint64) << np.uint64(52))
+    elif kind == 6:  # carry chains: all-ones / single-bit significands at every exponent (ripple_up)
+        man = rng.choice(np.array([0xFFFFFFFFFFFFF, 0, 0xFFFFFFFF00000, 0xFFFFF], dtype=np.uint64), n)
+        x = (u & np.uint64(0x8000000000000000)) | man | (rng.integers(0, 2047, n, dtype=np.uint64) << np.uint64(52))
+    elif kind == 7:  # top words with Inf/NaN among huge all-ones terms (ripple_down on the cancel)
+        x = (u & np.uint64(0x8000000000000000)) | np.uint64(0xFFFFFFFFFFFFF) | (
+            rng.integers(1985, 2047, n, dtype=np.uint64) << np.uint64(52))
+        m = rng.random(n) < 0.01
+        x[m] = np.uint64(0x7FF0000000000000) | (u[m] & np.uint64(0x800FFFFFFFFFFFFF))
     else:            # special-heavy
         x = (u & np.uint64(0x800FFFFFFFFFFFFF)) | (rng.integers(1, 2046, n, dtype=np.uint64) << np.uint64(52))
         m = rng.random(n) < 0.001
