@@ -234,8 +234,12 @@ __device__ __forceinline__ uint32_t exponent_field(uint32_t hi) { return (hi >> 
 
 // ------------------------------------------------------ lane accumulators
 
+#ifndef EXSUM_RIPPLE_TIMING1P
+#define EXSUM_RIPPLE_TIMING1P 0  // TIMING PROBE ONLY (wrong sums): both signs into one plane, four warps
+                                 // per row region, so 16 warps fit: what a 16-warp layout could reach
+#endif
 #ifndef EXSUM_WARPS
-#define EXSUM_WARPS (EXSUM_RIPPLE ? 12 : 8)  // warps per CTA (one CTA per SM)
+#define EXSUM_WARPS (EXSUM_RIPPLE_TIMING1P ? 16 : EXSUM_RIPPLE ? 12 : 8)  // warps per CTA (one CTA per SM)
 #endif
 #ifndef EXSUM_SLOTS
 #define EXSUM_SLOTS 66  // 65: one carry-only slot (fits a 9th warp in shared memory)
@@ -252,7 +256,7 @@ constexpr int kHPlane = kSlots * 32 * 8;
 static_assert(kWarps % 2 == 0, "warps pair up");
 constexpr int kRowBytes = 512;
 constexpr int kPairSmem = kChunks * kRowBytes;          // 34,304 B
-constexpr int kAccSmem = (kWarps / 2) * kPairSmem;      // 205,824 B (12 warps)
+constexpr int kAccSmem = (kWarps / (EXSUM_RIPPLE_TIMING1P ? 4 : 2)) * kPairSmem;  // 205,824 B (12 warps)
 #else
 constexpr int kWarpSmem = kLPlane + kHPlane;            // 25,344 B
 constexpr int kAccSmem = kWarps * kWarpSmem;
@@ -301,7 +305,11 @@ struct Lane {
 
 #if EXSUM_RIPPLE
 __device__ __forceinline__ unsigned char *warp_base(unsigned char *smem, int warp) {
+#if EXSUM_RIPPLE_TIMING1P
+  return smem + (warp >> 2) * kPairSmem + (warp & 3) * 128;
+#else
   return smem + (warp >> 1) * kPairSmem + (warp & 1) * 256;
+#endif
 }
 
 __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
@@ -320,7 +328,11 @@ __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
 __device__ __forceinline__ void zero_warp(unsigned char *warp_smem, int lane) {
 #pragma unroll 8
   for (int r = 0; r < kChunks; ++r)
+#if EXSUM_RIPPLE_TIMING1P
+    *reinterpret_cast<uint32_t *>(warp_smem + r * kRowBytes + lane * 4) = 0u;
+#else
     *reinterpret_cast<uint2 *>(warp_smem + r * kRowBytes + lane * 8) = make_uint2(0u, 0u);
+#endif
 }
 #else
 __device__ __forceinline__ unsigned char *warp_base(unsigned char *smem, int warp) {
@@ -401,7 +413,11 @@ __device__ __forceinline__ void decode96(uint32_t lo, uint32_t hi, uint32_t e, u
 __device__ __forceinline__ uint32_t word_addr(const Lane &a, uint32_t hi) {
   uint32_t r, t, la;
   asm("prmt.b32 %0, %1, %2, 0x443B;" : "=r"(r) : "r"(hi), "r"(0u));
+#if EXSUM_RIPPLE_TIMING1P
+  asm("and.b32 %0, %1, 0x7E00;" : "=r"(t) : "r"(r));
+#else
   asm("and.b32 %0, %1, 0x7E80;" : "=r"(t) : "r"(r));
+#endif
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(t), "r"(a.one), "r"(a.sl));
   return la;
 }
