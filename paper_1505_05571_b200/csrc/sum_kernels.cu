@@ -111,19 +111,6 @@
 #define EXSUM_SEG_AHEAD 0  // segmented: claim the next segment at the start of the current one and
                            // prefetch its head into L2 before the current epilogue
 #endif
-#ifndef EXSUM_RIPPLE_FAST0
-#define EXSUM_RIPPLE_FAST0 0  // ripple accumulators: a 256-bit vector with no zero, denormal, Inf or NaN
-                              // in the whole warp (one vote per vector) takes a decode without the
-                              // e = 0 handling and the Inf/NaN watch (18.3 instead of 23.5
-                              // instructions per term on that side); the vote serialises each
-                              // vector: config 5 and N(0,1) -10% in bursts, config 5 +5% held
-                              // (profiles/r02_ripple_fast0.log): off
-#endif
-#ifndef EXSUM_RIPPLE_PIPE
-#define EXSUM_RIPPLE_PIPE 0  // ripple accumulators: decode vector u + 1 before the read-modify-writes
-                             // of vector u (same basic block), so the decode is not exposed after
-                             // each vector's carry test; 0.6-3.5% slower (r02_ripple_fast0.log): off
-#endif
 #ifndef EXSUM_SEG_PF_NEXT
 #define EXSUM_SEG_PF_NEXT 0  // segmented: L2 prefetch of the next (already claimed) segment's head
                              // right after the current segment's chunk sums
@@ -234,12 +221,8 @@ __device__ __forceinline__ uint32_t exponent_field(uint32_t hi) { return (hi >> 
 
 // ------------------------------------------------------ lane accumulators
 
-#ifndef EXSUM_RIPPLE_TIMING1P
-#define EXSUM_RIPPLE_TIMING1P 0  // TIMING PROBE ONLY (wrong sums): both signs into one plane, four warps
-                                 // per row region, so 16 warps fit: what a 16-warp layout could reach
-#endif
 #ifndef EXSUM_WARPS
-#define EXSUM_WARPS (EXSUM_RIPPLE_TIMING1P ? 16 : EXSUM_RIPPLE ? 12 : 8)  // warps per CTA (one CTA per SM)
+#define EXSUM_WARPS (EXSUM_RIPPLE ? 12 : 8)  // warps per CTA (one CTA per SM)
 #endif
 #ifndef EXSUM_SLOTS
 #define EXSUM_SLOTS 66  // 65: one carry-only slot (fits a 9th warp in shared memory)
@@ -256,7 +239,7 @@ constexpr int kHPlane = kSlots * 32 * 8;
 static_assert(kWarps % 2 == 0, "warps pair up");
 constexpr int kRowBytes = 512;
 constexpr int kPairSmem = kChunks * kRowBytes;          // 34,304 B
-constexpr int kAccSmem = (kWarps / (EXSUM_RIPPLE_TIMING1P ? 4 : 2)) * kPairSmem;  // 205,824 B (12 warps)
+constexpr int kAccSmem = (kWarps / 2) * kPairSmem;      // 205,824 B (12 warps)
 #else
 constexpr int kWarpSmem = kLPlane + kHPlane;            // 25,344 B
 constexpr int kAccSmem = kWarps * kWarpSmem;
@@ -305,11 +288,7 @@ struct Lane {
 
 #if EXSUM_RIPPLE
 __device__ __forceinline__ unsigned char *warp_base(unsigned char *smem, int warp) {
-#if EXSUM_RIPPLE_TIMING1P
-  return smem + (warp >> 2) * kPairSmem + (warp & 3) * 128;
-#else
   return smem + (warp >> 1) * kPairSmem + (warp & 1) * 256;
-#endif
 }
 
 __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
@@ -328,11 +307,7 @@ __device__ __forceinline__ Lane lane_view(unsigned char *warp_smem, int lane) {
 __device__ __forceinline__ void zero_warp(unsigned char *warp_smem, int lane) {
 #pragma unroll 8
   for (int r = 0; r < kChunks; ++r)
-#if EXSUM_RIPPLE_TIMING1P
-    *reinterpret_cast<uint32_t *>(warp_smem + r * kRowBytes + lane * 4) = 0u;
-#else
     *reinterpret_cast<uint2 *>(warp_smem + r * kRowBytes + lane * 8) = make_uint2(0u, 0u);
-#endif
 }
 #else
 __device__ __forceinline__ unsigned char *warp_base(unsigned char *smem, int warp) {
@@ -413,11 +388,7 @@ __device__ __forceinline__ void decode96(uint32_t lo, uint32_t hi, uint32_t e, u
 __device__ __forceinline__ uint32_t word_addr(const Lane &a, uint32_t hi) {
   uint32_t r, t, la;
   asm("prmt.b32 %0, %1, %2, 0x443B;" : "=r"(r) : "r"(hi), "r"(0u));
-#if EXSUM_RIPPLE_TIMING1P
-  asm("and.b32 %0, %1, 0x7E00;" : "=r"(t) : "r"(r));
-#else
   asm("and.b32 %0, %1, 0x7E80;" : "=r"(t) : "r"(r));
-#endif
   asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(la) : "r"(t), "r"(a.one), "r"(a.sl));
   return la;
 }
@@ -484,43 +455,6 @@ __device__ __forceinline__ void add_term_cb(const Lane &a, uint32_t lo, uint32_t
   uint32_t u0, u1, u2;
   decode_mag(lo, hi, e, u0, u1, u2);
   words_add(word_addr(a, hi), u0, u1, u2, cb);
-}
-
-// A normal term (1 <= e <= 2046): the implicit bit is set and hi >> 20 is the
-// shift (the funnel shifts take it mod 32).
-__device__ __forceinline__ void add_normal_cb(const Lane &a, uint32_t lo, uint32_t hi,
-                                              uint32_t &cb) {
-  uint32_t sh, mh, u0, u1, u2;
-  asm("shr.u32 %0, %1, 20;" : "=r"(sh) : "r"(hi));
-  asm("lop3.b32 %0, %1, 0xFFFFF, %2, 0xEA;" : "=r"(mh) : "r"(hi), "r"(0x100000u));
-  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u0) : "r"(0u), "r"(lo), "r"(sh));
-  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u1) : "r"(lo), "r"(mh), "r"(sh));
-  asm("shf.l.wrap.b32 %0, %1, %2, %3;" : "=r"(u2) : "r"(mh), "r"(0u), "r"(sh));
-  words_add(word_addr(a, hi), u0, u1, u2, cb);
-}
-
-// 2 hi - 2^21 (mod 2^32) >= 0xFFC00000  <=>  the exponent field is 0 or 2047.
-__device__ __forceinline__ uint32_t normal_fit(const Lane &a, uint32_t hi) {
-  uint32_t f;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(f) : "r"(hi), "r"(a.two), "r"(0u - (1u << 21)));
-  return f;
-}
-
-// A vector's four terms decoded: magnitude words and the shared address.
-struct Dec4 {
-  uint32_t u0[4], u1[4], u2[4], la[4];
-};
-
-__device__ __forceinline__ void decode4(const Lane &a, const uint32_t (&w)[8], Dec4 &d,
-                                        uint32_t &emax) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint32_t lo = w[2 * q], hi = w[2 * q + 1];
-    const uint32_t e = exponent_field(hi);
-    emax = max(emax, e);
-    decode_mag(lo, hi, e, d.u0[q], d.u1[q], d.u2[q]);
-    d.la[q] = word_addr(a, hi);
-  }
 }
 
 // The carries of a vector's four terms (cold).
@@ -1115,69 +1049,10 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
   static_assert(kGroup == 0 || V % kGroup == 0, "groups tile the batch");
   constexpr int G = kGroup ? kGroup : 1;
   uint32_t emax = 0, flags = 0;
-#if EXSUM_RIPPLE && EXSUM_RIPPLE_PIPE
-  {
-    // software-pipelined: vector u + 1 is decoded in the basic block of vector
-    // u's read-modify-writes; emax_n is the Inf/NaN watch of the decoded vector
-    Dec4 d;
-    uint32_t emax_d = 0;
-    decode4(a, b.w[0], d, emax_d);
-#pragma unroll
-    for (int u = 0; u < V; ++u) {
-      Dec4 n;
-      uint32_t emax_n = 0;
-      if (u + 1 < V) decode4(a, b.w[u + 1], n, emax_n);
-      if (kGroup && u % G == 0) emax = 0;
-      emax = max(emax, emax_d);
-      if (kGroup && u % G == G - 1) flags |= static_cast<uint32_t>(emax == 0x7FFu) << (u / G);
-      uint32_t cb = 0u;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) words_add(d.la[q], d.u0[q], d.u1[q], d.u2[q], cb);
-      if (__builtin_expect(cb != 0u, 0)) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (cb & (8u >> q)) ripple_up(d.la[q] + 3 * kRowBytes);
-      }
-      const long long vec = nv + u * 32 + lane;
-      if (!kGuard || vec < nvec) {
-        EXSUM_DCHECK(vec >= 0 && vec < nvec);
-        load_vec<V, kOp>(b, u, X4, Y4, vec);
-      } else {
-        zero_vec<V, kOp>(b, u);
-      }
-      d = n;
-      emax_d = emax_n;
-    }
-    return kGroup ? flags : emax;
-  }
-#endif
 #pragma unroll
   for (int u = 0; u < V; ++u) {
     uint32_t lo[4], hi[4], e[4];
     if (kGroup && u % G == 0) emax = 0;
-#if EXSUM_RIPPLE && EXSUM_RIPPLE_FAST0
-    uint32_t cb = 0u;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {  // terms: products already in place (products_in_place)
-      lo[q] = b.w[u][2 * q];
-      hi[q] = b.w[u][2 * q + 1];
-    }
-    const uint32_t fit = max(max(normal_fit(a, hi[0]), normal_fit(a, hi[1])),
-                             max(normal_fit(a, hi[2]), normal_fit(a, hi[3])));
-    if (__builtin_expect(__any_sync(0xffffffffu, fit >= 0xFFC00000u), 0)) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        e[q] = exponent_field(hi[q]);
-        emax = max(emax, e[q]);
-        add_term_cb(a, lo[q], hi[q], e[q], cb);
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) add_normal_cb(a, lo[q], hi[q], cb);
-    }
-    if (kGroup && u % G == G - 1) flags |= static_cast<uint32_t>(emax == 0x7FFu) << (u / G);
-    if (__builtin_expect(cb != 0u, 0)) ripple_fix4(a, hi, cb);
-#else
 #pragma unroll
     for (int q = 0; q < 4; ++q) {  // terms: products already in place (products_in_place)
       lo[q] = b.w[u][2 * q];
@@ -1186,10 +1061,7 @@ __device__ __forceinline__ uint32_t batch_rolling(const Lane &a, Batch<V, kOp> &
       emax = max(emax, e[q]);
     }
     if (kGroup && u % G == G - 1) flags |= static_cast<uint32_t>(emax == 0x7FFu) << (u / G);
-#endif
-#if EXSUM_RIPPLE && EXSUM_RIPPLE_FAST0
-    // (added above)
-#elif EXSUM_RIPPLE
+#if EXSUM_RIPPLE
     uint32_t cb = 0u;
 #pragma unroll
     for (int q = 0; q < 4; ++q) add_term_cb(a, lo[q], hi[q], e[q], cb);

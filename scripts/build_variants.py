@@ -59,12 +59,6 @@ VARIANTS = {
     "rv4": ("EXSUM_VEC_PER_LANE=4",),
     "rv5": ("EXSUM_VEC_PER_LANE=5",),
     "rseg5": ("EXSUM_SEG_VEC=5",),
-    "rfast0": ("EXSUM_RIPPLE_FAST0=1",),
-    "rpipe": ("EXSUM_RIPPLE_PIPE=1",),
-    "rpipev7": ("EXSUM_RIPPLE_PIPE=1", "EXSUM_VEC_PER_LANE=7"),
-    "t16v8": ("EXSUM_RIPPLE_TIMING1P=1",),
-    "t16v6": ("EXSUM_RIPPLE_TIMING1P=1", "EXSUM_VEC_PER_LANE=6", "EXSUM_SEG_VEC=6"),
-    "t16v5": ("EXSUM_RIPPLE_TIMING1P=1", "EXSUM_VEC_PER_LANE=5", "EXSUM_SEG_VEC=5"),
     "rpf0": ("EXSUM_PREFETCH_BATCHES=0",),
     "rtp27": ("EXSUM_TWO_PHASE_MIN=(1ull<<26)",),
     "rpfnext": ("EXSUM_SEG_PF_NEXT=1",),
