@@ -90,8 +90,13 @@
 #ifndef EXSUM_VEC_PER_LANE
 #define EXSUM_VEC_PER_LANE 8  // single-sum kernel: 256-bit vectors per lane per batch
 #endif
+#ifndef EXSUM_SQNORM_VEC
+#define EXSUM_SQNORM_VEC 4  // sqnorm kernel: vectors per lane per batch (1e8 U[-1,1): 6130 GB/s; 3: 6214,
+                            // 5: 5811, 8: 4823 — a smaller loop body at 12 warps; r02_products_vec.log)
+#endif
 #ifndef EXSUM_DOT_VEC
-#define EXSUM_DOT_VEC 4  // dot kernel: vectors per lane per batch (x and y each)
+#define EXSUM_DOT_VEC 2  // dot kernel: vectors per lane per batch (x and y each; 2: 6751 / 6640 GB/s
+                         // co-aligned / misaligned, 3: 6697 / 6524, 4: 6592 / 6287; r02_products_vec.log)
 #endif
 #ifndef EXSUM_SEG_VEC
 #define EXSUM_SEG_VEC 7  // segmented kernel: vectors per lane per batch (7: config 5 2.083 -> 2.068 ms
@@ -2343,7 +2348,7 @@ exsum_sum_kernel(const double *__restrict__ x, const double *__restrict__ y, uns
   // the windowed pass did everything and rounded, nothing to do.
   if (jobs && __ldcg(&jobs[2 * njobs]) != 0ull) return;
   // vectors per lane per batch: a dot keeps two arrays' vectors in registers
-  constexpr int V = kOp >= kDot ? EXSUM_DOT_VEC : EXSUM_VEC_PER_LANE;
+  constexpr int V = kOp >= kDot ? EXSUM_DOT_VEC : kOp == kSqnorm ? EXSUM_SQNORM_VEC : EXSUM_VEC_PER_LANE;
   // Independent sums per CTA group (groups > 1 only when emulating ranks in one
   // cooperative launch): this CTA's group, its index and the group's grid size.
   const unsigned gctas = gridDim.x / static_cast<unsigned>(grp.groups);

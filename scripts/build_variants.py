@@ -59,6 +59,11 @@ VARIANTS = {
     "rv4": ("EXSUM_VEC_PER_LANE=4",),
     "rv5": ("EXSUM_VEC_PER_LANE=5",),
     "rseg5": ("EXSUM_SEG_VEC=5",),
+    "sq3": ("EXSUM_SQNORM_VEC=3",),
+    "sq8": ("EXSUM_SQNORM_VEC=8",),
+    "sq5": ("EXSUM_SQNORM_VEC=5",),
+    "dot4": ("EXSUM_DOT_VEC=4",),
+    "dot3": ("EXSUM_DOT_VEC=3",),
     "rpf0": ("EXSUM_PREFETCH_BATCHES=0",),
     "rtp27": ("EXSUM_TWO_PHASE_MIN=(1ull<<26)",),
     "rpfnext": ("EXSUM_SEG_PF_NEXT=1",),
